@@ -1,0 +1,202 @@
+/*
+ * tilefuse — C ABI of the B200-native (sm_100a) fused-collective library.
+ *
+ * This is the drop-in boundary under the reference package's Python primitive
+ * and operator API (overlapsim, arXiv 2605.02953).  Every entry point below
+ * names the reference interface it replaces (path:line relative to
+ * /root/reference/pkg/src/overlapsim/).  Plain pointers and sizes only: no
+ * torch types cross this boundary.  Streams are cudaStream_t passed as void*.
+ *
+ * Status codes (also the Python exception mapping in errors.py):
+ *   0 OK, 1 INVALID_ARG -> ValueError, 2 CONFIG -> ConfigError,
+ *   3 ALLOC -> AllocationError, 4 PROTOCOL -> ProtocolError,
+ *   5 CUDA -> RuntimeError, 6 TIMEOUT -> DeadlockError.
+ * The message for the last failure on the calling thread is tf_last_error().
+ *
+ * Asynchrony: every data-path call is enqueued on the given stream(s) and
+ * returns immediately; argument validation is synchronous.  Device-side spin
+ * timeouts are latched into the team's error word; tf_team_check() reads it.
+ */
+#ifndef TILEFUSE_H_
+#define TILEFUSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_MAX_WORLD 16
+
+enum {
+  TF_OK = 0,
+  TF_ERR_INVALID = 1,
+  TF_ERR_CONFIG = 2,
+  TF_ERR_ALLOC = 3,
+  TF_ERR_PROTOCOL = 4,
+  TF_ERR_CUDA = 5,
+  TF_ERR_TIMEOUT = 6,
+};
+
+enum { TF_DTYPE_BF16 = 0, TF_DTYPE_F32 = 1 };
+enum { TF_REDUCE_RING = 0, TF_REDUCE_ASCENDING = 1 };
+/* phases of a per-rank collective call */
+enum { TF_PHASE_PRE = 1, TF_PHASE_MAIN = 2, TF_PHASE_POST = 4, TF_PHASE_ALL = 7 };
+
+typedef struct tf_team tf_team;
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* tf_last_error(void);
+/* Library version / build string. */
+const char* tf_version(void);
+
+/* ------------------------------------------------------------------ tile order
+ * Host-side tile tables, bit-identical to the reference swizzles.
+ * tf_tile_map: entry j = row tile computed at step j.
+ *   mode 0 = gather  (ag_gemm_tile_map,  swizzle.py:178-180, 144-175, 109-141)
+ *   mode 1 = scatter (gemm_rs_tile_map,  swizzle.py:183-185)
+ * tf_swizzle_2d: grouped order (swizzle_2d, swizzle.py:76-88).
+ */
+int tf_tile_map(int64_t m, int rank, int world, int nnodes, int block_m, int mode,
+                int32_t* out, int64_t out_len);
+int tf_swizzle_2d(int64_t pid, int64_t num_pid_m, int64_t num_pid_n, int group_m,
+                  int64_t* pid_m, int64_t* pid_n);
+/* MoE dynamic schedule (swizzle_ag_moe, swizzle.py:225-286).  counts is
+ * [world, n_experts] row-major.  Output arrays are length >= *ntiles; call
+ * with out arrays NULL to query ntiles. */
+int tf_moe_schedule(const int64_t* counts, int world, int n_experts, int rank, int local_world,
+                    int block_m, int64_t* ntiles, int64_t* expert_id, int64_t* tiled_m,
+                    int64_t* segment_start, int64_t* segment_end, int64_t* stage);
+
+/* ------------------------------------------------------------------ team / heap
+ * Replaces SymmetricHeap (shmem.py:87-165).  A team is `world` PEs, each with a
+ * symmetric data region of heap_bytes and signal_slots uint64 flags.
+ *
+ * tf_team_create_local: all PEs live in this process.  devices[pe] is the CUDA
+ *   device of PE pe; devices may repeat (several PEs on one GPU: the
+ *   single-device emulation used for parity tests when fewer GPUs exist).
+ * tf_team_create_ipc: one PE per process (torchrun).  Allocates this rank's
+ *   region; exchange tf_team_export_handle() blobs out of band (the Python side
+ *   uses torch.distributed) and call tf_team_open_peers() with all of them.
+ */
+int tf_team_create_local(int world, const int* devices, size_t heap_bytes, size_t signal_slots,
+                         tf_team** out);
+int tf_team_create_ipc(int world, int rank, int device, size_t heap_bytes, size_t signal_slots,
+                       tf_team** out);
+int tf_team_export_handle(tf_team* t, void* blob, size_t blob_len); /* blob_len >= 128 */
+int tf_team_open_peers(tf_team* t, const void* blobs, size_t blob_len);
+int tf_team_destroy(tf_team* t);
+int tf_team_world(tf_team* t, int* world);
+int tf_team_device(tf_team* t, int pe, int* device);
+/* Reads and clears the device error word; TF_ERR_TIMEOUT if a spin timed out. */
+int tf_team_check(tf_team* t);
+
+/* alloc (shmem.py:109-121): identical offset on every PE, bump allocator. */
+int tf_heap_alloc(tf_team* t, size_t nbytes, size_t align, uint64_t* offset);
+/* alloc_signals (shmem.py:132-139). */
+int tf_signal_alloc(tf_team* t, size_t nslots, uint64_t* base);
+/* symm_at / remote_ptr / view (shmem.py:143-165): device pointer of PE pe's copy. */
+int tf_heap_ptr(tf_team* t, int pe, uint64_t offset, void** ptr);
+int tf_signal_ptr(tf_team* t, int pe, uint64_t slot, uint64_t** ptr);
+/* sig_view (shmem.py:155-157): synchronous copy of n slots to host. */
+int tf_signal_read(tf_team* t, int pe, uint64_t base, size_t n, uint64_t* host_out);
+/* zero n slots of PE pe (stream-ordered). */
+int tf_signal_reset(tf_team* t, int pe, uint64_t base, size_t n, void* stream);
+
+/* ------------------------------------------------------------------ one-sided ops
+ * Host-initiated, stream-ordered (copy engine where the driver uses one).
+ * putmem / getmem (shmem.py:239-251), putmem_signal (shmem.py:301-310):
+ * the signal on to_pe lands after the payload (release ordering). */
+int tf_putmem(tf_team* t, int to_pe, uint64_t dst_off, const void* src, size_t nbytes,
+              void* stream);
+int tf_getmem(tf_team* t, int from_pe, uint64_t src_off, void* dst, size_t nbytes, void* stream);
+int tf_putmem_signal(tf_team* t, int to_pe, uint64_t dst_off, const void* src, size_t nbytes,
+                     uint64_t sig_slot, uint64_t value, int op_add, void* stream);
+/* st / notify / atomic_add on a signal slot of PE pe (shmem.py:174-194). */
+int tf_signal_op(tf_team* t, int pe, uint64_t slot, uint64_t value, int op_add, void* stream);
+/* wait (shmem.py:208-235): stream waits until all n slots >= value. */
+int tf_signal_wait(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, void* stream);
+/* barrier_all (shmem.py:319-322), split so a single host thread can drive
+ * several PEs that share one stream: arrive, then wait. */
+int tf_barrier_arrive(tf_team* t, int rank, void* stream);
+int tf_barrier_wait(tf_team* t, int rank, void* stream);
+int tf_barrier_all(tf_team* t, int rank, void* stream);
+
+/* ------------------------------------------------------------------ GEMM tile
+ * Core GEMM (the tile body of ag_gemm.py:93-94 / gemm_rs.py:123): persistent,
+ * warp-specialised tcgen05 kernel, C[m,n] = sum_k A[m,k] * B[n,k], bf16 inputs,
+ * fp32 accumulation in TMEM, bf16 or fp32 output.  Tile order: linear step ->
+ * swizzle_2d(group_m) -> tile_map[pid_m] (ag_gemm.py:81-84). */
+typedef struct tf_gemm_args {
+  const void* a; /* [m, k] bf16, row stride lda elements (lda*2 % 16 == 0) */
+  const void* b; /* [n, k] bf16, row stride ldb elements */
+  void* c;       /* [m, n] out_dtype, row stride ldc elements */
+  int64_t m, n, k, lda, ldb, ldc;
+  int32_t out_dtype;   /* TF_DTYPE_BF16 or TF_DTYPE_F32 */
+  int32_t block_m;     /* 128 (tensor-core tile rows) */
+  int32_t block_n;     /* 128 or 256 */
+  int32_t block_k;     /* 64 */
+  int32_t group_m;     /* swizzle_2d group */
+  int32_t num_gemm_sms;/* persistent CTAs; 0 = all SMs (minus num_comm_sms) */
+  int32_t num_comm_sms;/* CTAs left free for reduce/pack kernels */
+  int32_t swizzle;     /* 1 = apply the gather/scatter tile map */
+  int32_t fuse_scatter;/* gemm_rs only; 1 = epilogue stores into owners' slots */
+  int32_t reduce_order;/* TF_REDUCE_* */
+  const int32_t* tile_map; /* optional device [ceil(m/block_m)] table; NULL = identity */
+} tf_gemm_args;
+
+int tf_gemm(const tf_gemm_args* args, void* stream);
+
+/* ------------------------------------------------------------------ fused collectives
+ * AllGather+GEMM (ag_gemm.py:20-94).  Per rank: a = local A shard [m/world, k],
+ * b = local B shard [n_local, k], c = [m, n_local].  The team owns the gather
+ * workspace (double-buffered) and arrival flags.  phase selects TF_PHASE_*:
+ *   PRE  = local copy into own workspace slot + arrival flag + barrier arrive
+ *   MAIN = barrier wait + peer pulls (rank+i)%w with per-chunk flags on
+ *          comm_stream, tile GEMM waiting per tile on covering chunks on stream
+ *   POST = nothing (flags are epoch-valued) unless reset_signals.
+ * args->m is the GATHERED row count. */
+int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
+               void* comm_stream);
+/* GEMM+ReduceScatter (gemm_rs.py:31-338).  Per rank: a = input shard [m, k_local],
+ * b = weight shard [n, k_local], c = output [m/world, n].
+ *   fuse_scatter=1: epilogue stores row-slices into owner slot [rank] and bumps
+ *   per-row-tile arrival counters (gemm_rs.py:135-162); the owner reduces its
+ *   world slots in ascending or ring order in fp32 (gemm_rs.py:325-338).
+ *   fuse_scatter=0: local GEMM + per-segment counters, owner pull-reduce
+ *   (gemm_rs.py:107-132, 177-196).
+ * phases: PRE = barrier arrive; MAIN = barrier wait + GEMM (+ overlapped reduce
+ * on comm_stream when overlap is possible); POST = reduce (if not overlapped)
+ * + counter reset. */
+int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
+               void* comm_stream);
+
+/* ------------------------------------------------------------------ MoE (expert parallel)
+ * Routing (not in the reference; deterministic rule documented in DESIGN.md):
+ * per token top-k of logits (descending, ties to lower expert id), weights =
+ * softmax of the selected logits. */
+int tf_moe_topk(const float* logits, int64_t tokens, int n_experts, int k, int32_t* topk_idx,
+                float* topk_w, void* stream);
+/* Count matrix row for this rank: counts[e] = #(token,slot) routed to e
+ * (the [world, E] routing matrix convention, ag_moe.py:28-33), plus the
+ * per-(token,slot) position inside the rank's expert-sorted chunk. */
+int tf_moe_count(const int32_t* topk_idx, int64_t tokens, int k, int n_experts,
+                 int32_t* counts, int32_t* sorted_pos, void* stream);
+/* Dispatch (EP all-to-all): scatter this rank's token rows to the receive
+ * buffers of the ranks owning each routed expert.  Receive layout on rank d:
+ * expert-major, then source rank, then source order (gather_tokens_by_expert,
+ * oracles.py:38-50).  all_counts is the device [world, E] matrix (int32). */
+int tf_moe_dispatch(tf_team* t, int rank, const void* x, int64_t tokens, int64_t hidden,
+                    const int32_t* topk_idx, int k, int n_experts, const int32_t* all_counts,
+                    const int32_t* sorted_pos, uint64_t recv_off, int phase, void* stream);
+/* Combine: out[t] = sum_j w[t,j] * y_owner[row(t,j)] (fp32, slot order), bf16 out. */
+int tf_moe_combine(tf_team* t, int rank, uint64_t expert_out_off, int64_t hidden,
+                   const int32_t* topk_idx, const float* topk_w, int64_t tokens, int k,
+                   int n_experts, const int32_t* all_counts, const int32_t* sorted_pos,
+                   void* out, int phase, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEFUSE_H_ */

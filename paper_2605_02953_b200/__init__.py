@@ -1,0 +1,29 @@
+"""B200-native (sm_100a) fused collectives behind the overlapsim operator API.
+
+Hot path (BASELINE.json north_star): AllGather+GEMM, GEMM+ReduceScatter and the
+MoE expert-parallel dispatch/combine, on a symmetric-memory runtime with
+device-side flags.  See DESIGN.md.
+"""
+
+from .context import WorkloadContext, WorkloadRun, reduce_visit_order
+from .errors import (AllocationError, BuildError, ConfigError, DeadlockError, ProtocolError,
+                     VerificationError)
+from .topology import LINK_PROFILES, LinkConfig, Topology, build_topology, local_rank_of, node_of
+
+__all__ = [
+    "WorkloadContext", "WorkloadRun", "reduce_visit_order", "AllocationError", "BuildError",
+    "ConfigError", "DeadlockError", "ProtocolError", "VerificationError", "LINK_PROFILES",
+    "LinkConfig", "Topology", "build_topology", "local_rank_of", "node_of",
+    "ag_gemm", "gemm_rs", "gemm", "AllGatherGemm", "GemmReduceScatter", "SymmetricHeap", "Team",
+]
+
+
+def __getattr__(name):
+    # the operator modules import torch + the CUDA library lazily
+    if name in ("ag_gemm", "gemm_rs", "gemm", "AllGatherGemm", "GemmReduceScatter"):
+        from . import kernels
+        return getattr(kernels, name)
+    if name in ("SymmetricHeap", "Team"):
+        from . import shmem
+        return getattr(shmem, name)
+    raise AttributeError(name)

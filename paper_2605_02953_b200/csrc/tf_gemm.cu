@@ -1,0 +1,426 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a — the core tile of the
+// fused collectives.
+//
+//   C[m, n] = sum_k A[m, k] * B[n, k]      (A, B bf16, K-major; fp32 in TMEM)
+//
+// This is the tile body of the reference's workers (ovs/kernels/ag_gemm.py:93-94,
+// gemm_rs.py:123, 151) re-done for Blackwell:
+//   warp 0      TMA producer: per tile, optionally acquire-waits the AllGather
+//               arrival flags of the row chunks the tile covers
+//               (ag_gemm.py:87-90), then streams 128x64 A and BNx64 B boxes
+//               (128-byte swizzle) into a STAGES-deep smem ring.
+//   warp 1      owns TMEM (2 x BN fp32 columns = double-buffered accumulator) and
+//               issues tcgen05.mma (M=128, N=BN, K=16) from one lane.
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns, convert, store.  In
+//               scatter mode each row slice goes straight to its owner's slot
+//               buffer (gemm_rs.py:152-161) and a release-add bumps the owner's
+//               per-row-tile arrival counter.
+// Tile order is the reference's persistent stride (ag_gemm.py:81): CTA s runs
+// steps s, s+grid, ...; each step -> swizzle_2d(group_m) -> tile_map[pid_m].
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "tf_internal.h"
+#include "tf_ptx.cuh"
+
+namespace tf {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
+constexpr int UMMA_K = 16;
+constexpr int kThreads = 192;          // 6 warps
+constexpr int kEpiWarp0 = 2;
+
+struct KParams {
+  int m, n, k;
+  int num_pid_m, num_pid_n, group_m;
+  int num_kb;
+  const int32_t* tile_map;
+  void* c;
+  long long ldc;
+  int vec_ok;                         // 16-byte aligned rows and n % 8 == 0
+  const uint64_t* chunk_flags;
+  unsigned long long epoch;
+  long long rows_per_chunk;
+  int rank, world;
+  long long rows_per_rank;
+  void* peer_slots[kMaxWorld];
+  uint64_t* peer_counts[kMaxWorld];
+  long long slot_ld;
+  unsigned long long* err;
+  unsigned long long timeout_ns;
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (BN >= 256) ? 4 : 6;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kTotal = 1024 /*align slack*/ + kStages * kStageBytes + kBarBytes;
+  static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;
+};
+
+__device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid_m, int& pid_n) {
+  // grouped order, ovs/swizzle.py:76-88
+  const int per_group = p.group_m * p.num_pid_n;
+  const int g = step / per_group;
+  const int first_m = g * p.group_m;
+  const int rows = min(p.num_pid_m - first_m, p.group_m);
+  const int r = step - g * per_group;
+  pid_m = first_m + r % rows;
+  pid_n = r / rows;
+  if (p.tile_map) pid_m = __ldg(p.tile_map + pid_m);
+}
+
+template <int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                      const __grid_constant__ CUtensorMap tmap_b,
+                      const __grid_constant__ KParams p) {
+  using S = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + S::kStages * S::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + S::kStages;
+  uint64_t* tfull_bar = bars + 2 * S::kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = p.num_pid_m * p.num_pid_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, S::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t ready_mask = 0;  // AllGather chunks already observed as arrived
+      for (int step = blockIdx.x; step < num_tiles; step += gridDim.x) {
+        int pid_m, pid_n;
+        tile_coords(p, step, pid_m, pid_n);
+        const int m0 = pid_m * BM;
+        const int n0 = pid_n * BN;
+        if constexpr (AG_WAIT) {
+          // wait(arrival, rank_beg, n) acquire -- ag_gemm.py:87-90
+          const int r1 = min(m0 + BM, p.m) - 1;
+          const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
+          const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
+          bool waited = false;
+          for (int c = c_beg; c <= c_end; ++c) {
+            if (ready_mask & (1u << c)) continue;
+            wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
+                         0x1000000ull | static_cast<unsigned long long>(c));
+            ready_mask |= 1u << c;
+            waited = true;
+          }
+          // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
+          if (waited) fence_proxy_async_global();
+        }
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          tma_load_2d(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
+          tma_load_2d(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int step = blockIdx.x; step < num_tiles; step += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(smem_a + stage * S::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * S::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
+            const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
+        }
+        __syncwarp();
+        if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;          // TMEM lanes [32*quarter, 32*quarter+32)
+    const int row_in_tile = quarter * 32 + lane;
+    int local = 0;
+    for (int step = blockIdx.x; step < num_tiles; step += gridDim.x, ++local) {
+      int pid_m, pid_n;
+      tile_coords(p, step, pid_m, pid_n);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = pid_m * BM + row_in_tile;
+      const bool row_ok = row < p.m;
+      uint8_t* dst_row = nullptr;
+      if (row_ok) {
+        if constexpr (EPI == 0) {
+          dst_row = static_cast<uint8_t*>(p.c) +
+                    (static_cast<long long>(row) * p.ldc) * (OUT_F32 ? 4 : 2);
+        } else {
+          // slot layout at the owner: [world][rows_per_rank][slot_ld], slot = source rank
+          const int owner = static_cast<int>(row / p.rows_per_rank);
+          const long long orow = row - owner * p.rows_per_rank;
+          dst_row = static_cast<uint8_t*>(p.peer_slots[owner]) +
+                    ((p.rank * p.rows_per_rank + orow) * p.slot_ld) * (OUT_F32 ? 4 : 2);
+        }
+      }
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + cc, v);
+        tmem_ld_wait();
+        const int col0 = pid_n * BN + cc;
+        if (!row_ok || col0 >= p.n) continue;
+        if (p.vec_ok && col0 + 32 <= p.n) {
+          if constexpr (OUT_F32) {
+            uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              d[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              d[j] = make_uint4(
+                  pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                  pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                  pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                  pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (col0 + j < p.n) {
+              if constexpr (OUT_F32) {
+                reinterpret_cast<float*>(dst_row)[col0 + j] = __uint_as_float(v[j]);
+              } else {
+                reinterpret_cast<uint16_t*>(dst_row)[col0 + j] =
+                    static_cast<uint16_t>(pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFF);
+              }
+            }
+          }
+        }
+      }
+      // accumulator drained: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if constexpr (EPI == 1) {
+        // publish: every thread's stores are made visible system-wide, the four
+        // epilogue warps meet, then one thread release-adds the owners' counters.
+        fence_sys();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == kEpiWarp0 * 32) {
+          const int r0 = pid_m * BM;
+          const int r1 = min(r0 + BM, p.m) - 1;
+          const int o0 = static_cast<int>(r0 / p.rows_per_rank);
+          const int o1 = static_cast<int>(r1 / p.rows_per_rank);
+          for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + pid_m, 1);
+        }
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, S::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                 int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TF_ERR_INVALID, "cuTensorMapEncodeTiled failed (code " + std::to_string(r) +
+                                    "): rows=" + std::to_string(rows) +
+                                    " cols=" + std::to_string(cols) + " ld=" + std::to_string(ld));
+  return TF_OK;
+}
+
+template <int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
+             cudaStream_t stream) {
+  auto kern = gemm_sm100_kernel<BN, OUT_F32, EPI, AG_WAIT>;
+  static bool attr_done = false;  // per template instance
+  if (!attr_done) {
+    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Smem<BN>::kTotal));
+    attr_done = true;
+  }
+  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ta, tb, kp);
+  TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}
+
+template <int BN>
+int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
+                const GemmLaunch& g, cudaStream_t s) {
+  const bool ag = g.chunk_flags != nullptr;
+  if (g.epilogue == 0) {
+    if (g.out_f32)
+      return ag ? launch_t<BN, true, 0, true>(ta, tb, kp, grid, s)
+                : launch_t<BN, true, 0, false>(ta, tb, kp, grid, s);
+    return ag ? launch_t<BN, false, 0, true>(ta, tb, kp, grid, s)
+              : launch_t<BN, false, 0, false>(ta, tb, kp, grid, s);
+  }
+  if (g.out_f32) return launch_t<BN, true, 1, false>(ta, tb, kp, grid, s);
+  return launch_t<BN, false, 1, false>(ta, tb, kp, grid, s);
+}
+
+}  // namespace
+
+int num_sms_of_current_device() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return n;
+}
+
+int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
+  if (g.m < 0 || g.n < 0 || g.k < 0) return fail(TF_ERR_INVALID, "negative GEMM dimension");
+  if (g.m == 0 || g.n == 0) return TF_OK;
+  if (g.block_n != 128 && g.block_n != 256)
+    return fail(TF_ERR_CONFIG, "block_n must be 128 or 256 on the tcgen05 path");
+  if ((g.lda * 2) % 16 || (g.ldb * 2) % 16)
+    return fail(TF_ERR_INVALID, "A/B row strides must be multiples of 16 bytes (K % 8 == 0)");
+  if ((reinterpret_cast<uintptr_t>(g.a) | reinterpret_cast<uintptr_t>(g.b)) & 15)
+    return fail(TF_ERR_INVALID, "A/B base pointers must be 16-byte aligned");
+  if (g.m > INT32_MAX || g.n > INT32_MAX || g.k > INT32_MAX)
+    return fail(TF_ERR_INVALID, "GEMM dimension exceeds int32");
+  if (g.epilogue == 1 && (g.world < 1 || g.world > kMaxWorld || g.rows_per_rank <= 0))
+    return fail(TF_ERR_INVALID, "scatter epilogue needs 1 <= world <= TF_MAX_WORLD");
+  if (g.chunk_flags && g.m / g.rows_per_chunk + 1 > 32)
+    return fail(TF_ERR_CONFIG, "AllGather wait supports at most 32 chunks");
+  if (g.group_m < 1) return fail(TF_ERR_CONFIG, "group_m must be >= 1");
+
+  KParams kp{};
+  kp.m = static_cast<int>(g.m);
+  kp.n = static_cast<int>(g.n);
+  kp.k = static_cast<int>(g.k);
+  kp.num_pid_m = static_cast<int>((g.m + BM - 1) / BM);
+  kp.num_pid_n = static_cast<int>((g.n + g.block_n - 1) / g.block_n);
+  kp.group_m = g.group_m;
+  kp.num_kb = static_cast<int>((g.k + BK - 1) / BK);
+  kp.tile_map = g.tile_map;
+  kp.c = g.c;
+  kp.ldc = g.epilogue == 1 ? g.slot_ld : g.ldc;
+  const int esz = g.out_f32 ? 4 : 2;
+  const uintptr_t cbase = g.epilogue == 1 ? 0 : reinterpret_cast<uintptr_t>(g.c);
+  bool vec = ((kp.ldc * esz) % 16 == 0) && (g.n % 8 == 0) && (cbase % 16 == 0);
+  if (g.epilogue == 1)
+    for (int r = 0; r < g.world; ++r) vec = vec && (reinterpret_cast<uintptr_t>(g.peer_slots[r]) % 16 == 0);
+  kp.vec_ok = vec ? 1 : 0;
+  kp.chunk_flags = g.chunk_flags;
+  kp.epoch = g.epoch;
+  kp.rows_per_chunk = g.rows_per_chunk > 0 ? g.rows_per_chunk : (g.m > 0 ? g.m : 1);
+  kp.rank = g.rank;
+  kp.world = g.world;
+  kp.rows_per_rank = g.rows_per_rank > 0 ? g.rows_per_rank : g.m;
+  for (int r = 0; r < kMaxWorld; ++r) {
+    kp.peer_slots[r] = g.peer_slots[r];
+    kp.peer_counts[r] = g.peer_counts[r];
+  }
+  kp.slot_ld = g.slot_ld;
+  kp.err = g.err;
+  kp.timeout_ns = g.timeout_ns;
+  if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
+
+  CUtensorMap ta, tb;
+  int rc = make_tmap_2d(&ta, g.a, g.m, g.k, g.lda, BM);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tb, g.b, g.n, g.k, g.ldb, g.block_n);
+  if (rc) return rc;
+
+  const int tiles = kp.num_pid_m * kp.num_pid_n;
+  int grid = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
+  if (grid > tiles) grid = tiles;
+  if (g.block_n == 256) return dispatch_bn<256>(ta, tb, kp, grid, g, stream);
+  return dispatch_bn<128>(ta, tb, kp, grid, g, stream);
+}
+
+}  // namespace tf

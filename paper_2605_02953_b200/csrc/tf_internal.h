@@ -1,0 +1,59 @@
+// Internal declarations shared by the CUDA translation units of libtilefuse.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tilefuse.h"
+
+namespace tf {
+
+constexpr int kMaxWorld = TF_MAX_WORLD;
+
+// Thread-local error text returned by tf_last_error().
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+#define TF_CUDA_TRY(expr)                                                             \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return ::tf::fail(TF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// One launch of the persistent sm_100a GEMM (see tf_gemm.cu).
+struct GemmLaunch {
+  // operands: A [M, K] row-major (lda elems), B [N, K] row-major (ldb elems), bf16
+  const void* a = nullptr;
+  const void* b = nullptr;
+  int64_t m = 0, n = 0, k = 0, lda = 0, ldb = 0;
+  // tiling / order (reference WorkloadContext semantics, ovs/kernels/context.py:18-54)
+  int block_n = 256;
+  int group_m = 8;
+  int num_sms = 0;                   // persistent CTAs (reference num_gemm_sms); 0 = all SMs
+  const int32_t* tile_map = nullptr; // device [num_pid_m] permutation or nullptr
+  // epilogue
+  int epilogue = 0;                  // 0 = store C, 1 = scatter row-slices to owners
+  int out_f32 = 0;                   // 1: fp32 output, 0: bf16 output
+  void* c = nullptr;
+  int64_t ldc = 0;
+  // AllGather consumer waits (chunk_flags[c] >= epoch before reading rows of chunk c)
+  const uint64_t* chunk_flags = nullptr;
+  uint64_t epoch = 0;
+  int64_t rows_per_chunk = 0;
+  // ReduceScatter producer (scatter epilogue)
+  int rank = 0, world = 1;
+  int64_t rows_per_rank = 0;
+  void* peer_slots[kMaxWorld] = {};     // owner's slot buffer base, [world*rows_per_rank, slot_ld]
+  uint64_t* peer_counts[kMaxWorld] = {};// owner's per-row-tile arrival counters
+  int64_t slot_ld = 0;
+  unsigned long long* err = nullptr;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+};
+
+int launch_gemm(const GemmLaunch& g, cudaStream_t stream);
+int num_sms_of_current_device();
+
+}  // namespace tf

@@ -1,0 +1,378 @@
+// Fused collective operators: AllGather+GEMM and GEMM+ReduceScatter.
+//
+// tf_ag_gemm  <- ovs/kernels/ag_gemm.py:20-94
+//   PRE : local A shard -> own workspace slot [rank] (D2D copy fusion), own
+//         arrival flag := epoch, barrier arrive              (ag_gemm.py:59-62)
+//   MAIN: barrier wait; on comm_stream the pull engine copies chunk
+//         (rank+i)%w from the peer's workspace (copy engine over NVLink) and
+//         then stores arrival[src] := epoch (ag_gemm.py:64-69); on `stream`
+//         the persistent tcgen05 GEMM runs the gather-swizzled tile order and
+//         acquire-waits per tile on the covering chunks (ag_gemm.py:72-94).
+//   The workspace is double-buffered by epoch parity so one barrier per call
+//   is enough (a peer can be at most one call behind).
+//
+// tf_gemm_rs  <- ovs/kernels/gemm_rs.py:31-338
+//   fused   : epilogue stores each tile's row slices into the owners' slot
+//             [rank] (gemm_rs.py:135-162) and release-adds the owner's
+//             per-row-tile counter; the owner reduces its `world` slots in fp32
+//             in ascending or ring order once a row tile's counter reaches
+//             world * num_pid_n (gemm_rs.py:325-338).
+//   unfused : tiles land in the producer's own gemm_out; the same counters
+//             (gemm_rs.py:107-132) release the owner's pull-reduce, which
+//             reads the peers' rows directly over NVLink (gemm_rs.py:177-196).
+//   Counters are reset by their owner after the reduce (gemm_rs.py:168-174);
+//   the barrier at the start of the next call orders the reset before any
+//   peer's next increment.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "tf_internal.h"
+#include "tf_ptx.cuh"
+#include "tf_team.h"
+
+namespace tf {
+namespace {
+
+constexpr int kBM = 128;
+
+struct ReduceSrc {
+  const void* src[kMaxWorld];  // row 0 of this owner's block in each source's buffer
+};
+
+// Owner-side reduction of `world` partial row blocks.  Work item = (row tile,
+// 2048-column chunk); waits on the row tile's arrival counter, then sums the
+// sources in `order` in fp32 with 16-byte vector loads.
+template <bool IN_F32>
+__global__ void __launch_bounds__(256) rs_reduce_kernel(
+    ReduceSrc srcs, long long src_ld, int world, int order_ring, int owner, void* out,
+    long long out_ld, int out_f32, long long rows, long long n, long long row0_global,
+    const uint64_t* counters, unsigned long long expected, int first_tile, int ntiles,
+    int col_chunks, unsigned long long timeout_ns, unsigned long long* err) {
+  const int items = ntiles * col_chunks;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int t = item / col_chunks;
+    const int cc = item - t * col_chunks;
+    const int pid_m = first_tile + t;
+    if (counters) {
+      if (threadIdx.x == 0)
+        wait_geq_sys(counters + pid_m, expected, timeout_ns, err, 0x4000000ull | pid_m);
+      __syncthreads();
+    }
+    // rows of this owner covered by global row tile pid_m
+    const long long g0 = max(static_cast<long long>(pid_m) * kBM, row0_global);
+    const long long g1 = min(static_cast<long long>(pid_m + 1) * kBM, row0_global + rows);
+    const long long c0 = static_cast<long long>(cc) * 2048;
+    const long long c1 = min(c0 + 2048, n);
+    const long long width = c1 - c0;
+    const long long vec_per_row = (width + 7) / 8;
+    const long long total = (g1 - g0) * vec_per_row;
+    for (long long v = threadIdx.x; v < total; v += blockDim.x) {
+      const long long r = g0 - row0_global + v / vec_per_row;
+      const long long c = c0 + (v % vec_per_row) * 8;
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      const bool full = c + 8 <= n;
+      for (int i = 0; i < world; ++i) {
+        const int s = order_ring ? (owner + 1 + i) % world : i;
+        if constexpr (IN_F32) {
+          const float* p = static_cast<const float*>(srcs.src[s]) + r * src_ld + c;
+          if (full) {
+            const float4 x0 = *reinterpret_cast<const float4*>(p);
+            const float4 x1 = *reinterpret_cast<const float4*>(p + 4);
+            acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
+            acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j) acc[j] += p[j];
+          }
+        } else {
+          const uint16_t* p = static_cast<const uint16_t*>(srcs.src[s]) + r * src_ld + c;
+          if (full) {
+            const uint4 x = *reinterpret_cast<const uint4*>(p);
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc[2 * j] += __uint_as_float(w[j] << 16);
+              acc[2 * j + 1] += __uint_as_float(w[j] & 0xFFFF0000u);
+            }
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j)
+              acc[j] += __uint_as_float(static_cast<uint32_t>(p[j]) << 16);
+          }
+        }
+      }
+      if (out_f32) {
+        float* o = static_cast<float*>(out) + r * out_ld + c;
+        if (full) {
+          *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+          for (int j = 0; j < 8 && c + j < n; ++j) o[j] = acc[j];
+        }
+      } else {
+        uint16_t* o = static_cast<uint16_t*>(out) + r * out_ld + c;
+        if (full) {
+          *reinterpret_cast<uint4*>(o) =
+              make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                         pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+        } else {
+          for (int j = 0; j < 8 && c + j < n; ++j)
+            o[j] = static_cast<uint16_t>(pack_bf16x2(acc[j], 0.f) & 0xFFFF);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct StreamJoin {
+  // fork `side` from `main` and join back; no-ops when they are the same stream
+  static int fork(cudaStream_t main, cudaStream_t side) {
+    if (main == side) return TF_OK;
+    cudaEvent_t e;
+    TF_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TF_CUDA_TRY(cudaEventRecord(e, main));
+    TF_CUDA_TRY(cudaStreamWaitEvent(side, e, 0));
+    cudaEventDestroy(e);
+    return TF_OK;
+  }
+};
+
+int check_gemm_args(const tf_gemm_args* a) {
+  if (!a) return fail(TF_ERR_INVALID, "args is NULL");
+  if (a->m < 0 || a->n < 0 || a->k < 1) return fail(TF_ERR_INVALID, "bad GEMM shape");
+  if (a->block_m != 0 && a->block_m != kBM)
+    return fail(TF_ERR_CONFIG, "block_m must be 128 on the tcgen05 path");
+  if (a->block_n != 0 && a->block_n != 128 && a->block_n != 256)
+    return fail(TF_ERR_CONFIG, "block_n must be 128 or 256");
+  if (a->block_k != 0 && a->block_k != 64) return fail(TF_ERR_CONFIG, "block_k must be 64");
+  if (a->out_dtype != TF_DTYPE_BF16 && a->out_dtype != TF_DTYPE_F32)
+    return fail(TF_ERR_INVALID, "out_dtype must be TF_DTYPE_BF16 or TF_DTYPE_F32");
+  if (a->num_gemm_sms < 0 || a->num_comm_sms < 0) return fail(TF_ERR_CONFIG, "negative SM count");
+  return TF_OK;
+}
+
+GemmLaunch base_launch(const tf_gemm_args* a) {
+  GemmLaunch g;
+  g.a = a->a;
+  g.b = a->b;
+  g.m = a->m;
+  g.n = a->n;
+  g.k = a->k;
+  g.lda = a->lda ? a->lda : a->k;
+  g.ldb = a->ldb ? a->ldb : a->k;
+  g.block_n = a->block_n ? a->block_n : 256;
+  g.group_m = a->group_m > 0 ? a->group_m : 8;
+  g.tile_map = a->swizzle ? a->tile_map : nullptr;
+  g.out_f32 = a->out_dtype == TF_DTYPE_F32;
+  g.c = a->c;
+  g.ldc = a->ldc ? a->ldc : a->n;
+  return g;
+}
+
+int gemm_grid(const tf_gemm_args* a) {
+  const int sms = num_sms_of_current_device();
+  int g = a->num_gemm_sms > 0 ? a->num_gemm_sms : sms - a->num_comm_sms;
+  if (g < 1) g = 1;
+  if (g > sms) g = sms;
+  return g;
+}
+
+}  // namespace
+}  // namespace tf
+
+using tf::fail;
+
+extern "C" {
+
+int tf_gemm(const tf_gemm_args* args, void* stream) {
+  int rc = tf::check_gemm_args(args);
+  if (rc) return rc;
+  tf::GemmLaunch g = tf::base_launch(args);
+  g.num_sms = tf::gemm_grid(args);
+  return tf::launch_gemm(g, static_cast<cudaStream_t>(stream));
+}
+
+int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
+               void* comm_stream) {
+  if (!t || rank < 0 || rank >= t->world) return fail(TF_ERR_INVALID, "rank out of range");
+  if (!t->is_local(rank)) return fail(TF_ERR_INVALID, "rank is not owned by this process");
+  int rc = tf::check_gemm_args(args);
+  if (rc) return rc;
+  const int w = t->world;
+  if (args->m % w) return fail(TF_ERR_INVALID, "gathered M must divide evenly across ranks");
+  if ((args->k * 2) % 16) return fail(TF_ERR_INVALID, "K must be a multiple of 8 (16-byte rows)");
+  const int64_t mpr = args->m / w;
+  const size_t chunk_bytes = static_cast<size_t>(mpr) * args->k * 2;
+  const std::string key = "ag:" + std::to_string(args->m) + "x" + std::to_string(args->k);
+  tf::Workspace* ws = t->workspace(key, 2 * chunk_bytes * w, 2 * w, &rc);
+  if (!ws) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  auto cs = comm_stream ? static_cast<cudaStream_t>(comm_stream) : s;
+
+  if (phase & TF_PHASE_PRE) {
+    const uint64_t e = ++t->op_epoch[rank];
+    const int par = static_cast<int>(e & 1);
+    uint8_t* own = t->pes[rank].base + ws->data_off + par * chunk_bytes * w;
+    const int64_t lda = args->lda ? args->lda : args->k;
+    TF_CUDA_TRY(cudaMemcpy2DAsync(own + rank * chunk_bytes, args->k * 2, args->a, lda * 2,
+                                  args->k * 2, mpr, cudaMemcpyDefault, s));
+    rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + rank, e, s);
+    if (rc) return rc;
+    rc = tf::team_barrier_arrive(t, rank, s);
+    if (rc) return rc;
+  }
+  if (phase & TF_PHASE_MAIN) {
+    const uint64_t e = t->op_epoch[rank];
+    const int par = static_cast<int>(e & 1);
+    const size_t buf_off = ws->data_off + par * chunk_bytes * w;
+    uint8_t* own = t->pes[rank].base + buf_off;
+    rc = tf::team_barrier_wait(t, rank, s);
+    if (rc) return rc;
+    rc = tf::StreamJoin::fork(s, cs);
+    if (rc) return rc;
+    for (int i = 1; i < w; ++i) {
+      const int src = (rank + i) % w;  // pull order of ag_gemm.py:64-69
+      TF_CUDA_TRY(cudaMemcpyAsync(own + src * chunk_bytes,
+                                  t->pes[src].base + buf_off + src * chunk_bytes, chunk_bytes,
+                                  cudaMemcpyDefault, cs));
+      rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + src, e, cs);
+      if (rc) return rc;
+    }
+    tf::GemmLaunch g = tf::base_launch(args);
+    g.a = own;
+    g.lda = args->k;
+    g.num_sms = tf::gemm_grid(args);
+    g.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
+    g.epoch = e;
+    g.rows_per_chunk = mpr;
+    g.err = t->err_word(rank);
+    g.timeout_ns = t->timeout_ns;
+    rc = tf::launch_gemm(g, s);
+    if (rc) return rc;
+    rc = tf::StreamJoin::fork(cs, s);  // join: next call's comm is ordered after this GEMM
+    if (rc) return rc;
+  }
+  if (phase & TF_PHASE_POST) {
+    // epoch flags need no reset; nothing to do
+  }
+  return TF_OK;
+}
+
+int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
+               void* comm_stream) {
+  if (!t || rank < 0 || rank >= t->world) return fail(TF_ERR_INVALID, "rank out of range");
+  if (!t->is_local(rank)) return fail(TF_ERR_INVALID, "rank is not owned by this process");
+  int rc = tf::check_gemm_args(args);
+  if (rc) return rc;
+  const int w = t->world;
+  if (args->m % w) return fail(TF_ERR_INVALID, "M must divide evenly across ranks");
+  const int64_t mpr = args->m / w;
+  const int64_t n = args->n;
+  const bool f32 = args->out_dtype == TF_DTYPE_F32;
+  const int esz = f32 ? 4 : 2;
+  const int64_t ld = (n + 7) / 8 * 8;  // 16-byte aligned slot rows
+  const int64_t num_pid_m = (args->m + tf::kBM - 1) / tf::kBM;
+  const int bn = args->block_n ? args->block_n : 256;
+  const int64_t num_pid_n = (n + bn - 1) / bn;
+  const bool fused = args->fuse_scatter != 0;
+  // fused: [world][mpr][ld] slots; unfused: gemm_out [m][ld] (same size)
+  const size_t bytes = static_cast<size_t>(args->m) * ld * esz;
+  const std::string key = std::string(fused ? "rsf:" : "rsu:") + std::to_string(args->m) + "x" +
+                          std::to_string(n) + (f32 ? "f" : "h") + ":" + std::to_string(bn);
+  tf::Workspace* ws = t->workspace(key, bytes, static_cast<size_t>(num_pid_m), &rc);
+  if (!ws) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  auto cs = comm_stream ? static_cast<cudaStream_t>(comm_stream) : s;
+  // the reduce may overlap the GEMM only when no other rank shares this device
+  const bool overlap = t->distinct_devices && cs != s;
+
+  auto launch_reduce = [&](cudaStream_t rs) -> int {
+    tf::ReduceSrc srcs{};
+    for (int src = 0; src < w; ++src) {
+      if (fused)
+        srcs.src[src] = t->pes[rank].base + ws->data_off + static_cast<size_t>(src) * mpr * ld * esz;
+      else
+        srcs.src[src] = t->pes[src].base + ws->data_off + static_cast<size_t>(rank) * mpr * ld * esz;
+    }
+    const int64_t first_tile = rank * mpr / tf::kBM;
+    const int64_t last_tile = ((rank + 1) * mpr - 1) / tf::kBM;
+    const int ntiles = static_cast<int>(last_tile - first_tile + 1);
+    const int col_chunks = static_cast<int>((n + 2047) / 2048);
+    const int ldc = static_cast<int>(args->ldc ? args->ldc : n);
+    int grid = args->num_comm_sms > 0 ? args->num_comm_sms * 2 : tf::num_sms_of_current_device();
+    if (!overlap) grid = tf::num_sms_of_current_device();
+    const int items = ntiles * col_chunks;
+    if (grid > items) grid = items;
+    if (grid < 1) grid = 1;
+    const unsigned long long expected = static_cast<unsigned long long>(w) * num_pid_n;
+    const uint64_t* cnt = t->pes[rank].sig + ws->sig_base;
+    if (f32)
+      tf::rs_reduce_kernel<true><<<grid, 256, 0, rs>>>(
+          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 1, mpr, n,
+          rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
+          t->timeout_ns, t->err_word(rank));
+    else
+      tf::rs_reduce_kernel<false><<<grid, 256, 0, rs>>>(
+          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 0, mpr, n,
+          rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
+          t->timeout_ns, t->err_word(rank));
+    TF_CUDA_TRY(cudaGetLastError());
+    // owner resets its counters once consumed (gemm_rs.py:168-174)
+    TF_CUDA_TRY(cudaMemsetAsync(t->pes[rank].sig + ws->sig_base, 0, num_pid_m * sizeof(uint64_t), rs));
+    return TF_OK;
+  };
+
+  if (phase & TF_PHASE_PRE) {
+    rc = tf::team_barrier_arrive(t, rank, s);
+    if (rc) return rc;
+  }
+  if (phase & TF_PHASE_MAIN) {
+    rc = tf::team_barrier_wait(t, rank, s);
+    if (rc) return rc;
+    tf::GemmLaunch g = tf::base_launch(args);
+    g.num_sms = tf::gemm_grid(args);
+    g.epilogue = 1;
+    g.rank = rank;
+    g.world = w;
+    g.rows_per_rank = mpr;
+    g.slot_ld = ld;
+    g.out_f32 = f32;
+    for (int o = 0; o < w; ++o) {
+      uint8_t* slots_o = t->pes[o].base + ws->data_off;
+      if (fused) {
+        g.peer_slots[o] = slots_o;
+      } else {
+        // own gemm_out, biased so that row = o*mpr + orow lands at its natural place
+        uint8_t* own = t->pes[rank].base + ws->data_off;
+        g.peer_slots[o] = own + (static_cast<int64_t>(o) - rank) * mpr * ld * esz;
+      }
+      g.peer_counts[o] = t->pes[o].sig + ws->sig_base;
+    }
+    g.err = t->err_word(rank);
+    g.timeout_ns = t->timeout_ns;
+    if (overlap) {
+      rc = tf::StreamJoin::fork(s, cs);
+      if (rc) return rc;
+      rc = launch_reduce(cs);
+      if (rc) return rc;
+    }
+    rc = tf::launch_gemm(g, s);
+    if (rc) return rc;
+    if (overlap) {
+      rc = tf::StreamJoin::fork(cs, s);
+      if (rc) return rc;
+    }
+  }
+  if (phase & TF_PHASE_POST) {
+    if (!overlap) {
+      rc = launch_reduce(s);
+      if (rc) return rc;
+    }
+  }
+  return TF_OK;
+}
+
+}  // extern "C"

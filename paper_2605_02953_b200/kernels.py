@@ -1,0 +1,413 @@
+"""Fused collective operators behind the reference's operator API.
+
+Drop-in entry points (same names, argument order and errors as the reference):
+  ag_gemm(a_shards, b_shards, ctx)                          ovs/kernels/ag_gemm.py:20
+  gemm_rs(input_shards, weight_shards, ctx,
+          assume_full_mesh_links=True)                      ovs/kernels/gemm_rs.py:31
+All ranks' shards are passed in one call (ag_gemm.py:24-25).  Shards may be
+torch bf16 CUDA tensors (production: bf16 output unless ctx.out_dtype) or the
+reference's numpy float32 / int64 arrays (parity: computed in bf16 with fp32
+accumulation and fp32 output, returned as numpy of the input dtype; int64
+"exact mode" inputs must be bf16-exact integers so results are bit-identical).
+
+Per-rank persistent operators for one-process-per-GPU use (torchrun) and for
+benchmarking: `AllGatherGemm`, `GemmReduceScatter`, and the single-GPU core
+`gemm()`.  Everything runs through libtilefuse; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .context import SUPPORTED_NUMPY, WorkloadContext, WorkloadRun
+from .shmem import SigHandle, SymmetricHeap, Team
+
+BM = 128
+_side_streams: dict[int, torch.cuda.Stream] = {}
+
+
+def side_stream(device: int) -> torch.cuda.Stream:
+    s = _side_streams.get(device)
+    if s is None:
+        with torch.cuda.device(device):
+            s = torch.cuda.Stream(device=device)
+        _side_streams[device] = s
+    return s
+
+
+# ----------------------------------------------------------------- input prep
+class _Prepared:
+    def __init__(self, tensors, kind, np_dtype, k_orig):
+        self.tensors = tensors
+        self.kind = kind          # "torch" | "exact" | "float"
+        self.np_dtype = np_dtype
+        self.k = k_orig
+
+
+def _is_torch(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+def check_dtype(*arrays):
+    """Reference check_dtype (context.py:67-74) extended with torch bf16."""
+    first = arrays[0]
+    if _is_torch(first):
+        for a in arrays:
+            if not _is_torch(a) or a.dtype != torch.bfloat16:
+                raise ValueError(f"unsupported dtype {getattr(a, 'dtype', type(a))}; "
+                                 "torch inputs must be bfloat16")
+            if not a.is_cuda:
+                raise ValueError("torch inputs must be CUDA tensors (there is no CPU path)")
+        return torch.bfloat16
+    dt = np.asarray(first).dtype
+    if dt not in SUPPORTED_NUMPY:
+        raise ValueError(f"unsupported dtype {dt}; use float32 or int64 (exact mode), or torch bfloat16")
+    for a in arrays[1:]:
+        if _is_torch(a) or np.asarray(a).dtype != dt:
+            raise ValueError(f"mixed dtypes: {dt} vs {getattr(a, 'dtype', type(a))}")
+    return dt
+
+
+def _pad_k(t: torch.Tensor, kp: int) -> torch.Tensor:
+    if t.shape[1] == kp and t.stride(1) == 1 and (t.stride(0) * 2) % 16 == 0 and t.data_ptr() % 16 == 0:
+        return t
+    out = torch.zeros((t.shape[0], kp), dtype=t.dtype, device=t.device)
+    out[:, : t.shape[1]] = t
+    return out
+
+
+def _prepare(shards, devices, kp: int) -> _Prepared:
+    dt = check_dtype(*shards)
+    k = shards[0].shape[1]
+    if dt is torch.bfloat16:
+        return _Prepared([_pad_k(s, kp) for s in shards], "torch", None, k)
+    kind = "exact" if dt == np.int64 else "float"
+    out = []
+    for s, dev in zip(shards, devices):
+        arr = np.asarray(s)
+        if kind == "exact" and arr.size and np.abs(arr).max() > 256:
+            raise ValueError("exact mode needs integers with |x| <= 256 (exact in bf16)")
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(torch.bfloat16)
+        t = _pad_k(t, kp) if kp != k else t
+        out.append(t.to(f"cuda:{dev}"))
+    return _Prepared(out, kind, dt, k)
+
+
+def _exact_bound_check(prep_a: _Prepared, prep_b: _Prepared, k: int, extra_terms: int = 1):
+    if prep_a.kind != "exact":
+        return
+    amax = max((float(t.float().abs().max()) for t in prep_a.tensors if t.numel()), default=0.0)
+    bmax = max((float(t.float().abs().max()) for t in prep_b.tensors if t.numel()), default=0.0)
+    if amax * bmax * k * extra_terms >= 2 ** 24:
+        raise ValueError("exact mode: |sum| may exceed 2^24, fp32 accumulation would not be exact")
+
+
+def _finish(out: torch.Tensor, prep: _Prepared):
+    if prep.kind == "torch":
+        return out
+    host = out.float().cpu().numpy()
+    if prep.kind == "exact":
+        return np.rint(host).astype(np.int64)
+    return host.astype(np.float32)
+
+
+def _out_dtype(ctx_out: str | None, prep: _Prepared) -> torch.dtype:
+    if prep.kind != "torch":
+        return torch.float32
+    return torch.float32 if ctx_out == "f32" else torch.bfloat16
+
+
+def _tf_dtype(t: torch.dtype) -> int:
+    return _lib.TF_DTYPE_F32 if t == torch.float32 else _lib.TF_DTYPE_BF16
+
+
+def tile_map_tensor(m: int, rank: int, world: int, nnodes: int, mode: str, device,
+                    block_m: int = BM) -> torch.Tensor:
+    """Gather (mode 'ag_gemm') / scatter ('gemm_rs') map from the C library, on device."""
+    tiles = (m + block_m - 1) // block_m
+    buf = (C.c_int32 * max(tiles, 1))()
+    _lib.call("tf_tile_map", int(m), int(rank), int(world), int(nnodes), int(block_m),
+              0 if mode == "ag_gemm" else 1, buf, tiles)
+    host = np.frombuffer(bytes(buf), dtype=np.int32)[:tiles].copy()
+    return torch.from_numpy(host).to(device)
+
+
+def tile_map_host(m: int, rank: int, world: int, nnodes: int, block_m: int, mode: str) -> np.ndarray:
+    tiles = (m + block_m - 1) // block_m
+    buf = (C.c_int32 * max(tiles, 1))()
+    _lib.call("tf_tile_map", int(m), int(rank), int(world), int(nnodes), int(block_m),
+              0 if mode == "ag_gemm" else 1, buf, tiles)
+    return np.frombuffer(bytes(buf), dtype=np.int32)[:tiles].astype(np.int64)
+
+
+def _args(a, b, c, m, n, k, *, out_dtype, block_n, group_m, num_gemm_sms, num_comm_sms,
+          swizzle, tile_map, fuse_scatter=0, reduce_order="ring", ldc=None) -> _lib.GemmArgs:
+    g = _lib.GemmArgs()
+    g.a = a.data_ptr() if a is not None else None
+    g.b = b.data_ptr() if b is not None else None
+    g.c = c.data_ptr() if c is not None else None
+    g.m, g.n, g.k = int(m), int(n), int(k)
+    g.lda = int(a.stride(0)) if a is not None else int(k)
+    g.ldb = int(b.stride(0)) if b is not None else int(k)
+    g.ldc = int(ldc if ldc is not None else (c.stride(0) if c is not None else n))
+    g.out_dtype = _tf_dtype(out_dtype)
+    g.block_m, g.block_n, g.block_k = BM, int(block_n), 64
+    g.group_m = int(group_m)
+    g.num_gemm_sms = int(num_gemm_sms)
+    g.num_comm_sms = int(num_comm_sms)
+    g.swizzle = 1 if (swizzle and tile_map is not None) else 0
+    g.fuse_scatter = 1 if fuse_scatter else 0
+    g.reduce_order = _lib.TF_REDUCE_RING if reduce_order == "ring" else _lib.TF_REDUCE_ASCENDING
+    g.tile_map = tile_map.data_ptr() if tile_map is not None else None
+    return g
+
+
+def _streams(team: Team, rank: int):
+    dev = team.devices[rank]
+    s = torch.cuda.current_stream(dev)
+    if team.distinct_devices:
+        return s, side_stream(dev)
+    return s, None
+
+
+def _ptr(s) -> int | None:
+    return None if s is None else s.cuda_stream
+
+
+def _drive(team: Team, fn_name: str, per_rank_args: dict, ranks):
+    """Run PRE for all local ranks, then MAIN, then POST (single-process teams)."""
+    for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
+        for r in ranks:
+            dev = team.devices[r]
+            with torch.cuda.device(dev):
+                s, cs = _streams(team, r)
+                _lib.call(fn_name, team.handle, r, C.byref(per_rank_args[r]), phase,
+                          _ptr(s), _ptr(cs))
+
+
+# ----------------------------------------------------------------- core GEMM
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
+         out_dtype: torch.dtype = torch.bfloat16, block_n: int = 256, group_m: int = 8,
+         num_sms: int = 0, tile_map: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """C = A @ B.T on one GPU with the tcgen05 kernel (bf16 in, fp32 accumulate)."""
+    check_dtype(a, b)
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
+        raise ValueError(f"need A [M,K], B [N,K]; got {tuple(a.shape)} and {tuple(b.shape)}")
+    m, k = a.shape
+    n = b.shape[0]
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise ValueError("A and B must be K-contiguous")
+    if out is None:
+        out = torch.empty((m, n), dtype=out_dtype, device=a.device)
+    g = _args(a, b, out, m, n, k, out_dtype=out.dtype, block_n=block_n, group_m=group_m,
+              num_gemm_sms=num_sms, num_comm_sms=0, swizzle=tile_map is not None,
+              tile_map=tile_map)
+    s = stream if stream is not None else torch.cuda.current_stream(a.device)
+    _lib.call("tf_gemm", C.byref(g), s.cuda_stream)
+    return out
+
+
+# ----------------------------------------------------------------- AllGather + GEMM
+def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
+    """Per rank r: C_r = concat(a_0..a_{w-1}) @ b_r.T, shape [M, N_per_rank]."""
+    topo = ctx.topology
+    world = topo.world_size
+    if len(a_shards) != world or len(b_shards) != world:
+        raise ValueError(f"need {world} shards per operand")
+    check_dtype(*a_shards, *b_shards)
+    m_per_rank, k = a_shards[0].shape
+    n_per_rank = b_shards[0].shape[0]
+    for a, b in zip(a_shards, b_shards):
+        if tuple(a.shape) != (m_per_rank, k):
+            raise ValueError(f"ragged A shards: {tuple(a.shape)} vs {(m_per_rank, k)}")
+        if tuple(b.shape) != (n_per_rank, k):
+            raise ValueError(f"B shard must be [N_per_rank, K]-shaped, got {tuple(b.shape)}")
+    m = m_per_rank * world
+    kp = (k + 7) // 8 * 8
+    devices = _devices_for(ctx, a_shards)
+    pa = _prepare(a_shards, devices, kp)
+    pb = _prepare(b_shards, devices, kp)
+    _exact_bound_check(pa, pb, k)
+    odt = _out_dtype(ctx.out_dtype, pa)
+    heap_bytes = 2 * m * kp * 2 + (1 << 20)
+    team = Team(world, devices, heap_bytes, 4 * world + 64)
+    heap = SymmetricHeap(topo, team=team)
+    outs, args, keep = [], {}, []
+    for r in range(world):
+        dev = devices[r]
+        out = torch.empty((m, n_per_rank), dtype=odt, device=f"cuda:{dev}")
+        tm = tile_map_tensor(m, r, world, topo.nnodes, "ag_gemm", f"cuda:{dev}") if ctx.swizzle else None
+        a = pa.tensors[r]
+        args[r] = _args(a, pb.tensors[r], out, m, n_per_rank, kp, out_dtype=odt,
+                        block_n=ctx.hw_block_n, group_m=ctx.group_m,
+                        num_gemm_sms=ctx.num_gemm_sms, num_comm_sms=ctx.num_comm_sms,
+                        swizzle=ctx.swizzle, tile_map=tm)
+        outs.append(out)
+        keep.append(tm)
+    if m_per_rank > 0 and n_per_rank > 0:
+        _drive(team, "tf_ag_gemm", args, range(world))
+    for d in sorted(set(devices)):
+        torch.cuda.synchronize(d)
+    team.check()
+    del keep
+    return WorkloadRun([_finish(o, pa) for o in outs], None, heap, {})
+
+
+# ----------------------------------------------------------------- GEMM + ReduceScatter
+def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
+            assume_full_mesh_links: bool = True) -> WorkloadRun:
+    """Per rank r: rows r of sum_w(input_w @ weight_w.T), shape [M_per_rank, N].
+
+    `assume_full_mesh_links` is accepted for API parity: NVSwitch gives every
+    GPU full bandwidth to every peer, so the ring fallback is never needed."""
+    topo = ctx.topology
+    world = topo.world_size
+    if len(input_shards) != world or len(weight_shards) != world:
+        raise ValueError(f"need {world} shards per operand")
+    check_dtype(*input_shards, *weight_shards)
+    m, k_local = input_shards[0].shape
+    n = weight_shards[0].shape[0]
+    if m % world != 0:
+        raise ValueError(f"M={m} must divide evenly across {world} ranks")
+    for inp, w in zip(input_shards, weight_shards):
+        if tuple(inp.shape) != (m, k_local) or tuple(w.shape) != (n, k_local):
+            raise ValueError("ragged shards")
+    mpr = m // world
+    kp = (k_local + 7) // 8 * 8
+    devices = _devices_for(ctx, input_shards)
+    px = _prepare(input_shards, devices, kp)
+    pw = _prepare(weight_shards, devices, kp)
+    _exact_bound_check(px, pw, k_local, extra_terms=world)
+    odt = _out_dtype(ctx.out_dtype, px)
+    esz = 4 if odt == torch.float32 else 2
+    ld = (n + 7) // 8 * 8
+    heap_bytes = m * ld * esz + (1 << 20)
+    num_pid_m = (m + BM - 1) // BM
+    team = Team(world, devices, heap_bytes, num_pid_m + 64)
+    heap = SymmetricHeap(topo, team=team)
+    outs, args, keep = [], {}, []
+    for r in range(world):
+        dev = devices[r]
+        out = torch.empty((mpr, n), dtype=odt, device=f"cuda:{dev}")
+        tm = tile_map_tensor(m, r, world, topo.nnodes, "gemm_rs", f"cuda:{dev}") if ctx.swizzle else None
+        args[r] = _args(px.tensors[r], pw.tensors[r], out, m, n, kp, out_dtype=odt,
+                        block_n=ctx.hw_block_n, group_m=ctx.group_m,
+                        num_gemm_sms=ctx.num_gemm_sms, num_comm_sms=ctx.num_comm_sms,
+                        swizzle=ctx.swizzle, tile_map=tm, fuse_scatter=ctx.fuse_scatter,
+                        reduce_order=ctx.reduce_order)
+        outs.append(out)
+        keep.append(tm)
+    if mpr > 0 and n > 0:
+        _drive(team, "tf_gemm_rs", args, range(world))
+    for d in sorted(set(devices)):
+        torch.cuda.synchronize(d)
+    team.check()
+    # counters live right after the reserved slots; expose them for hygiene checks
+    handles = {"counters": SigHandle(base=world + 1, nslots=num_pid_m)}
+    return WorkloadRun([_finish(o, px) for o in outs], None, heap, handles)
+
+
+def _devices_for(ctx: WorkloadContext, shards) -> list[int]:
+    if ctx.devices is not None:
+        return [int(d) for d in ctx.devices]
+    if _is_torch(shards[0]):
+        return [s.device.index for s in shards]
+    world = ctx.topology.world_size
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise RuntimeError("no CUDA device: the tilefuse operators have no CPU path")
+    return list(range(world)) if ndev >= world else [0] * world
+
+
+# ----------------------------------------------------------------- persistent per-rank ops
+class AllGatherGemm:
+    """Reusable AllGather+GEMM for a fixed shape over a team.
+
+    For an IPC team (torchrun) call `forward(a_local, b_local, out)`; for a local
+    team pass lists indexed by rank.  The workspace and flags are created once
+    in the team heap; each call is one epoch."""
+
+    def __init__(self, team: Team, m: int, k: int, n_local: int, *, out_dtype=torch.bfloat16,
+                 block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
+                 swizzle: bool = True, nnodes: int = 1):
+        if k % 8:
+            raise ValueError("K must be a multiple of 8")
+        self.team, self.m, self.k, self.n = team, m, k, n_local
+        self.out_dtype = out_dtype
+        self.block_n, self.group_m, self.num_gemm_sms = block_n, group_m, num_gemm_sms
+        self.maps = {r: (tile_map_tensor(m, r, team.world, nnodes, "ag_gemm",
+                                         f"cuda:{team.devices[r]}") if swizzle else None)
+                     for r in team.local_ranks()}
+
+    def _args(self, r, a, b, out):
+        return _args(a, b, out, self.m, self.n, self.k, out_dtype=out.dtype, block_n=self.block_n,
+                     group_m=self.group_m, num_gemm_sms=self.num_gemm_sms, num_comm_sms=0,
+                     swizzle=self.maps[r] is not None, tile_map=self.maps[r])
+
+    def forward(self, a, b, out=None):
+        t = self.team
+        if t.rank is not None:
+            r = t.rank
+            if out is None:
+                out = torch.empty((self.m, self.n), dtype=self.out_dtype, device=a.device)
+            g = self._args(r, a, b, out)
+            s, cs = torch.cuda.current_stream(), side_stream(a.device.index)
+            _lib.call("tf_ag_gemm", t.handle, r, C.byref(g), _lib.PHASE_ALL, s.cuda_stream, cs.cuda_stream)
+            return out
+        outs = out or [torch.empty((self.m, self.n), dtype=self.out_dtype,
+                                   device=f"cuda:{t.devices[r]}") for r in range(t.world)]
+        args = {r: self._args(r, a[r], b[r], outs[r]) for r in range(t.world)}
+        _drive(t, "tf_ag_gemm", args, range(t.world))
+        return outs
+
+    __call__ = forward
+
+
+class GemmReduceScatter:
+    """Reusable fused GEMM+ReduceScatter for a fixed shape over a team."""
+
+    def __init__(self, team: Team, m: int, k_local: int, n: int, *, out_dtype=torch.bfloat16,
+                 block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
+                 num_comm_sms: int = 8, swizzle: bool = True, fuse_scatter: bool = True,
+                 reduce_order: str = "ascending", nnodes: int = 1):
+        if k_local % 8:
+            raise ValueError("K must be a multiple of 8")
+        if m % team.world:
+            raise ValueError("M must divide evenly across ranks")
+        self.team, self.m, self.k, self.n = team, m, k_local, n
+        self.out_dtype = out_dtype
+        self.block_n, self.group_m = block_n, group_m
+        self.num_gemm_sms, self.num_comm_sms = num_gemm_sms, num_comm_sms
+        self.fuse, self.order = fuse_scatter, reduce_order
+        self.maps = {r: (tile_map_tensor(m, r, team.world, nnodes, "gemm_rs",
+                                         f"cuda:{team.devices[r]}") if swizzle else None)
+                     for r in team.local_ranks()}
+
+    def _args(self, r, x, w, out):
+        return _args(x, w, out, self.m, self.n, self.k, out_dtype=out.dtype, block_n=self.block_n,
+                     group_m=self.group_m, num_gemm_sms=self.num_gemm_sms,
+                     num_comm_sms=self.num_comm_sms, swizzle=self.maps[r] is not None,
+                     tile_map=self.maps[r], fuse_scatter=self.fuse, reduce_order=self.order)
+
+    def forward(self, x, w, out=None):
+        t = self.team
+        mpr = self.m // t.world
+        if t.rank is not None:
+            r = t.rank
+            if out is None:
+                out = torch.empty((mpr, self.n), dtype=self.out_dtype, device=x.device)
+            g = self._args(r, x, w, out)
+            s, cs = torch.cuda.current_stream(), side_stream(x.device.index)
+            _lib.call("tf_gemm_rs", t.handle, r, C.byref(g), _lib.PHASE_ALL, s.cuda_stream, cs.cuda_stream)
+            return out
+        outs = out or [torch.empty((mpr, self.n), dtype=self.out_dtype,
+                                   device=f"cuda:{t.devices[r]}") for r in range(t.world)]
+        args = {r: self._args(r, x[r], w[r], outs[r]) for r in range(t.world)}
+        _drive(t, "tf_gemm_rs", args, range(t.world))
+        return outs
+
+    __call__ = forward

@@ -1,0 +1,359 @@
+"""Device symmetric heap: the B200 replacement of ovs/shmem.py:87-473.
+
+`SymmetricHeap` keeps the reference's host-visible API -- alloc /
+alloc_collective / alloc_signals / view / sig_view / symm_at / remote_ptr and
+the one-sided data and signal ops -- on top of a C-ABI team (libtilefuse).
+Every PE's region is real device memory; `view()` returns a zero-copy torch
+tensor of it, `sig_view()` a host snapshot of the uint64 signal slots.
+
+The reference's generator-style device ops (`yield from heap.wait(...)`) have
+no host meaning on hardware: the device side of those primitives lives in
+csrc/tf_ptx.cuh (ld.acquire.sys / st.release.sys / red.release.sys spins used
+inside the kernels).  The host methods here enqueue the same semantics on CUDA
+streams: putmem/getmem are copy-engine transfers, putmem_signal orders the
+signal after the payload, wait blocks the stream until all slots reach the
+value, barrier_all is a stream-ordered all-rank rendezvous.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ProtocolError
+from .topology import Topology
+
+SCOPES = ("gpu", "sys")
+SEMANTICS = ("relaxed", "acquire", "release")
+
+
+@dataclass(frozen=True)
+class SymmHandle:
+    offset: int
+    nbytes: int
+
+
+@dataclass(frozen=True)
+class SigHandle:
+    base: int
+    nslots: int
+
+
+class _CudaMem:
+    """Minimal __cuda_array_interface__ exporter for zero-copy torch views."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+            "version": 3, "strides": None,
+        }
+
+
+def tensor_from_ptr(ptr: int, nbytes: int, device: int) -> torch.Tensor:
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaMem(ptr, nbytes), device=f"cuda:{device}")
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+@dataclass(frozen=True)
+class RemoteRegion:
+    """Addressable view of one PE's copy of a symmetric region (shmem.py:65-77)."""
+
+    heap: "SymmetricHeap"
+    handle: SymmHandle
+    pe: int
+
+    @property
+    def nbytes(self) -> int:
+        return self.handle.nbytes
+
+    def view(self, dtype, shape=None, offset: int = 0):
+        return self.heap.view(self.handle, self.pe, dtype, shape=shape, offset=offset)
+
+
+class Team:
+    """Owns a C tf_team.  Local (all PEs in this process) or IPC (one PE here)."""
+
+    def __init__(self, world: int, devices=None, heap_bytes: int = 1 << 24,
+                 signal_slots: int = 1 << 14, *, ipc_rank: int | None = None,
+                 ipc_device: int | None = None):
+        self.world = int(world)
+        self.heap_bytes = int(heap_bytes)
+        self.signal_slots = int(signal_slots)
+        h = C.c_void_p()
+        if ipc_rank is None:
+            if devices is None:
+                ndev = torch.cuda.device_count()
+                devices = [r % max(ndev, 1) if ndev >= world else 0 for r in range(world)]
+            self.devices = [int(d) for d in devices]
+            arr = (C.c_int * self.world)(*self.devices)
+            _lib.call("tf_team_create_local", self.world, arr, self.heap_bytes,
+                      self.signal_slots, C.byref(h))
+            self.rank = None
+        else:
+            dev = torch.cuda.current_device() if ipc_device is None else int(ipc_device)
+            self.devices = [dev] * self.world
+            _lib.call("tf_team_create_ipc", self.world, int(ipc_rank), dev, self.heap_bytes,
+                      self.signal_slots, C.byref(h))
+            self.rank = int(ipc_rank)
+        self.handle = h
+
+    @classmethod
+    def from_process_group(cls, heap_bytes: int, signal_slots: int = 1 << 14, group=None):
+        """IPC team over the current torch.distributed group (one GPU per rank)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        team = cls(world, heap_bytes=heap_bytes, signal_slots=signal_slots, ipc_rank=rank,
+                   ipc_device=torch.cuda.current_device())
+        blob = (C.c_uint8 * 128)()
+        _lib.call("tf_team_export_handle", team.handle, blob, 128)
+        mine = bytes(blob)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine, group=group)
+        allb = b"".join(gathered)
+        _lib.call("tf_team_open_peers", team.handle, C.c_char_p(allb), 128)
+        return team
+
+    @property
+    def distinct_devices(self) -> bool:
+        return len(set(self.devices)) == len(self.devices)
+
+    def local_ranks(self):
+        return [self.rank] if self.rank is not None else list(range(self.world))
+
+    def check(self):
+        _lib.call("tf_team_check", self.handle)
+
+    def close(self):
+        if self.handle:
+            _lib.lib().tf_team_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def heap_ptr(self, pe: int, offset: int) -> int:
+        p = C.c_void_p()
+        _lib.call("tf_heap_ptr", self.handle, int(pe), int(offset), C.byref(p))
+        return int(p.value or 0)
+
+    def signal_ptr(self, pe: int, slot: int) -> int:
+        p = C.c_void_p()
+        _lib.call("tf_signal_ptr", self.handle, int(pe), int(slot), C.byref(p))
+        return int(p.value or 0)
+
+
+class SymmetricHeap:
+    """Per-PE mirrored device regions plus uint64 signal slots (shmem.py:87-105).
+
+    `topology` fixes the world size; `devices` maps PEs to CUDA devices (defaults
+    to one GPU per PE when enough exist, else every PE on cuda:0).  The `engine`
+    argument of the reference constructor is accepted and ignored.
+    """
+
+    def __init__(self, topology: Topology, engine=None, data_bytes: int = 1 << 24,
+                 signal_slots: int = 1 << 14, *, devices=None, team: Team | None = None):
+        self.topology = topology
+        self.engine = engine
+        self.data_bytes = int(data_bytes)
+        self.signal_slots = int(signal_slots)
+        self.team = team or Team(topology.world_size, devices, self.data_bytes, self.signal_slots)
+
+    # ------------------------------------------------------------------ alloc
+    def alloc(self, nbytes: int, align: int = 16) -> SymmHandle:
+        if nbytes < 0:
+            raise ValueError("allocation size must be >= 0")
+        off = C.c_uint64()
+        _lib.call("tf_heap_alloc", self.team.handle, int(nbytes), int(align), C.byref(off))
+        return SymmHandle(offset=int(off.value), nbytes=int(nbytes))
+
+    def alloc_collective(self, sizes) -> SymmHandle:
+        sizes = list(sizes)
+        if len(sizes) != self.topology.world_size:
+            raise ProtocolError(f"collective allocation needs {self.topology.world_size} "
+                                f"requests, got {len(sizes)}")
+        if len(set(sizes)) != 1:
+            raise ProtocolError(f"mismatched collective allocation sizes: {sizes}")
+        return self.alloc(sizes[0])
+
+    def alloc_signals(self, nslots: int) -> SigHandle:
+        if nslots < 0:
+            raise ValueError("signal slot count must be >= 0")
+        base = C.c_uint64()
+        _lib.call("tf_signal_alloc", self.team.handle, int(nslots), C.byref(base))
+        return SigHandle(base=int(base.value), nslots=int(nslots))
+
+    # ------------------------------------------------------------------ views
+    def _check_pe(self, pe: int):
+        if not 0 <= pe < self.topology.world_size:
+            raise ValueError(f"pe {pe} out of range [0, {self.topology.world_size})")
+
+    def view(self, handle: SymmHandle, pe: int, dtype, shape=None, offset: int = 0):
+        """Zero-copy torch view of PE `pe`'s copy (shmem.py:143-153)."""
+        self._check_pe(pe)
+        if offset < 0 or offset > handle.nbytes:
+            raise ValueError(f"offset {offset} outside region of {handle.nbytes} bytes")
+        nbytes = handle.nbytes - offset
+        tdtype = _torch_dtype(dtype)
+        dev = self.team.devices[pe] if self.team.rank is None else self.team.devices[self.team.rank]
+        if nbytes == 0:
+            raw = torch.empty(0, dtype=torch.uint8, device=f"cuda:{dev}")
+        else:
+            raw = tensor_from_ptr(self.team.heap_ptr(pe, handle.offset + offset), nbytes, dev)
+        isz = torch.empty(0, dtype=tdtype).element_size()
+        arr = raw[: (nbytes // isz) * isz].view(tdtype)
+        if shape is not None:
+            count = int(np.prod(shape)) if shape else 1
+            arr = arr[:count].reshape(shape)
+        return arr
+
+    def sig_view(self, sig: SigHandle, pe: int) -> np.ndarray:
+        """Host snapshot of the signal slots (shmem.py:155-157), int64 like the reference."""
+        self._check_pe(pe)
+        out = (C.c_uint64 * max(sig.nslots, 1))()
+        _lib.call("tf_signal_read", self.team.handle, int(pe), int(sig.base), int(sig.nslots), out)
+        return np.frombuffer(bytes(out), dtype=np.uint64)[: sig.nslots].astype(np.int64)
+
+    def symm_at(self, handle: SymmHandle, pe: int) -> RemoteRegion:
+        self._check_pe(pe)
+        return RemoteRegion(self, handle, pe)
+
+    remote_ptr = symm_at
+
+    # ------------------------------------------------------- signal plane ops
+    def _slot(self, sig: SigHandle, idx: int, n: int, pe: int) -> int:
+        self._check_pe(pe)
+        if idx < 0 or idx + n > sig.nslots:
+            raise ValueError(f"signal slots [{idx}, {idx + n}) exceed handle of {sig.nslots}")
+        return sig.base + idx
+
+    def ld(self, sig: SigHandle, idx: int, pe: int, scope: str = "gpu",
+           semantic: str = "acquire") -> int:
+        _check_scope_semantic(scope, semantic)
+        self._slot(sig, idx, 1, pe)
+        torch.cuda.synchronize(self.team.devices[pe])
+        return int(self.sig_view(SigHandle(sig.base + idx, 1), pe)[0])
+
+    def st(self, sig: SigHandle, idx: int, value: int, pe: int, scope: str = "gpu",
+           semantic: str = "relaxed", name: str = "st", stream=None) -> None:
+        _check_scope_semantic(scope, semantic)
+        slot = self._slot(sig, idx, 1, pe)
+        _lib.call("tf_signal_op", self.team.handle, int(pe), slot, int(value), 0, _stream_ptr(stream))
+
+    def notify(self, sig: SigHandle, idx: int, pe: int, value: int, semantic: str = "release",
+               stream=None) -> None:
+        self.st(sig, idx, value, pe, scope="sys", semantic=semantic, name="notify", stream=stream)
+
+    def atomic_add(self, sig: SigHandle, idx: int, val: int, pe: int, semantic: str = "release",
+                   scope: str = "gpu", stream=None) -> None:
+        """Stream-ordered release add.  Unlike the reference it does not return
+        the old value (a host round trip would serialise the device)."""
+        _check_scope_semantic(scope, semantic)
+        slot = self._slot(sig, idx, 1, pe)
+        _lib.call("tf_signal_op", self.team.handle, int(pe), slot, int(val), 1, _stream_ptr(stream))
+
+    def wait(self, sig: SigHandle, idx: int, num_slots: int, pe: int, scope: str = "gpu",
+             semantic: str = "acquire", value: int = 1, note=None, stream=None) -> None:
+        """Stream waits until every slot in [idx, idx+num_slots) >= value."""
+        _check_scope_semantic(scope, semantic)
+        if num_slots < 1:
+            raise ValueError("wait needs num_slots >= 1")
+        slot = self._slot(sig, idx, num_slots, pe)
+        _lib.call("tf_signal_wait", self.team.handle, int(pe), slot, int(num_slots), int(value),
+                  _stream_ptr(stream))
+
+    def reset_signals(self, sig: SigHandle, pe: int, stream=None) -> None:
+        slot = self._slot(sig, 0, sig.nslots, pe)
+        _lib.call("tf_signal_reset", self.team.handle, int(pe), slot, int(sig.nslots), _stream_ptr(stream))
+
+    # ---------------------------------------------------------- data plane ops
+    def putmem(self, dest: RemoteRegion, dest_off: int, src: torch.Tensor, *, from_pe: int = 0,
+               note: str = "putmem", stream=None):
+        nbytes = src.numel() * src.element_size()
+        _check_range(dest.handle, dest_off, nbytes)
+        src = src.contiguous()
+        _lib.call("tf_putmem", self.team.handle, int(dest.pe), dest.handle.offset + int(dest_off),
+                  src.data_ptr(), nbytes, _stream_ptr(stream))
+
+    def getmem(self, dst: torch.Tensor, src: RemoteRegion, src_off: int, *, from_pe: int = 0,
+               note: str = "getmem", stream=None):
+        if not dst.is_contiguous():
+            raise ValueError("getmem destination must be contiguous")
+        nbytes = dst.numel() * dst.element_size()
+        _check_range(src.handle, src_off, nbytes)
+        _lib.call("tf_getmem", self.team.handle, int(src.pe), src.handle.offset + int(src_off),
+                  dst.data_ptr(), nbytes, _stream_ptr(stream))
+
+    def putmem_signal(self, dest: RemoteRegion, dest_off: int, src: torch.Tensor, sig: SigHandle,
+                      idx: int, value: int, sig_op: str = "set", *, from_pe: int = 0,
+                      note: str = "putmem_signal", stream=None):
+        if sig_op not in ("set", "add"):
+            raise ValueError(f"sig_op must be 'set' or 'add', got {sig_op!r}")
+        slot = self._slot(sig, idx, 1, dest.pe)
+        nbytes = src.numel() * src.element_size()
+        _check_range(dest.handle, dest_off, nbytes)
+        src = src.contiguous()
+        _lib.call("tf_putmem_signal", self.team.handle, int(dest.pe),
+                  dest.handle.offset + int(dest_off), src.data_ptr(), nbytes, slot, int(value),
+                  1 if sig_op == "add" else 0, _stream_ptr(stream))
+
+    putmem_nbi = putmem
+    getmem_nbi = getmem
+
+    def fence(self, from_pe: int) -> None:
+        """Ordering of puts from one stream is already issue-order (copy engine queue)."""
+        self._check_pe(from_pe)
+
+    def barrier_all(self, rank: int | None = None, stream=None):
+        """All-rank rendezvous ordered after every prior op on the rank's stream.
+        With rank=None every local PE arrives and then waits (single-process team)."""
+        ranks = self.team.local_ranks() if rank is None else [rank]
+        for r in ranks:
+            self._check_pe(r)
+            with torch.cuda.device(self.team.devices[r]):
+                _lib.call("tf_barrier_arrive", self.team.handle, r, _stream_ptr(stream))
+        for r in ranks:
+            with torch.cuda.device(self.team.devices[r]):
+                _lib.call("tf_barrier_wait", self.team.handle, r, _stream_ptr(stream))
+
+    sync_all = barrier_all
+
+
+def _check_scope_semantic(scope: str, semantic: str):
+    if scope not in SCOPES:
+        raise ValueError(f"invalid scope {scope!r}; expected one of {SCOPES}")
+    if semantic not in SEMANTICS:
+        raise ValueError(f"invalid semantic {semantic!r}; expected one of {SEMANTICS}")
+
+
+def _check_range(handle: SymmHandle, off: int, nbytes: int):
+    if off < 0 or off + nbytes > handle.nbytes:
+        raise ValueError(f"range [{off}, {off + nbytes}) exceeds region of {handle.nbytes} bytes")
+
+
+_NP2T = {
+    np.dtype(np.uint8): torch.uint8, np.dtype(np.int8): torch.int8,
+    np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
+    np.dtype(np.float32): torch.float32, np.dtype(np.float16): torch.float16,
+    np.dtype(np.float64): torch.float64, np.dtype(np.uint64): torch.uint64,
+}
+
+
+def _torch_dtype(dtype) -> torch.dtype:
+    if isinstance(dtype, torch.dtype):
+        return dtype
+    return _NP2T[np.dtype(dtype)]
