@@ -47,7 +47,7 @@ struct ReduceSrc {
 template <bool IN_F32>
 __global__ void __launch_bounds__(256) rs_reduce_kernel(
     ReduceSrc srcs, long long src_ld, int world, int order_ring, int owner, void* out,
-    long long out_ld, int out_f32, long long rows, long long n, long long row0_global,
+    long long out_ld, int out_f32, int out_vec, long long rows, long long n, long long row0_global,
     const uint64_t* counters, unsigned long long expected, int first_tile, int ntiles,
     int col_chunks, unsigned long long timeout_ns, unsigned long long* err) {
   const int items = ntiles * col_chunks;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(
       }
       if (out_f32) {
         float* o = static_cast<float*>(out) + r * out_ld + c;
-        if (full) {
+        if (full && out_vec) {
           *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
           *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
         } else {
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(
         }
       } else {
         uint16_t* o = static_cast<uint16_t*>(out) + r * out_ld + c;
-        if (full) {
+        if (full && out_vec) {
           *reinterpret_cast<uint4*>(o) =
               make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
                          pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
@@ -302,21 +302,25 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     const int ntiles = static_cast<int>(last_tile - first_tile + 1);
     const int col_chunks = static_cast<int>((n + 2047) / 2048);
     const int ldc = static_cast<int>(args->ldc ? args->ldc : n);
-    int grid = args->num_comm_sms > 0 ? args->num_comm_sms * 2 : tf::num_sms_of_current_device();
-    if (!overlap) grid = tf::num_sms_of_current_device();
+    // overlapped: a few co-resident CTAs (they fit beside the 1-CTA/SM GEMM);
+    // serialised: the whole GPU
+    int grid = overlap ? (args->num_comm_sms > 0 ? args->num_comm_sms * 2 : 16)
+                       : tf::num_sms_of_current_device();
     const int items = ntiles * col_chunks;
     if (grid > items) grid = items;
     if (grid < 1) grid = 1;
     const unsigned long long expected = static_cast<unsigned long long>(w) * num_pid_n;
     const uint64_t* cnt = t->pes[rank].sig + ws->sig_base;
+    const int out_vec = ((static_cast<int64_t>(ldc) * esz) % 16 == 0) &&
+                        (reinterpret_cast<uintptr_t>(args->c) % 16 == 0);
     if (f32)
       tf::rs_reduce_kernel<true><<<grid, 256, 0, rs>>>(
-          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 1, mpr, n,
+          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 1, out_vec, mpr, n,
           rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
           t->timeout_ns, t->err_word(rank));
     else
       tf::rs_reduce_kernel<false><<<grid, 256, 0, rs>>>(
-          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 0, mpr, n,
+          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 0, out_vec, mpr, n,
           rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
           t->timeout_ns, t->err_word(rank));
     TF_CUDA_TRY(cudaGetLastError());
@@ -353,15 +357,21 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     }
     g.err = t->err_word(rank);
     g.timeout_ns = t->timeout_ns;
+    // The GEMM is enqueued first and the reduce only waits on the pre-GEMM
+    // point of `stream`: whatever the streams' blocking semantics, the spinning
+    // reduce can never sit in front of the producer it waits for.
+    cudaEvent_t pre = nullptr;
     if (overlap) {
-      rc = tf::StreamJoin::fork(s, cs);
-      if (rc) return rc;
-      rc = launch_reduce(cs);
-      if (rc) return rc;
+      TF_CUDA_TRY(cudaEventCreateWithFlags(&pre, cudaEventDisableTiming));
+      TF_CUDA_TRY(cudaEventRecord(pre, s));
     }
     rc = tf::launch_gemm(g, s);
     if (rc) return rc;
     if (overlap) {
+      TF_CUDA_TRY(cudaStreamWaitEvent(cs, pre, 0));
+      cudaEventDestroy(pre);
+      rc = launch_reduce(cs);
+      if (rc) return rc;
       rc = tf::StreamJoin::fork(cs, s);
       if (rc) return rc;
     }
