@@ -1,0 +1,375 @@
+"""Benchmark of the fused-collective hot path (BASELINE.json config 2).
+
+One step = one tensor-parallel Llama-3-70B MLP pass through the fused ops:
+    h_r = AllGather+GEMM(x_r, W1_r)      x_r [8192/TP, 8192], W1_r [28672/TP, 8192]
+    y_r = GEMM+ReduceScatter(h_r, W2_r)  h_r [8192, 28672/TP], W2_r [8192, 28672/TP]
+bf16 inputs, fp32 accumulation, bf16 outputs; TP = number of GPUs (one process
+per GPU under torchrun, IPC symmetric heap).  At N=1 both ops degenerate to the
+local GEMM (no exchange), which is what the round-end 1-GPU bench measures.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0 (contract in the task statement): value = total
+TFLOP/s over all ranks (max-over-ranks device time), roofline of the dominant
+kernel (the tcgen05 GEMM) against MEASURED_PEAKS.json, e2e through the public
+API with pinned host buffers, cuBLAS comparator, clocks sampled during the timed
+region, and the CPU baseline (the numpy oracle on a bounded sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AG-GEMM/GEMM-RS TFLOPS at 1/2/4/8 B200 vs roofline; MoE a2a GB/s"
+TOKENS, HIDDEN, FFN = 8192, 8192, 28672
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512):
+    """Oracle (numpy) MLP step on a bounded sample: `rows` tokens instead of 8192,
+    fp32, all host threads.  Returns (TFLOP/s, seconds, cores, sample text)."""
+    import numpy as np
+
+    from oracle import collectives as O
+    cores = len(os.sched_getaffinity(0))
+    rng = np.random.default_rng(0)
+    f_tp = FFN // tp
+    mpr = max(rows // tp, 1)
+    x = [rng.standard_normal((mpr, HIDDEN), dtype=np.float32) for _ in range(tp)]
+    w1 = [rng.standard_normal((f_tp, HIDDEN), dtype=np.float32) for _ in range(tp)]
+    w2 = [rng.standard_normal((HIDDEN, f_tp), dtype=np.float32) for _ in range(tp)]
+    flops = 2 * 2 * (mpr * tp) * HIDDEN * FFN
+    O.ref_allgather_gemm(x, w1[:1])  # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        h = O.ref_allgather_gemm(x, w1)
+        O.ref_reduce_scatter(h, w2)
+    dt = (time.perf_counter() - t0) / steps
+    sample = (f"oracle ref_allgather_gemm + ref_reduce_scatter (numpy fp32, OpenBLAS) on "
+              f"{mpr * tp} of {TOKENS} tokens, TP={tp}, hidden {HIDDEN}, ffn {FFN}")
+    return flops / dt / 1e12, dt, cores, sample
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (the oracle port of
+    ovs/kernels/oracles.py, since the reference is pure Python) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    tp = args.gpus
+    vals = []
+    cores = None
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=256)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(dt for _, dt in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"llama3-70b MLP AG-GEMM+GEMM-RS, TP={tp}, sampled on 256 tokens",
+                   "tokens": TOKENS, "hidden": HIDDEN, "ffn": FFN, "tp": tp},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_02953_b200 import kernels as K
+    from paper_2605_02953_b200.shmem import Team
+
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    distributed = world_env > 1
+    if distributed:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        rank, world = dist.get_rank(), dist.get_world_size()
+    else:
+        torch.cuda.set_device(0)
+        rank, world = 0, 1
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dev = torch.cuda.current_device()
+    tp = world
+    m, f_tp = TOKENS, FFN // tp
+    mpr = m // tp
+    peaks, peaks_kind = load_peaks()
+
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    def rnd(*shape, scale=1.0):
+        return (torch.randn(*shape, generator=g) * scale).to(torch.bfloat16).to(f"cuda:{dev}")
+    x = rnd(mpr, HIDDEN)
+    w1 = rnd(f_tp, HIDDEN, scale=HIDDEN ** -0.5)
+    w2 = rnd(HIDDEN, f_tp, scale=f_tp ** -0.5)
+    h = torch.empty(m, f_tp, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    y = torch.empty(mpr, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
+
+    heap = 2 * m * HIDDEN * 2 + m * ((HIDDEN + 7) // 8 * 8) * 2 + (64 << 20)
+    if distributed:
+        team = Team.from_process_group(heap_bytes=heap, signal_slots=4096)
+    else:
+        team = Team(1, [dev], heap_bytes=(1 << 20), signal_slots=4096)
+    ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=8)
+    rs = K.GemmReduceScatter(team, m, f_tp, HIDDEN, block_n=256, group_m=8, num_comm_sms=8,
+                             fuse_scatter=True, reduce_order="ascending")
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
+    def step():
+        ag(x, w1, h)
+        rs(h, w2, y)
+
+    n_events = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_events)]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(dev)
+        clocks.start()
+        time.sleep(0.3)
+        for i in range(args.steps):
+            flush.zero_()  # evict L2 between steps (outside the per-step events)
+            ev[i][0].record(stream)
+            ag(x, w1, h)
+            ev[i][1].record(stream)
+            rs(h, w2, y)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+    team.check()
+    ag_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(n_events)]
+    rs_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(n_events)]
+    step_ms = sum(a + b for a, b in zip(ag_ms, rs_ms)) / n_events
+    gemm_flops = 2.0 * m * f_tp * HIDDEN  # per GEMM per rank
+    # max over ranks
+    t = torch.tensor([step_ms, sum(ag_ms) / n_events, sum(rs_ms) / n_events], device=f"cuda:{dev}")
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, ag_avg, rs_avg = (float(v) for v in t.tolist())
+    total_flops = 2 * gemm_flops * world
+    value = total_flops / (step_ms * 1e-3) / 1e12
+
+    # ---- cuBLAS comparator (same GEMMs, torch.matmul; unfused NCCL at N>1)
+    cub_ms = None
+    with torch.cuda.stream(stream):
+        xg = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
+        hp = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
+        def cublas_step():
+            if distributed:
+                dist.all_gather_into_tensor(xg, x)
+                hh = torch.matmul(xg, w1.t())
+                torch.matmul(hh, w2.t(), out=hp)
+                dist.reduce_scatter_tensor(y, hp)
+            else:
+                hh = torch.matmul(x, w1.t())
+                torch.matmul(hh, w2.t())
+        for _ in range(3):
+            cublas_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            e0.record(stream)
+            cublas_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        cub_ms = tot / max(3, args.steps // 2)
+    tc = torch.tensor([cub_ms], device=f"cuda:{dev}")
+    if distributed:
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+    cub_ms = float(tc.item())
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        x_host = x.cpu().pin_memory()
+        y_host = torch.empty(mpr, HIDDEN, dtype=torch.bfloat16).pin_memory()
+        x_dev = torch.empty_like(x)
+        with torch.cuda.stream(stream):
+            def e2e_step():
+                x_dev.copy_(x_host, non_blocking=True)
+                ag(x_dev, w1, h)
+                rs(h, w2, y)
+                y_host.copy_(y, non_blocking=True)
+            for _ in range(2):
+                e2e_step()
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=f"cuda:{dev}")
+        if distributed:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item())
+        e2e = {"value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+               "ms_per_step": round(e2e_ms, 4),
+               "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": y.numel() * 2}
+
+    # ---- roofline of the dominant kernel (the tcgen05 GEMM; one launch per op at N=1)
+    peak = peaks.get("bf16_tflops", 1622.7)
+    peak_sus = peaks.get("bf16_tflops_sustained", peak)
+    gemm_ms = min(ag_avg, rs_avg) if world == 1 else ag_avg
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
+    nv_bytes = (world - 1) / world * m * HIDDEN * 2 if world > 1 else 0
+    roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "frac_of_sustained": round(achieved / peak_sus, 4),
+            "peak_kind": f"{peaks_kind} burst bf16 (MEASURED_PEAKS.json bf16_tflops)",
+            "traffic": None, "kernel": "gemm_sm100_kernel<256,bf16>",
+            "flops_per_launch": gemm_flops, "nvlink_bytes_per_ag": nv_bytes,
+            "per_op_ms": {"ag_gemm": round(ag_avg, 4), "gemm_rs": round(rs_avg, 4)}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+        v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=1024)
+        cpu = {"value": round(v, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": sample, "seconds": round(dt, 3)}
+
+    launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded N(0,1) activations, 1/sqrt(K)-scaled weights)",
+            "config": {"workload": f"llama3-70b MLP: AG-GEMM(M={m},N={f_tp},K={HIDDEN}) + "
+                                   f"GEMM-RS(M={m},N={HIDDEN},K={f_tp}), TP={tp}",
+                       "tokens": TOKENS, "hidden": HIDDEN, "ffn": FFN, "tp": tp,
+                       "parallelism": f"tp{tp}", "l2": "flushed between steps (256 MiB memset), "
+                       "outside the per-step events"},
+            "roofline": roof,
+            "comparator": {"impl": "cuBLAS (torch.matmul)" + (" + NCCL all_gather/reduce_scatter"
+                                                           if distributed else ""),
+                           "ms_per_step": round(cub_ms, 4),
+                           "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
+                           "speedup": round(cub_ms / step_ms, 4)},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -205,6 +205,13 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
   if (args->m % w) return fail(TF_ERR_INVALID, "gathered M must divide evenly across ranks");
   if ((args->k * 2) % 16) return fail(TF_ERR_INVALID, "K must be a multiple of 8 (16-byte rows)");
   const int64_t mpr = args->m / w;
+  if (w == 1) {
+    // no exchange: the local GEMM straight from the caller's A (no workspace copy)
+    if (!(phase & TF_PHASE_MAIN)) return TF_OK;
+    tf::GemmLaunch g = tf::base_launch(args);
+    g.num_sms = tf::gemm_grid(args);
+    return tf::launch_gemm(g, static_cast<cudaStream_t>(stream));
+  }
   const size_t chunk_bytes = static_cast<size_t>(mpr) * args->k * 2;
   const std::string key = "ag:" + std::to_string(args->m) + "x" + std::to_string(args->k);
   tf::Workspace* ws = t->workspace(key, 2 * chunk_bytes * w, 2 * w, &rc);
@@ -271,6 +278,13 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
   if (args->m % w) return fail(TF_ERR_INVALID, "M must divide evenly across ranks");
   const int64_t mpr = args->m / w;
   const int64_t n = args->n;
+  if (w == 1) {
+    // no exchange: rows of the only rank are the whole GEMM (tests/test_kernels.py:203-207)
+    if (!(phase & TF_PHASE_MAIN)) return TF_OK;
+    tf::GemmLaunch g = tf::base_launch(args);
+    g.num_sms = tf::gemm_grid(args);
+    return tf::launch_gemm(g, static_cast<cudaStream_t>(stream));
+  }
   const bool f32 = args->out_dtype == TF_DTYPE_F32;
   const int esz = f32 ? 4 : 2;
   const int64_t ld = (n + 7) / 8 * 8;  // 16-byte aligned slot rows

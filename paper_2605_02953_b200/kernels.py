@@ -350,8 +350,8 @@ class AllGatherGemm:
 
     def forward(self, a, b, out=None):
         t = self.team
-        if t.rank is not None:
-            r = t.rank
+        if t.rank is not None or (t.world == 1 and isinstance(a, torch.Tensor)):
+            r = t.rank or 0
             if out is None:
                 out = torch.empty((self.m, self.n), dtype=self.out_dtype, device=a.device)
             g = self._args(r, a, b, out)
@@ -396,8 +396,8 @@ class GemmReduceScatter:
     def forward(self, x, w, out=None):
         t = self.team
         mpr = self.m // t.world
-        if t.rank is not None:
-            r = t.rank
+        if t.rank is not None or (t.world == 1 and isinstance(x, torch.Tensor)):
+            r = t.rank or 0
             if out is None:
                 out = torch.empty((mpr, self.n), dtype=self.out_dtype, device=x.device)
             g = self._args(r, x, w, out)
