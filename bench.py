@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--group-m", type=int, default=int(os.environ.get("TF_GROUP_M", "16")))
     return p.parse_args()
 
 
@@ -205,8 +206,8 @@ def main_ours(args):
         team = Team.from_process_group(heap_bytes=heap, signal_slots=4096)
     else:
         team = Team(1, [dev], heap_bytes=(1 << 20), signal_slots=4096)
-    ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=8)
-    rs = K.GemmReduceScatter(team, m, f_tp, HIDDEN, block_n=256, group_m=8, num_comm_sms=8,
+    ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=args.group_m)
+    rs = K.GemmReduceScatter(team, m, f_tp, HIDDEN, block_n=256, group_m=args.group_m, num_comm_sms=8,
                              fuse_scatter=True, reduce_order="ascending")
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -325,7 +326,8 @@ def main_ours(args):
     roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "frac_of_sustained": round(achieved / peak_sus, 4),
             "peak_kind": f"{peaks_kind} burst bf16 (MEASURED_PEAKS.json bf16_tflops)",
-            "traffic": None, "kernel": "gemm_sm100_kernel<256,bf16>",
+            "traffic": None, "kernel": "gemm_sm100_kernel<CG=2,BN=256,bf16> (256x256 tile per CTA pair)",
+            "group_m": args.group_m,
             "flops_per_launch": gemm_flops, "nvlink_bytes_per_ag": nv_bytes,
             "per_op_ms": {"ag_gemm": round(ag_avg, 4), "gemm_rs": round(rs_avg, 4)}}
 

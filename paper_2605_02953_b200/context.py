@@ -64,7 +64,8 @@ class WorkloadContext:
 
     @property
     def hw_block_m(self) -> int:
-        return 128
+        # 256 = CTA pair per tile (tcgen05 cta_group::2); smaller = one CTA, 128 rows
+        return 256 if self.block_m >= 256 else 128
 
 
 @dataclass

@@ -30,7 +30,6 @@ namespace tf {
 
 namespace {
 
-constexpr int BM = 128;
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
 constexpr int UMMA_K = 16;
 constexpr int kThreads = 192;          // 6 warps
@@ -56,12 +55,14 @@ struct KParams {
   unsigned long long timeout_ns;
 };
 
-template <int BN>
+template <int CG, int BN>
 struct Smem {
-  static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kTileM = 128 * CG;           // rows per (pair) tile
+  static constexpr int kABytes = 128 * BK * 2;      // per CTA: 128 rows of A
+  static constexpr int kBRows = BN / CG;            // per CTA: BN/CG rows of B
+  static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN >= 256) ? 4 : 6;
+  static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
   static constexpr int kBarBytes = 256;
   static constexpr int kTotal = 1024 /*align slack*/ + kStages * kStageBytes + kBarBytes;
   static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;
@@ -79,12 +80,16 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid
   if (p.tile_map) pid_m = __ldg(p.tile_map + pid_m);
 }
 
-template <int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+// CG = 1: one CTA per 128 x BN tile (tcgen05 cta_group::1).
+// CG = 2: a CTA pair (cluster of 2) per 256 x BN tile (tcgen05 cta_group::2): each
+//         CTA stages 128 rows of A and BN/2 rows of B, the leader issues the
+//         M=256 MMAs, each CTA's TMEM holds its 128 rows of the accumulator.
+template <int CG, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ KParams p) {
-  using S = Smem<BN>;
+  using S = Smem<CG, BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -100,6 +105,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.num_pid_m * p.num_pid_n;
+  const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = cta_rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -108,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty_bar[s], 4 * CG);  // every epilogue warp of the pair
     }
     fence_barrier_init();
   }
@@ -116,9 +125,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, S::kTmemCols);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, S::kTmemCols);
+    else tmem_alloc(tmem_slot, S::kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -128,81 +141,100 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ready_mask = 0;  // AllGather chunks already observed as arrived
-      for (int step = blockIdx.x; step < num_tiles; step += gridDim.x) {
+      for (int step = cluster_id; step < num_tiles; step += num_clusters) {
         int pid_m, pid_n;
         tile_coords(p, step, pid_m, pid_n);
-        const int m0 = pid_m * BM;
-        const int n0 = pid_n * BN;
+        const int m0 = pid_m * S::kTileM + 128 * cta_rank;   // this CTA's A rows
+        const int n0 = pid_n * BN + S::kBRows * cta_rank;    // this CTA's B rows
         if constexpr (AG_WAIT) {
-          // wait(arrival, rank_beg, n) acquire -- ag_gemm.py:87-90
-          const int r1 = min(m0 + BM, p.m) - 1;
-          const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
-          const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
-          bool waited = false;
-          for (int c = c_beg; c <= c_end; ++c) {
-            if (ready_mask & (1u << c)) continue;
-            wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
-                         0x1000000ull | static_cast<unsigned long long>(c));
-            ready_mask |= 1u << c;
-            waited = true;
+          // wait(arrival, rank_beg, n) acquire -- ag_gemm.py:87-90 (this CTA's rows)
+          if (m0 < p.m) {
+            const int r1 = min(m0 + 128, p.m) - 1;
+            const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
+            const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
+            bool waited = false;
+            for (int c = c_beg; c <= c_end; ++c) {
+              if (ready_mask & (1u << c)) continue;
+              wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
+                           0x1000000ull | static_cast<unsigned long long>(c));
+              ready_mask |= 1u << c;
+              waited = true;
+            }
+            // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
+            if (waited) fence_proxy_async_global();
           }
-          // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
-          if (waited) fence_proxy_async_global();
         }
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
-          tma_load_2d(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
-          tma_load_2d(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            tma_load_2d_pair(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
+            tma_load_2d_pair(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+            tma_load_2d(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
+            tma_load_2d(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+          }
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int step = blockIdx.x; step < num_tiles; step += gridDim.x, ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        mbar_wait(&full_bar[stage], phase);
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(S::kTileM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(smem_a + stage * S::kABytes);
-          const uint32_t b_addr = smem_u32(smem_b + stage * S::kBBytes);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smem_a + stage * S::kABytes);
+            const uint32_t b_addr = smem_u32(smem_b + stage * S::kBBytes);
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
-            const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+              const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
+              const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
+              if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+              else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            }
+            // smem slot free (in both CTAs) once these MMAs retire
+            if constexpr (CG == 2) umma_commit_pair_mc(&empty_bar[stage], 0x3);
+            else umma_commit(&empty_bar[stage]);
           }
-          umma_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
+          __syncwarp();
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) {  // accumulator ready for the epilogues
+          if constexpr (CG == 2) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+          else umma_commit(&tfull_bar[acc]);
         }
         __syncwarp();
-        if (++stage == S::kStages) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
-      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const int quarter = warp & 3;          // TMEM lanes [32*quarter, 32*quarter+32)
-    const int row_in_tile = quarter * 32 + lane;
+    const int row_in_cta = quarter * 32 + lane;
+    const uint32_t tempty_leader =
+        CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
     int local = 0;
-    for (int step = blockIdx.x; step < num_tiles; step += gridDim.x, ++local) {
+    for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
       int pid_m, pid_n;
       tile_coords(p, step, pid_m, pid_n);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = pid_m * BM + row_in_tile;
+      const int row0 = pid_m * S::kTileM + 128 * cta_rank;
+      const int row = row0 + row_in_cta;
       const bool row_ok = row < p.m;
       uint8_t* dst_row = nullptr;
       if (row_ok) {
@@ -256,30 +288,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // accumulator drained: hand TMEM back to the MMA warp
+      // accumulator drained: hand TMEM back to the leader's MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       if constexpr (EPI == 1) {
         // publish: every thread's stores are made visible system-wide, the four
-        // epilogue warps meet, then one thread release-adds the owners' counters.
+        // epilogue warps meet, then one thread release-adds the owners' counters
+        // (one counter per 128-row block of the output).
         fence_sys();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == kEpiWarp0 * 32) {
-          const int r0 = pid_m * BM;
-          const int r1 = min(r0 + BM, p.m) - 1;
-          const int o0 = static_cast<int>(r0 / p.rows_per_rank);
+        if (threadIdx.x == kEpiWarp0 * 32 && row0 < p.m) {
+          const int r1 = min(row0 + 128, p.m) - 1;
+          const int o0 = static_cast<int>(row0 / p.rows_per_rank);
           const int o1 = static_cast<int>(r1 / p.rows_per_rank);
-          for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + pid_m, 1);
+          for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
         }
       }
     }
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::kTmemCols);
+    if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, S::kTmemCols);
+    else tmem_dealloc(tmem_base, S::kTmemCols);
   }
 }
 
@@ -322,34 +360,47 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
   return TF_OK;
 }
 
-template <int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+template <int CG, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
              cudaStream_t stream) {
-  auto kern = gemm_sm100_kernel<BN, OUT_F32, EPI, AG_WAIT>;
-  static bool attr_done = false;  // per template instance
-  if (!attr_done) {
+  auto kern = gemm_sm100_kernel<CG, BN, OUT_F32, EPI, AG_WAIT>;
+  static uint64_t attr_done = 0;  // per template instance, bit per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_done & (1ull << dev))) {
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Smem<BN>::kTotal));
-    attr_done = true;
+                                     Smem<CG, BN>::kTotal));
+    attr_done |= 1ull << dev;
   }
-  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ta, tb, kp);
-  TF_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Smem<CG, BN>::kTotal;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, kp));
   return TF_OK;
 }
 
-template <int BN>
+template <int CG, int BN>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
                 const GemmLaunch& g, cudaStream_t s) {
   const bool ag = g.chunk_flags != nullptr;
   if (g.epilogue == 0) {
     if (g.out_f32)
-      return ag ? launch_t<BN, true, 0, true>(ta, tb, kp, grid, s)
-                : launch_t<BN, true, 0, false>(ta, tb, kp, grid, s);
-    return ag ? launch_t<BN, false, 0, true>(ta, tb, kp, grid, s)
-              : launch_t<BN, false, 0, false>(ta, tb, kp, grid, s);
+      return ag ? launch_t<CG, BN, true, 0, true>(ta, tb, kp, grid, s)
+                : launch_t<CG, BN, true, 0, false>(ta, tb, kp, grid, s);
+    return ag ? launch_t<CG, BN, false, 0, true>(ta, tb, kp, grid, s)
+              : launch_t<CG, BN, false, 0, false>(ta, tb, kp, grid, s);
   }
-  if (g.out_f32) return launch_t<BN, true, 1, false>(ta, tb, kp, grid, s);
-  return launch_t<BN, false, 1, false>(ta, tb, kp, grid, s);
+  if (g.out_f32) return launch_t<CG, BN, true, 1, false>(ta, tb, kp, grid, s);
+  return launch_t<CG, BN, false, 1, false>(ta, tb, kp, grid, s);
 }
 
 }  // namespace
@@ -366,6 +417,9 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   if (g.m == 0 || g.n == 0) return TF_OK;
   if (g.block_n != 128 && g.block_n != 256)
     return fail(TF_ERR_CONFIG, "block_n must be 128 or 256 on the tcgen05 path");
+  if (g.block_m != 128 && g.block_m != 256)
+    return fail(TF_ERR_CONFIG, "block_m must be 128 (one CTA) or 256 (CTA pair)");
+  const int tile_m = g.block_m;
   if ((g.lda * 2) % 16 || (g.ldb * 2) % 16)
     return fail(TF_ERR_INVALID, "A/B row strides must be multiples of 16 bytes (K % 8 == 0)");
   if ((reinterpret_cast<uintptr_t>(g.a) | reinterpret_cast<uintptr_t>(g.b)) & 15)
@@ -382,7 +436,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.m = static_cast<int>(g.m);
   kp.n = static_cast<int>(g.n);
   kp.k = static_cast<int>(g.k);
-  kp.num_pid_m = static_cast<int>((g.m + BM - 1) / BM);
+  kp.num_pid_m = static_cast<int>((g.m + tile_m - 1) / tile_m);
   kp.num_pid_n = static_cast<int>((g.n + g.block_n - 1) / g.block_n);
   kp.group_m = g.group_m;
   kp.num_kb = static_cast<int>((g.k + BK - 1) / BK);
@@ -410,17 +464,25 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.timeout_ns = g.timeout_ns;
   if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
 
+  const int cg = tile_m / 128;
   CUtensorMap ta, tb;
-  int rc = make_tmap_2d(&ta, g.a, g.m, g.k, g.lda, BM);
+  int rc = make_tmap_2d(&ta, g.a, g.m, g.k, g.lda, 128);
   if (rc) return rc;
-  rc = make_tmap_2d(&tb, g.b, g.n, g.k, g.ldb, g.block_n);
+  rc = make_tmap_2d(&tb, g.b, g.n, g.k, g.ldb, g.block_n / cg);
   if (rc) return rc;
 
   const int tiles = kp.num_pid_m * kp.num_pid_n;
-  int grid = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
-  if (grid > tiles) grid = tiles;
-  if (g.block_n == 256) return dispatch_bn<256>(ta, tb, kp, grid, g, stream);
-  return dispatch_bn<128>(ta, tb, kp, grid, g, stream);
+  int ctas = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
+  int clusters = ctas / cg;
+  if (clusters < 1) clusters = 1;
+  if (clusters > tiles) clusters = tiles;
+  const int grid = clusters * cg;
+  if (cg == 2) {
+    if (g.block_n == 256) return dispatch_bn<2, 256>(ta, tb, kp, grid, g, stream);
+    return dispatch_bn<2, 128>(ta, tb, kp, grid, g, stream);
+  }
+  if (g.block_n == 256) return dispatch_bn<1, 256>(ta, tb, kp, grid, g, stream);
+  return dispatch_bn<1, 128>(ta, tb, kp, grid, g, stream);
 }
 
 }  // namespace tf

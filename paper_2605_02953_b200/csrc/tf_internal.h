@@ -30,6 +30,7 @@ struct GemmLaunch {
   const void* b = nullptr;
   int64_t m = 0, n = 0, k = 0, lda = 0, ldb = 0;
   // tiling / order (reference WorkloadContext semantics, ovs/kernels/context.py:18-54)
+  int block_m = 128;                 // 128 = one CTA per tile, 256 = CTA pair (cta_group::2)
   int block_n = 256;
   int group_m = 8;
   int num_sms = 0;                   // persistent CTAs (reference num_gemm_sms); 0 = all SMs

@@ -145,7 +145,8 @@ def tile_map_host(m: int, rank: int, world: int, nnodes: int, block_m: int, mode
 
 
 def _args(a, b, c, m, n, k, *, out_dtype, block_n, group_m, num_gemm_sms, num_comm_sms,
-          swizzle, tile_map, fuse_scatter=0, reduce_order="ring", ldc=None) -> _lib.GemmArgs:
+          swizzle, tile_map, fuse_scatter=0, reduce_order="ring", ldc=None,
+          block_m=BM) -> _lib.GemmArgs:
     g = _lib.GemmArgs()
     g.a = a.data_ptr() if a is not None else None
     g.b = b.data_ptr() if b is not None else None
@@ -155,7 +156,7 @@ def _args(a, b, c, m, n, k, *, out_dtype, block_n, group_m, num_gemm_sms, num_co
     g.ldb = int(b.stride(0)) if b is not None else int(k)
     g.ldc = int(ldc if ldc is not None else (c.stride(0) if c is not None else n))
     g.out_dtype = _tf_dtype(out_dtype)
-    g.block_m, g.block_n, g.block_k = BM, int(block_n), 64
+    g.block_m, g.block_n, g.block_k = int(block_m), int(block_n), 64
     g.group_m = int(group_m)
     g.num_gemm_sms = int(num_gemm_sms)
     g.num_comm_sms = int(num_comm_sms)
@@ -191,9 +192,12 @@ def _drive(team: Team, fn_name: str, per_rank_args: dict, ranks):
 
 # ----------------------------------------------------------------- core GEMM
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
-         out_dtype: torch.dtype = torch.bfloat16, block_n: int = 256, group_m: int = 8,
-         num_sms: int = 0, tile_map: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """C = A @ B.T on one GPU with the tcgen05 kernel (bf16 in, fp32 accumulate)."""
+         out_dtype: torch.dtype = torch.bfloat16, block_m: int = 256, block_n: int = 256,
+         group_m: int = 8, num_sms: int = 0, tile_map: torch.Tensor | None = None,
+         stream=None) -> torch.Tensor:
+    """C = A @ B.T on one GPU with the tcgen05 kernel (bf16 in, fp32 accumulate).
+    block_m=256 uses a CTA pair per tile (cta_group::2), 128 one CTA; a tile_map
+    must be expressed in tiles of block_m rows."""
     check_dtype(a, b)
     if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
         raise ValueError(f"need A [M,K], B [N,K]; got {tuple(a.shape)} and {tuple(b.shape)}")
@@ -205,7 +209,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
         out = torch.empty((m, n), dtype=out_dtype, device=a.device)
     g = _args(a, b, out, m, n, k, out_dtype=out.dtype, block_n=block_n, group_m=group_m,
               num_gemm_sms=num_sms, num_comm_sms=0, swizzle=tile_map is not None,
-              tile_map=tile_map)
+              tile_map=tile_map, block_m=block_m)
     s = stream if stream is not None else torch.cuda.current_stream(a.device)
     _lib.call("tf_gemm", C.byref(g), s.cuda_stream)
     return out
@@ -240,12 +244,13 @@ def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     for r in range(world):
         dev = devices[r]
         out = torch.empty((m, n_per_rank), dtype=odt, device=f"cuda:{dev}")
-        tm = tile_map_tensor(m, r, world, topo.nnodes, "ag_gemm", f"cuda:{dev}") if ctx.swizzle else None
+        tm = (tile_map_tensor(m, r, world, topo.nnodes, "ag_gemm", f"cuda:{dev}", ctx.hw_block_m)
+              if ctx.swizzle else None)
         a = pa.tensors[r]
         args[r] = _args(a, pb.tensors[r], out, m, n_per_rank, kp, out_dtype=odt,
                         block_n=ctx.hw_block_n, group_m=ctx.group_m,
                         num_gemm_sms=ctx.num_gemm_sms, num_comm_sms=ctx.num_comm_sms,
-                        swizzle=ctx.swizzle, tile_map=tm)
+                        swizzle=ctx.swizzle, tile_map=tm, block_m=ctx.hw_block_m)
         outs.append(out)
         keep.append(tm)
     if m_per_rank > 0 and n_per_rank > 0:
@@ -293,12 +298,13 @@ def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
     for r in range(world):
         dev = devices[r]
         out = torch.empty((mpr, n), dtype=odt, device=f"cuda:{dev}")
-        tm = tile_map_tensor(m, r, world, topo.nnodes, "gemm_rs", f"cuda:{dev}") if ctx.swizzle else None
+        tm = (tile_map_tensor(m, r, world, topo.nnodes, "gemm_rs", f"cuda:{dev}", ctx.hw_block_m)
+              if ctx.swizzle else None)
         args[r] = _args(px.tensors[r], pw.tensors[r], out, m, n, kp, out_dtype=odt,
                         block_n=ctx.hw_block_n, group_m=ctx.group_m,
                         num_gemm_sms=ctx.num_gemm_sms, num_comm_sms=ctx.num_comm_sms,
                         swizzle=ctx.swizzle, tile_map=tm, fuse_scatter=ctx.fuse_scatter,
-                        reduce_order=ctx.reduce_order)
+                        reduce_order=ctx.reduce_order, block_m=ctx.hw_block_m)
         outs.append(out)
         keep.append(tm)
     if mpr > 0 and n > 0:
@@ -332,21 +338,23 @@ class AllGatherGemm:
     in the team heap; each call is one epoch."""
 
     def __init__(self, team: Team, m: int, k: int, n_local: int, *, out_dtype=torch.bfloat16,
-                 block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
-                 swizzle: bool = True, nnodes: int = 1):
+                 block_m: int = 256, block_n: int = 256, group_m: int = 8,
+                 num_gemm_sms: int = 0, swizzle: bool = True, nnodes: int = 1):
         if k % 8:
             raise ValueError("K must be a multiple of 8")
         self.team, self.m, self.k, self.n = team, m, k, n_local
         self.out_dtype = out_dtype
-        self.block_n, self.group_m, self.num_gemm_sms = block_n, group_m, num_gemm_sms
+        self.block_m, self.block_n = block_m, block_n
+        self.group_m, self.num_gemm_sms = group_m, num_gemm_sms
         self.maps = {r: (tile_map_tensor(m, r, team.world, nnodes, "ag_gemm",
-                                         f"cuda:{team.devices[r]}") if swizzle else None)
+                                         f"cuda:{team.devices[r]}", block_m) if swizzle else None)
                      for r in team.local_ranks()}
 
     def _args(self, r, a, b, out):
         return _args(a, b, out, self.m, self.n, self.k, out_dtype=out.dtype, block_n=self.block_n,
                      group_m=self.group_m, num_gemm_sms=self.num_gemm_sms, num_comm_sms=0,
-                     swizzle=self.maps[r] is not None, tile_map=self.maps[r])
+                     swizzle=self.maps[r] is not None, tile_map=self.maps[r],
+                     block_m=self.block_m)
 
     def forward(self, a, b, out=None):
         t = self.team
@@ -371,7 +379,7 @@ class GemmReduceScatter:
     """Reusable fused GEMM+ReduceScatter for a fixed shape over a team."""
 
     def __init__(self, team: Team, m: int, k_local: int, n: int, *, out_dtype=torch.bfloat16,
-                 block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
+                 block_m: int = 256, block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
                  num_comm_sms: int = 8, swizzle: bool = True, fuse_scatter: bool = True,
                  reduce_order: str = "ascending", nnodes: int = 1):
         if k_local % 8:
@@ -380,18 +388,19 @@ class GemmReduceScatter:
             raise ValueError("M must divide evenly across ranks")
         self.team, self.m, self.k, self.n = team, m, k_local, n
         self.out_dtype = out_dtype
-        self.block_n, self.group_m = block_n, group_m
+        self.block_m, self.block_n, self.group_m = block_m, block_n, group_m
         self.num_gemm_sms, self.num_comm_sms = num_gemm_sms, num_comm_sms
         self.fuse, self.order = fuse_scatter, reduce_order
         self.maps = {r: (tile_map_tensor(m, r, team.world, nnodes, "gemm_rs",
-                                         f"cuda:{team.devices[r]}") if swizzle else None)
+                                         f"cuda:{team.devices[r]}", block_m) if swizzle else None)
                      for r in team.local_ranks()}
 
     def _args(self, r, x, w, out):
         return _args(x, w, out, self.m, self.n, self.k, out_dtype=out.dtype, block_n=self.block_n,
                      group_m=self.group_m, num_gemm_sms=self.num_gemm_sms,
                      num_comm_sms=self.num_comm_sms, swizzle=self.maps[r] is not None,
-                     tile_map=self.maps[r], fuse_scatter=self.fuse, reduce_order=self.order)
+                     tile_map=self.maps[r], fuse_scatter=self.fuse, reduce_order=self.order,
+                     block_m=self.block_m)
 
     def forward(self, x, w, out=None):
         t = self.team

@@ -44,23 +44,25 @@ def _bf16(rng, shape, scale=1.0):
     return (torch.from_numpy(rng.standard_normal(shape).astype(np.float32)) * scale).to(torch.bfloat16)
 
 
+@pytest.mark.parametrize("bm", [128, 256])
 @pytest.mark.parametrize("m,n,k,bn", [(128, 256, 64, 256), (256, 512, 1024, 256),
                                       (300, 200, 136, 128), (1000, 1000, 520, 256),
                                       (2048, 1536, 4096, 256), (64, 40, 8, 128)])
-def test_core_gemm_vs_torch_fp32(m, n, k, bn):
+def test_core_gemm_vs_torch_fp32(m, n, k, bn, bm):
     K = _k()
     rng = np.random.default_rng(m * 7 + n)
     a = _bf16(rng, (m, k)).cuda()
     b = _bf16(rng, (n, k)).cuda()
-    out = K.gemm(a, b, block_n=bn)
+    out = K.gemm(a, b, block_n=bn, block_m=bm)
     ref = a.float() @ b.float().T
     torch.cuda.synchronize()
     err = O.compare(out.float().cpu().numpy(), ref.cpu().numpy())
     assert err <= TOL_BF16, err
 
 
+@pytest.mark.parametrize("bm", [128, 256])
 @pytest.mark.parametrize("bn", [128, 256])
-def test_core_gemm_exact_lattice_fp32_out(bn):
+def test_core_gemm_exact_lattice_fp32_out(bn, bm):
     K = _k()
     rng = np.random.default_rng(bn)
     m, n, k = 512, 768, 2048
@@ -68,7 +70,7 @@ def test_core_gemm_exact_lattice_fp32_out(bn):
     b = rng.integers(-8, 8, (n, k))
     ta = torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).cuda()
     tb = torch.from_numpy(b.astype(np.float32)).to(torch.bfloat16).cuda()
-    out = K.gemm(ta, tb, out_dtype=torch.float32, block_n=bn)
+    out = K.gemm(ta, tb, out_dtype=torch.float32, block_n=bn, block_m=bm)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().astype(np.int64), a @ b.T)
 
@@ -80,32 +82,35 @@ def test_core_gemm_persistent_grid_and_tile_map_order_irrelevant():
     a = _bf16(rng, (m, k)).cuda()
     b = _bf16(rng, (n, k)).cuda()
     base = K.gemm(a, b)
-    tm = K.tile_map_tensor(m, 3, 8, 1, "ag_gemm", "cuda")
-    for sms in (1, 3, 148):
-        out = K.gemm(a, b, num_sms=sms, tile_map=tm, group_m=3)
-        torch.cuda.synchronize()
-        assert torch.equal(out, base)
+    for bm in (128, 256):
+        tm = K.tile_map_tensor(m, 3, 8, 1, "ag_gemm", "cuda", bm)
+        for sms in (1, 3, 148):
+            out = K.gemm(a, b, num_sms=sms, tile_map=tm, group_m=3, block_m=bm)
+            torch.cuda.synchronize()
+            assert torch.equal(out, base)
 
 
+@pytest.mark.parametrize("bm", [128, 256])
 @pytest.mark.parametrize("case", range(12))
-def test_ag_gemm_exact_vs_reference_fixture(case):
+def test_ag_gemm_exact_vs_reference_fixture(case, bm):
     K = _k()
     c = G.workloads()[case]
     w = c["world"]
-    run = K.ag_gemm(list(c["ag_a"]), list(c["ag_b"]), _ctx(w))
+    run = K.ag_gemm(list(c["ag_a"]), list(c["ag_b"]), _ctx(w, block_m=bm))
     for r in range(w):
         assert run.outputs[r].dtype == np.int64
         assert np.array_equal(run.outputs[r], c["ag_c"][r]), (case, r)
 
 
 @pytest.mark.parametrize("case", range(12))
-@pytest.mark.parametrize("variant", ["fused_asc", "fused_ring", "unfused"])
+@pytest.mark.parametrize("variant", ["fused_asc", "fused_ring", "unfused", "fused_pair"])
 def test_gemm_rs_exact_vs_reference_fixture(case, variant):
     K = _k()
     c = G.workloads()[case]
     w = c["world"]
     ctx = _ctx(w, fuse_scatter=variant.startswith("fused"),
-               reduce_order="ring" if variant == "fused_ring" else "ascending")
+               reduce_order="ring" if variant == "fused_ring" else "ascending",
+               block_m=256 if variant == "fused_pair" else 128)
     run = K.gemm_rs(list(c["rs_x"]), list(c["rs_w"]), ctx)
     for r in range(w):
         assert np.array_equal(run.outputs[r], c["rs_y"][r]), (case, variant, r)
@@ -124,14 +129,15 @@ def test_config1_ag_gemm_world2_1024_exact_digest():
         assert hashlib.sha256(o.astype(np.int64).tobytes()).hexdigest() == meta["sha256_per_rank"][r]
 
 
+@pytest.mark.parametrize("bm", [128, 256])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_ag_gemm_bf16_production_tolerance(world):
+def test_ag_gemm_bf16_production_tolerance(world, bm):
     K = _k()
     rng = np.random.default_rng(world)
     mpr, n, k = 256, 384, 1024
     a = [_bf16(rng, (mpr, k)).cuda() for _ in range(world)]
     b = [_bf16(rng, (n, k), 1 / 32).cuda() for _ in range(world)]
-    run = K.ag_gemm(a, b, _ctx(world))
+    run = K.ag_gemm(a, b, _ctx(world, block_m=bm))
     ref = O.ref_allgather_gemm([x.float().cpu().numpy() for x in a],
                                [x.float().cpu().numpy() for x in b])
     for r in range(world):
@@ -139,15 +145,16 @@ def test_ag_gemm_bf16_production_tolerance(world):
         assert O.compare(run.outputs[r].float().cpu().numpy(), ref[r]) <= TOL_BF16
 
 
+@pytest.mark.parametrize("bm", [128, 256])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("fused", [True, False])
-def test_gemm_rs_bf16_production_tolerance(world, fused):
+def test_gemm_rs_bf16_production_tolerance(world, fused, bm):
     K = _k()
     rng = np.random.default_rng(world + 10 * fused)
     m, n, k = world * 128, 512, 768
     x = [_bf16(rng, (m, k)).cuda() for _ in range(world)]
     w = [_bf16(rng, (n, k), 1 / 32).cuda() for _ in range(world)]
-    run = K.gemm_rs(x, w, _ctx(world, fuse_scatter=fused))
+    run = K.gemm_rs(x, w, _ctx(world, fuse_scatter=fused, block_m=bm))
     ref = O.ref_reduce_scatter([t.float().cpu().numpy() for t in x],
                                [t.float().cpu().numpy() for t in w])
     for r in range(world):
