@@ -173,28 +173,55 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
                void* comm_stream);
 
 /* ------------------------------------------------------------------ MoE (expert parallel)
- * Routing (not in the reference; deterministic rule documented in DESIGN.md):
- * per token top-k of logits (descending, ties to lower expert id), weights =
- * softmax of the selected logits. */
+ * Not in the reference as an all-to-all; what the reference pins
+ * is the layout: the [world, E] routing-count matrix (ag_moe.py:28-33) and the
+ * expert-major, then source-rank, then source-order receive layout
+ * (gather_tokens_by_expert, oracles.py:38-50).  Rank d owns experts
+ * [d*E/world, (d+1)*E/world).
+ *
+ * Routing: top-k of logits per token, descending, ties to the lower expert id;
+ * weights = softmax of the selected logits (fp32). */
 int tf_moe_topk(const float* logits, int64_t tokens, int n_experts, int k, int32_t* topk_idx,
                 float* topk_w, void* stream);
-/* Count matrix row for this rank: counts[e] = #(token,slot) routed to e
- * (the [world, E] routing matrix convention, ag_moe.py:28-33), plus the
- * per-(token,slot) position inside the rank's expert-sorted chunk. */
-int tf_moe_count(const int32_t* topk_idx, int64_t tokens, int k, int n_experts,
-                 int32_t* counts, int32_t* sorted_pos, void* stream);
-/* Dispatch (EP all-to-all): scatter this rank's token rows to the receive
- * buffers of the ranks owning each routed expert.  Receive layout on rank d:
- * expert-major, then source rank, then source order (gather_tokens_by_expert,
- * oracles.py:38-50).  all_counts is the device [world, E] matrix (int32). */
-int tf_moe_dispatch(tf_team* t, int rank, const void* x, int64_t tokens, int64_t hidden,
-                    const int32_t* topk_idx, int k, int n_experts, const int32_t* all_counts,
-                    const int32_t* sorted_pos, uint64_t recv_off, int phase, void* stream);
-/* Combine: out[t] = sum_j w[t,j] * y_owner[row(t,j)] (fp32, slot order), bf16 out. */
-int tf_moe_combine(tf_team* t, int rank, uint64_t expert_out_off, int64_t hidden,
-                   const int32_t* topk_idx, const float* topk_w, int64_t tokens, int k,
-                   int n_experts, const int32_t* all_counts, const int32_t* sorted_pos,
-                   void* out, int phase, void* stream);
+/* This rank's routing row and send order: counts[e] = #(token, slot) routed to
+ * expert e; sorted_pos[t*k+j] = position of (t, j) in the rank's expert-sorted
+ * chunk (stable: expert, then token, then slot).  Deterministic (no atomics
+ * decide positions).  scratch: >= tf_moe_count_scratch_bytes(tokens*k, n_experts). */
+int64_t tf_moe_count_scratch_bytes(int64_t entries, int n_experts);
+int tf_moe_count(const int32_t* topk_idx, int64_t tokens, int k, int n_experts, int32_t* counts,
+                 int32_t* sorted_pos, void* scratch, void* stream);
+
+typedef struct tf_moe_args {
+  int64_t tokens;         /* T: tokens on this rank */
+  int64_t hidden;         /* H (multiple of 8) */
+  int32_t k;              /* top-k */
+  int32_t n_experts;      /* E, divisible by world */
+  int64_t max_recv;       /* receive capacity in rows on every rank */
+  const void* x;          /* [T, H] bf16 dispatch input */
+  const int32_t* topk_idx;/* [T, k] */
+  const float* topk_w;    /* [T, k] combine weights */
+  void* out;              /* [T, H] bf16 combine output */
+  int32_t* counts;        /* [world, E] device: full routing matrix (filled by dispatch) */
+  int32_t* sorted_pos;    /* [T, k] device: from tf_moe_count */
+  int32_t* dest_row;      /* [T, k] device: receive row of (t, j) on its owner (filled by dispatch) */
+  int64_t* recv_rows;     /* [1] device: rows received by this rank (filled by dispatch) */
+} tf_moe_args;
+
+/* Device pointers of this rank's receive buffer [max_recv, H] bf16 and expert
+ * output buffer [max_recv, H] bf16 inside the symmetric heap. */
+int tf_moe_buffers(tf_team* t, int rank, const tf_moe_args* a, void** recv, void** expert_out);
+/* Dispatch (EP all-to-all):
+ *   PRE  = routing counts + send order of this rank (as tf_moe_count, into
+ *          a->sorted_pos), count row pushed to every peer's matrix + flag;
+ *   MAIN = wait for all rows, copy the full matrix to a->counts, compute
+ *          a->dest_row / a->recv_rows, 16-byte vector scatter of token rows into
+ *          the owners' receive buffers, release a per-source flag on each owner;
+ *   POST = wait until every source has delivered to this rank. */
+int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream);
+/* Combine: PRE = announce this rank's expert outputs ready; MAIN = wait all
+ * owners, pull the k expert rows of every token over NVLink and reduce
+ * out[t] = sum_j w[t,j] * y[row(t,j)] in fp32 (slot order), bf16 out. */
+int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream);
 
 #ifdef __cplusplus
 }

@@ -36,6 +36,14 @@ class GemmArgs(C.Structure):
     ]
 
 
+class MoeArgs(C.Structure):
+    _fields_ = [
+        ("tokens", i64), ("hidden", i64), ("k", i32), ("n_experts", i32), ("max_recv", i64),
+        ("x", vp), ("topk_idx", vp), ("topk_w", vp), ("out", vp), ("counts", vp),
+        ("sorted_pos", vp), ("dest_row", vp), ("recv_rows", vp),
+    ]
+
+
 _SIGS = {
     "tf_last_error": (C.c_char_p, []),
     "tf_version": (C.c_char_p, []),
@@ -68,9 +76,11 @@ _SIGS = {
     "tf_ag_gemm": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_gemm_rs": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_moe_topk": (ci, [vp, i64, ci, ci, vp, vp, vp]),
-    "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp]),
-    "tf_moe_dispatch": (ci, [vp, ci, vp, i64, i64, vp, ci, ci, vp, vp, u64, ci, vp]),
-    "tf_moe_combine": (ci, [vp, ci, u64, i64, vp, vp, i64, ci, ci, vp, vp, vp, ci, vp]),
+    "tf_moe_count_scratch_bytes": (i64, [i64, ci]),
+    "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp, vp]),
+    "tf_moe_buffers": (ci, [vp, ci, C.POINTER(MoeArgs), C.POINTER(vp), C.POINTER(vp)]),
+    "tf_moe_dispatch": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
+    "tf_moe_combine": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
 }
 
 _lib = None
@@ -79,7 +89,7 @@ _lib = None
 def header_symbols() -> list[str]:
     """Every function the public header declares."""
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(tf_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tf_\w+)\s*\(", text, re.M)))
 
 
 def lib() -> C.CDLL:

@@ -1,24 +1,487 @@
-// Expert-parallel MoE routing / dispatch / combine (filled in below the GEMM milestone).
+// Expert-parallel MoE: routing, counts/offsets, dispatch and combine.
+//
+// The reference has no all-to-all -- its MoE path is AllGather +
+// grouped GEMM (ovs/kernels/ag_moe.py:20-158).  What it pins, and what this
+// file keeps bit-exact, is the layout:
+//   * routing counts are a [world, E] matrix, entry (s, e) = rows source rank s
+//     sends to expert e (ag_moe.py:28-33);
+//   * a rank's chunk is grouped by expert, then keeps source order
+//     (ag_moe.py:_pull_engine, oracles.py:38-50);
+//   * the receive side is expert-major, then source rank, then source order
+//     (gather_tokens_by_expert, oracles.py:38-50).
+// Rank d owns experts [d*E/w, (d+1)*E/w).
+//
+// Kernels
+//   topk_kernel        warp per token: k rounds of warp argmax (ties -> lower id)
+//   hist / scan / rank deterministic stable send order: chunk histograms in smem,
+//                      per-expert exclusive scan over chunks, in-chunk ranks via
+//                      __match_any_sync + per-warp prefix -- no atomic decides a
+//                      position, so counts, offsets and layout are bit-exact
+//   layout_kernel      per-expert destination segment base on the owner
+//   scatter_kernel     warp per (token, slot): 16-byte vector copy of the token
+//                      row straight into the owner's receive buffer (NVLink P2P
+//                      stores for remote owners)
+//   combine_kernel     warp per token: pulls the k expert rows (16-byte loads,
+//                      k loads in flight per lane), fp32 weighted sum in slot
+//                      order, bf16 out
 #include <cuda_runtime.h>
 
+#include <string>
+
 #include "tf_internal.h"
+#include "tf_ptx.cuh"
 #include "tf_team.h"
+
+namespace tf {
+namespace {
+
+constexpr int kChunk = 1024;  // (token, slot) entries per ranking chunk
+
+// ---------------------------------------------------------------- routing
+__global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, int E, int k,
+                            int32_t* __restrict__ idx, float* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= tokens) return;
+  const float* row = logits + t * E;
+  uint32_t taken = 0;  // bit c: expert lane + 32*c already selected (E <= 1024)
+  float sel_val[16];
+  int sel_idx[16];
+  for (int r = 0; r < k; ++r) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int e = lane, c = 0; e < E; e += 32, ++c) {
+      if (taken & (1u << c)) continue;
+      const float v = row[e];
+      if (v > best || (v == best && e < bi)) { best = v; bi = e; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+    sel_val[r] = best;
+    sel_idx[r] = bi;
+  }
+  if (lane == 0) {
+    float z = 0.f;
+    for (int r = 0; r < k; ++r) z += __expf(sel_val[r] - sel_val[0]);
+    for (int r = 0; r < k; ++r) {
+      idx[t * k + r] = sel_idx[r];
+      w[t * k + r] = __expf(sel_val[r] - sel_val[0]) / z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- stable counting
+__global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t entries, int E,
+                            int32_t* __restrict__ chunk_hist /* [nchunks][E] */) {
+  extern __shared__ int32_t h[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) h[e] = 0;
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kChunk;
+  for (int i = threadIdx.x; i < kChunk; i += blockDim.x) {
+    const int64_t g = base + i;
+    if (g < entries) {
+      const int e = idx[g];
+      if (e >= 0 && e < E) atomicAdd(&h[e], 1);  // order-independent count
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_hist[static_cast<int64_t>(blockIdx.x) * E + e] = h[e];
+}
+
+// one block: per-expert exclusive scan over chunks, totals, and expert bases
+__global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E,
+                            int32_t* __restrict__ counts, int32_t* __restrict__ expert_base) {
+  extern __shared__ int32_t tot[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int32_t v = chunk_hist[static_cast<int64_t>(c) * E + e];
+      chunk_hist[static_cast<int64_t>(c) * E + e] = run;
+      run += v;
+    }
+    tot[e] = run;
+    counts[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;
+    for (int e = 0; e < E; ++e) {
+      expert_base[e] = run;
+      run += tot[e];
+    }
+  }
+}
+
+// 1024 threads: entry i of the chunk; rank among same-expert entries before it.
+__global__ void __launch_bounds__(kChunk) rank_kernel(const int32_t* __restrict__ idx,
+                                                      int64_t entries, int E,
+                                                      const int32_t* __restrict__ chunk_off,
+                                                      const int32_t* __restrict__ expert_base,
+                                                      int32_t* __restrict__ sorted_pos) {
+  extern __shared__ int32_t wc[];  // [32 warps][E]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wc[i] = 0;
+  __syncthreads();
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * kChunk + threadIdx.x;
+  const int e = g < entries ? idx[g] : -1;
+  const unsigned same = __match_any_sync(0xffffffffu, e);
+  const int in_warp = __popc(same & ((1u << lane) - 1));
+  if (e >= 0 && in_warp == 0) wc[warp * E + e] = __popc(same);
+  __syncthreads();
+  if (e >= 0) {
+    int before = 0;
+    for (int w2 = 0; w2 < warp; ++w2) before += wc[w2 * E + e];
+    sorted_pos[g] = expert_base[e] + chunk_off[static_cast<int64_t>(blockIdx.x) * E + e] + before +
+                    in_warp;
+  }
+}
+
+// ---------------------------------------------------------------- exchange / layout
+struct PeerPtrs {
+  void* p[kMaxWorld];
+};
+struct PeerSig {
+  uint64_t* p[kMaxWorld];
+};
+
+// push this rank's count row into every peer's matrix, then release its flag
+__global__ void push_counts_kernel(const int32_t* __restrict__ row, int E, PeerPtrs mats,
+                                   PeerSig flags, int world, int rank, uint64_t epoch) {
+  for (int p = 0; p < world; ++p) {
+    int32_t* dst = static_cast<int32_t*>(mats.p[p]) + static_cast<int64_t>(rank) * E;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) dst[e] = row[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < world) {
+    fence_sys();
+    st_release_sys(flags.p[threadIdx.x] + rank, epoch);
+  }
+}
+
+__global__ void wait_flags_kernel(const uint64_t* flags, int n, uint64_t epoch, uint64_t timeout_ns,
+                                  unsigned long long* err, unsigned long long tag) {
+  const int i = threadIdx.x;
+  if (i < n) wait_geq_sys(flags + i, epoch, timeout_ns, err, tag | i);
+  __syncthreads();
+}
+
+// seg_base[e] = start row, on e's owner, of the segment (expert e, source `rank`)
+__global__ void layout_kernel(const int32_t* __restrict__ mat /* [world][E] */, int world, int E,
+                              int rank, int32_t* __restrict__ seg_base,
+                              int32_t* __restrict__ counts_out, int64_t* __restrict__ recv_rows) {
+  const int epr = E / world;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int owner = e / epr;
+    int64_t base = 0;
+    for (int e2 = owner * epr; e2 < e; ++e2)
+      for (int s = 0; s < world; ++s) base += mat[s * E + e2];
+    for (int s = 0; s < rank; ++s) base += mat[s * E + e];
+    seg_base[e] = static_cast<int32_t>(base);
+  }
+  for (int i = threadIdx.x; i < world * E; i += blockDim.x) counts_out[i] = mat[i];
+  if (threadIdx.x == 0) {
+    int64_t tot = 0;
+    for (int e = rank * epr; e < (rank + 1) * epr; ++e)
+      for (int s = 0; s < world; ++s) tot += mat[s * E + e];
+    *recv_rows = tot;
+  }
+}
+
+// warp per (token, slot): 16-byte vector copy of x[t] into the owner's receive row
+__global__ void __launch_bounds__(256) scatter_kernel(
+    const uint4* __restrict__ x, int64_t tokens, int64_t vec_per_row, int k, int E, int world,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ sorted_pos,
+    const int32_t* __restrict__ expert_base, const int32_t* __restrict__ seg_base,
+    int32_t* __restrict__ dest_row, PeerPtrs recv, int64_t max_recv, unsigned long long* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int epr = E / world;
+  for (int64_t wi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       wi < tokens * k; wi += nwarps) {
+    const int64_t t = wi / k;
+    const int e = idx[wi];
+    const int owner = e / epr;
+    const int64_t row = static_cast<int64_t>(seg_base[e]) + (sorted_pos[wi] - expert_base[e]);
+    if (lane == 0) dest_row[wi] = static_cast<int32_t>(row);
+    if (row >= max_recv) {
+      if (lane == 0 && err) atomicCAS(err, 0ull, 0x5000000ull | 0xFFFFFFull);
+      continue;
+    }
+    const uint4* src = x + t * vec_per_row;
+    uint4* dst = static_cast<uint4*>(recv.p[owner]) + row * vec_per_row;
+    int64_t v = lane;
+    for (; v + 96 < vec_per_row; v += 128) {  // 4 independent 16-byte loads in flight per lane
+      const uint4 a0 = __ldg(src + v), a1 = __ldg(src + v + 32), a2 = __ldg(src + v + 64),
+                  a3 = __ldg(src + v + 96);
+      dst[v] = a0; dst[v + 32] = a1; dst[v + 64] = a2; dst[v + 96] = a3;
+    }
+    for (; v < vec_per_row; v += 32) dst[v] = __ldg(src + v);
+  }
+}
+
+// after the scatter kernel (stream order): release "source `rank` delivered" on every owner
+__global__ void release_kernel(PeerSig flags, int world, int rank, uint64_t epoch) {
+  if (threadIdx.x < world) {
+    fence_sys();
+    st_release_sys(flags.p[threadIdx.x] + rank, epoch);
+  }
+}
+
+// warp per token; hidden in 256-element chunks (8 bf16 = 16 bytes per lane)
+__global__ void __launch_bounds__(256) combine_kernel(
+    int64_t tokens, int64_t vec_per_row, int k, int E, int world,
+    const int32_t* __restrict__ idx, const float* __restrict__ w,
+    const int32_t* __restrict__ dest_row, PeerPtrs yout, uint4* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int epr = E / world;
+  for (int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < tokens;
+       t += nwarps) {
+    const uint4* rows[16];
+    float wt[16];
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[t * k + j];
+      rows[j] = static_cast<const uint4*>(yout.p[e / epr]) +
+                static_cast<int64_t>(dest_row[t * k + j]) * vec_per_row;
+      wt[j] = w[t * k + j];
+    }
+    for (int64_t v = lane; v < vec_per_row; v += 32) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint4 val[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < k) val[j] = rows[j][v];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < k) {
+          const uint32_t u[4] = {val[j].x, val[j].y, val[j].z, val[j].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[2 * q] = fmaf(wt[j], __uint_as_float(u[q] << 16), acc[2 * q]);
+            acc[2 * q + 1] = fmaf(wt[j], __uint_as_float(u[q] & 0xFFFF0000u), acc[2 * q + 1]);
+          }
+        }
+      }
+      out[t * vec_per_row + v] =
+          make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                     pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    }
+  }
+}
+
+int64_t count_scratch_bytes(int64_t entries, int E) {
+  const int64_t nchunks = (entries + kChunk - 1) / kChunk;
+  return (std::max<int64_t>(nchunks, 1) * E + E) * 4 + 256;
+}
+
+// counts[e], ebase[e] (exclusive scan of counts) and the stable send positions
+int run_count(const int32_t* idx, int64_t entries, int E, int32_t* counts, int32_t* sorted_pos,
+              void* scratch, int32_t* ebase, cudaStream_t s) {
+  const int nchunks = static_cast<int>(std::max<int64_t>((entries + kChunk - 1) / kChunk, 1));
+  int32_t* chunk = static_cast<int32_t*>(scratch);
+  if (!ebase) ebase = chunk + static_cast<int64_t>(nchunks) * E;
+  if (static_cast<size_t>(32) * E * 4 > 227 * 1024) return fail(TF_ERR_CONFIG, "too many experts");
+  hist_kernel<<<nchunks, 256, E * 4, s>>>(idx, entries, E, chunk);
+  scan_kernel<<<1, 1024, E * 4, s>>>(chunk, nchunks, E, counts, ebase);
+  if (entries > 0) {
+    const size_t sm = static_cast<size_t>(32) * E * 4;
+    static bool attr = false;
+    if (!attr && sm > 48 * 1024) {
+      TF_CUDA_TRY(cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+      attr = true;
+    }
+    rank_kernel<<<nchunks, kChunk, sm, s>>>(idx, entries, E, chunk, ebase, sorted_pos);
+  }
+  TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}
+
+// Per-PE workspace: count matrix [w][E] (peers write their rows), this PE's
+// expert bases [E] and destination segment bases [E], receive buffer and
+// expert-output buffer ([max_recv][H] bf16 each).
+struct MoeWs {
+  Workspace* ws;
+  size_t mat_off, ebase_off, seg_off, recv_off, yout_off;
+};
+
+int moe_workspace(tf_team* t, const tf_moe_args* a, MoeWs* out) {
+  const int w = t->world;
+  const size_t mat = (static_cast<size_t>(w) * a->n_experts * 4 + 1023) / 1024 * 1024;
+  const size_t vec = (static_cast<size_t>(a->n_experts) * 4 + 1023) / 1024 * 1024;
+  const size_t buf = (static_cast<size_t>(a->max_recv) * a->hidden * 2 + 1023) / 1024 * 1024;
+  const std::string key = "moe:" + std::to_string(a->n_experts) + "x" + std::to_string(a->hidden) +
+                          "x" + std::to_string(a->max_recv);
+  int rc = TF_OK;
+  Workspace* ws = t->workspace(key, mat + 2 * vec + 2 * buf, 3 * static_cast<size_t>(w), &rc);
+  if (!ws) return rc;
+  out->ws = ws;
+  out->mat_off = ws->data_off;
+  out->ebase_off = ws->data_off + mat;
+  out->seg_off = out->ebase_off + vec;
+  out->recv_off = out->seg_off + vec;
+  out->yout_off = out->recv_off + buf;
+  return TF_OK;
+}
+
+int check_moe(tf_team* t, int rank, const tf_moe_args* a) {
+  if (!t || !a) return fail(TF_ERR_INVALID, "NULL argument");
+  if (rank < 0 || rank >= t->world) return fail(TF_ERR_INVALID, "rank out of range");
+  if (!t->is_local(rank)) return fail(TF_ERR_INVALID, "rank is not owned by this process");
+  if (a->n_experts < 1 || a->n_experts % t->world)
+    return fail(TF_ERR_INVALID, "n_experts must be >= 1 and divisible by world");
+  if (a->k < 1 || a->k > 16 || a->k > a->n_experts) return fail(TF_ERR_INVALID, "need 1 <= k <= min(16, E)");
+  if (a->hidden < 8 || a->hidden % 8) return fail(TF_ERR_INVALID, "hidden must be a positive multiple of 8");
+  if (a->tokens < 0 || a->max_recv < 0) return fail(TF_ERR_INVALID, "negative size");
+  return TF_OK;
+}
+
+int grid_for(int64_t warps) {
+  int64_t blocks = (warps * 32 + 255) / 256;
+  const int cap = num_sms_of_current_device() * 8;
+  if (blocks > cap) blocks = cap;
+  return static_cast<int>(std::max<int64_t>(blocks, 1));
+}
+
+}  // namespace
+}  // namespace tf
 
 using tf::fail;
 
 extern "C" {
-int tf_moe_topk(const float*, int64_t, int, int, int32_t*, float*, void*) {
-  return fail(TF_ERR_CONFIG, "tf_moe_topk: not built yet");
+
+int tf_moe_topk(const float* logits, int64_t tokens, int n_experts, int k, int32_t* topk_idx,
+                float* topk_w, void* stream) {
+  if (n_experts < 1 || n_experts > 1024) return fail(TF_ERR_INVALID, "1 <= n_experts <= 1024");
+  if (k < 1 || k > 16 || k > n_experts) return fail(TF_ERR_INVALID, "need 1 <= k <= min(16, E)");
+  if (tokens <= 0) return TF_OK;
+  const int64_t threads = tokens * 32;
+  tf::topk_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0,
+                    static_cast<cudaStream_t>(stream)>>>(logits, tokens, n_experts, k, topk_idx,
+                                                         topk_w);
+  TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
 }
-int tf_moe_count(const int32_t*, int64_t, int, int, int32_t*, int32_t*, void*) {
-  return fail(TF_ERR_CONFIG, "tf_moe_count: not built yet");
+
+int64_t tf_moe_count_scratch_bytes(int64_t entries, int n_experts) {
+  return tf::count_scratch_bytes(entries, n_experts);
 }
-int tf_moe_dispatch(tf_team*, int, const void*, int64_t, int64_t, const int32_t*, int, int,
-                    const int32_t*, const int32_t*, uint64_t, int, void*) {
-  return fail(TF_ERR_CONFIG, "tf_moe_dispatch: not built yet");
+
+int tf_moe_count(const int32_t* topk_idx, int64_t tokens, int k, int n_experts, int32_t* counts,
+                 int32_t* sorted_pos, void* scratch, void* stream) {
+  if (n_experts < 1) return fail(TF_ERR_INVALID, "n_experts must be >= 1");
+  if (tokens < 0 || k < 1) return fail(TF_ERR_INVALID, "bad tokens/k");
+  if (!scratch) return fail(TF_ERR_INVALID, "scratch is NULL");
+  return tf::run_count(topk_idx, tokens * k, n_experts, counts, sorted_pos, scratch, nullptr,
+                       static_cast<cudaStream_t>(stream));
 }
-int tf_moe_combine(tf_team*, int, uint64_t, int64_t, const int32_t*, const float*, int64_t, int,
-                   int, const int32_t*, const int32_t*, void*, int, void*) {
-  return fail(TF_ERR_CONFIG, "tf_moe_combine: not built yet");
+
+int tf_moe_buffers(tf_team* t, int rank, const tf_moe_args* a, void** recv, void** expert_out) {
+  int rc = tf::check_moe(t, rank, a);
+  if (rc) return rc;
+  tf::MoeWs m;
+  rc = tf::moe_workspace(t, a, &m);
+  if (rc) return rc;
+  if (recv) *recv = t->pes[rank].base + m.recv_off;
+  if (expert_out) *expert_out = t->pes[rank].base + m.yout_off;
+  return TF_OK;
 }
+
+int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream) {
+  int rc = tf::check_moe(t, rank, a);
+  if (rc) return rc;
+  tf::MoeWs m;
+  rc = tf::moe_workspace(t, a, &m);
+  if (rc) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int w = t->world, E = a->n_experts;
+  const int64_t entries = a->tokens * a->k;
+  const size_t sig = m.ws->sig_base;  // [0,w) counts ready, [w,2w) delivered, [2w,3w) outputs ready
+  const int dev = t->pes[rank].device;
+  int32_t* ebase = reinterpret_cast<int32_t*>(t->pes[rank].base + m.ebase_off);
+  int32_t* seg_base = reinterpret_cast<int32_t*>(t->pes[rank].base + m.seg_off);
+  if (phase & TF_PHASE_PRE) {
+    const uint64_t e = ++m.ws->epoch[rank];
+    // count into this rank's own row of its local matrix, then push the row to all peers
+    int32_t* own_row = reinterpret_cast<int32_t*>(t->pes[rank].base + m.mat_off) +
+                       static_cast<int64_t>(rank) * E;
+    void* chunk = t->scratch(dev, tf::count_scratch_bytes(entries, E));
+    if (!chunk) return fail(TF_ERR_ALLOC, "cannot allocate MoE count scratch");
+    rc = tf::run_count(a->topk_idx, entries, E, own_row, a->sorted_pos, chunk, ebase, s);
+    if (rc) return rc;
+    tf::PeerPtrs mats{};
+    tf::PeerSig flags{};
+    for (int p = 0; p < w; ++p) {
+      mats.p[p] = t->pes[p].base + m.mat_off;
+      flags.p[p] = t->pes[p].sig + sig;
+    }
+    tf::push_counts_kernel<<<1, 256, 0, s>>>(own_row, E, mats, flags, w, rank, e);
+    TF_CUDA_TRY(cudaGetLastError());
+  }
+  if (phase & TF_PHASE_MAIN) {
+    const uint64_t e = m.ws->epoch[rank];
+    tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e, t->timeout_ns,
+                                                             t->err_word(rank), 0x5000000ull);
+    const int32_t* mat = reinterpret_cast<const int32_t*>(t->pes[rank].base + m.mat_off);
+    tf::layout_kernel<<<1, 256, 0, s>>>(mat, w, E, rank, seg_base, a->counts, a->recv_rows);
+    tf::PeerPtrs recv{};
+    tf::PeerSig flags{};
+    for (int p = 0; p < w; ++p) {
+      recv.p[p] = t->pes[p].base + m.recv_off;
+      flags.p[p] = t->pes[p].sig + sig + w;
+    }
+    if (entries > 0)
+      tf::scatter_kernel<<<tf::grid_for(entries), 256, 0, s>>>(
+          static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
+          a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank));
+    tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
+    TF_CUDA_TRY(cudaGetLastError());
+  }
+  if (phase & TF_PHASE_POST) {
+    const uint64_t e = m.ws->epoch[rank];
+    tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig + w, w, e,
+                                                             t->timeout_ns, t->err_word(rank),
+                                                             0x5100000ull);
+    TF_CUDA_TRY(cudaGetLastError());
+  }
+  return TF_OK;
 }
+
+int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream) {
+  int rc = tf::check_moe(t, rank, a);
+  if (rc) return rc;
+  tf::MoeWs m;
+  rc = tf::moe_workspace(t, a, &m);
+  if (rc) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int w = t->world;
+  const size_t sig = m.ws->sig_base + 2 * w;
+  const uint64_t e = m.ws->epoch[rank];  // same epoch as the dispatch it answers
+  if (phase & TF_PHASE_PRE) {
+    tf::PeerSig flags{};
+    for (int p = 0; p < w; ++p) flags.p[p] = t->pes[p].sig + sig;
+    tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
+    TF_CUDA_TRY(cudaGetLastError());
+  }
+  if (phase & TF_PHASE_MAIN) {
+    tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e,
+                                                             t->timeout_ns, t->err_word(rank),
+                                                             0x5200000ull);
+    tf::PeerPtrs y{};
+    for (int p = 0; p < w; ++p) y.p[p] = t->pes[p].base + m.yout_off;
+    if (a->tokens > 0)
+      tf::combine_kernel<<<tf::grid_for(a->tokens), 256, 0, s>>>(
+          a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
+          static_cast<uint4*>(a->out));
+    TF_CUDA_TRY(cudaGetLastError());
+  }
+  return TF_OK;
+}
+
+}  // extern "C"

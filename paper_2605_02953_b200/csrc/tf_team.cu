@@ -84,17 +84,6 @@ StreamWriteFn get_stream_write_fn() {
   return fn;
 }
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
 }  // namespace
 
 // stream-ordered signal store (copy-engine friendly: no kernel when the driver
@@ -135,6 +124,20 @@ int team_barrier_wait(tf_team* t, int rank, cudaStream_t s) {
 
 using tf::fail;
 
+void* tf_team::scratch(int device, size_t bytes) {
+  auto it = scratch_bufs.find(device);
+  if (it != scratch_bufs.end() && it->second.second >= bytes) return it->second.first;
+  tf::DeviceGuard g(device);
+  if (it != scratch_bufs.end()) {
+    cudaDeviceSynchronize();
+    cudaFree(it->second.first);
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  scratch_bufs[device] = {p, bytes};
+  return p;
+}
+
 unsigned long long* tf_team::err_word(int pe) {
   return reinterpret_cast<unsigned long long*>(pes[pe].sig + world);
 }
@@ -156,6 +159,7 @@ tf::Workspace* tf_team::workspace(const std::string& key, size_t data_bytes, siz
     *rc = tf::fail(TF_ERR_ALLOC, "signal space exhausted creating workspace '" + key + "'");
     return nullptr;
   }
+  w.epoch.assign(world, 0);
   w.data_off = off;
   w.data_bytes = data_bytes;
   w.sig_base = sig_top;
@@ -321,6 +325,10 @@ int tf_team_destroy(tf_team* t) {
   for (auto& kv : t->dev_tables) {
     tf::DeviceGuard g(kv.first);
     cudaFree(kv.second);
+  }
+  for (auto& kv : t->scratch_bufs) {
+    tf::DeviceGuard g(kv.first);
+    cudaFree(kv.second.first);
   }
   delete t;
   return TF_OK;

@@ -23,9 +23,21 @@ struct PE {
 struct Workspace {
   size_t data_off = 0, data_bytes = 0;
   size_t sig_base = 0, sig_slots = 0;
+  std::vector<uint64_t> epoch;  // per-rank call epoch of this workspace's protocol
 };
 
 const char* last_error_cstr();
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 }  // namespace tf
 
@@ -44,7 +56,10 @@ struct tf_team {
   std::map<std::string, tf::Workspace> workspaces;
   std::map<int, void*> dev_tables;  // per-device scratch (freed at destroy)
 
+  std::map<int, std::pair<void*, size_t>> scratch_bufs;  // per-device private scratch
+
   unsigned long long* err_word(int pe);
+  void* scratch(int device, size_t bytes);
   tf::Workspace* workspace(const std::string& key, size_t data_bytes, size_t sig_slots, int* rc);
   bool is_local(int pe) const { return !ipc || pe == my_rank; }
 };
