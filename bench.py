@@ -42,7 +42,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--group-m", type=int, default=int(os.environ.get("TF_GROUP_M", "16")))
+    p.add_argument("--group-m", type=int, default=int(os.environ.get("TF_GROUP_M", "8")))
+    p.add_argument("--no-moe", action="store_true")
     return p.parse_args()
 
 
@@ -166,6 +167,74 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ MoE EP (config 4)
+MOE_E, MOE_K, MOE_H, MOE_T = 256, 8, 7168, 4096
+
+
+def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed, peaks):
+    """DeepSeek-V3-like EP dispatch + combine: 256 experts, top-8, hidden 7168,
+    4096 tokens/rank, EP = number of GPUs.  Routing from N(0,1) logits through
+    the device top-k; expert compute excluded (expert outputs = received rows)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_02953_b200 import moe as M
+    g = torch.Generator(device="cpu").manual_seed(4321 + rank)
+    x = torch.randn(MOE_T, MOE_H, generator=g).to(torch.bfloat16).to(f"cuda:{dev}")
+    logits = torch.randn(MOE_T, MOE_E, generator=g).to(f"cuda:{dev}")
+    ep = M.ExpertParallelMoE(team, MOE_E, MOE_H, MOE_K, max_tokens=MOE_T)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for i in range(warmup + steps):
+            if i >= warmup:
+                flush.zero_()
+                ev[i - warmup][0].record(stream)
+            idx, w = M.moe_route(logits, MOE_K, stream=stream)
+            recv = ep.dispatch(x, idx)
+            if i >= warmup:
+                ev[i - warmup][1].record(stream)
+            if i == 0:
+                torch.cuda.synchronize()
+                n = ep.recv_rows()
+                ep.expert_out()[:n].copy_(recv[:n])
+            ep.combine(idx, w)
+            if i >= warmup:
+                ev[i - warmup][2].record(stream)
+        torch.cuda.synchronize()
+    team.check()
+    d_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    c_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    t = torch.tensor([d_ms, c_ms], device=f"cuda:{dev}")
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    d_ms, c_ms = (float(v) for v in t.tolist())
+    rows = MOE_T * MOE_K
+    row_b = MOE_H * 2
+    moved = rows * row_b  # token rows delivered by dispatch (and pulled back by combine), per rank
+    remote = moved * (world - 1) / world
+    hbm = (MOE_T * row_b + moved)  # per phase: unique x read + routed rows written (or the mirror)
+    peak_hbm = peaks.get("hbm_gbs", 6550.1)
+    out = {
+        "workload": f"EP={world}: {MOE_E} experts, top-{MOE_K}, hidden {MOE_H}, {MOE_T} tokens/rank, "
+                    "bf16, routing from N(0,1) logits (device top-k); expert compute excluded",
+        "dispatch_ms": round(d_ms, 4), "combine_ms": round(c_ms, 4),
+        "gbps": round(world * 2 * moved / ((d_ms + c_ms) * 1e-3) / 1e9, 2),
+        "unit": "GB/s (routed token bytes moved by dispatch + combine, all ranks)",
+        "nvlink_bytes_per_rank_per_phase": remote,
+    }
+    if world == 1:
+        ach = 2 * hbm / ((d_ms + c_ms) * 1e-3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_hbm,
+                           "unit": "GB/s", "frac": round(ach / peak_hbm, 4),
+                           "bytes_per_phase": hbm}
+    else:
+        ach = remote / (max(d_ms, c_ms) * 1e-3) / 1e9
+        out["roofline"] = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 770.0,
+                           "unit": "GB/s per rank per direction (measured peer copy, B200_PROFILING.md)",
+                           "frac": round(ach / 770.0, 4)}
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main_ours(args):
     import torch
@@ -202,10 +271,12 @@ def main_ours(args):
     y = torch.empty(mpr, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
 
     heap = 2 * m * HIDDEN * 2 + m * ((HIDDEN + 7) // 8 * 8) * 2 + (64 << 20)
+    if not args.no_moe:  # EP receive + expert-output buffers (worst case: every token to one rank)
+        heap += 2 * MOE_T * MOE_K * world * MOE_H * 2 + (8 << 20)
     if distributed:
         team = Team.from_process_group(heap_bytes=heap, signal_slots=4096)
     else:
-        team = Team(1, [dev], heap_bytes=(1 << 20), signal_slots=4096)
+        team = Team(1, [dev], heap_bytes=heap, signal_slots=4096)
     ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=args.group_m)
     rs = K.GemmReduceScatter(team, m, f_tp, HIDDEN, block_n=256, group_m=args.group_m, num_comm_sms=8,
                              fuse_scatter=True, reduce_order="ascending")
@@ -338,6 +409,11 @@ def main_ours(args):
         cpu = {"value": round(v, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
                "sample": sample, "seconds": round(dt, 3)}
 
+    moe = None
+    if not args.no_moe:
+        moe = bench_moe(team, dev, world, rank, args.steps, args.warmup, flush, stream,
+                        distributed, peaks)
+
     launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
     if rank == 0:
         line = {
@@ -356,7 +432,7 @@ def main_ours(args):
                            "ms_per_step": round(cub_ms, 4),
                            "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
                            "speedup": round(cub_ms / step_ms, 4)},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)

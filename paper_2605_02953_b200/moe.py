@@ -134,23 +134,28 @@ class ExpertParallelMoE:
         per = {r: self._fill(r, xx.contiguous(), ii.contiguous()) for r, (xx, ii) in items.items()}
         self._keep = items
         self._drive("tf_moe_dispatch", per)
-        if len(per) == 1 and self.team.rank is not None:
-            return self.state[self.team.rank]["recv"]
+        if isinstance(topk_idx, torch.Tensor):
+            return self.state[next(iter(per))]["recv"]
         return [self.state[r]["recv"] for r in per]
 
+    def _r(self, r):
+        if r is not None:
+            return r
+        return self.team.rank if self.team.rank is not None else 0
+
     def counts(self, r=None):
-        return self.state[self.team.rank if r is None else r]["counts"]
+        return self.state[self._r(r)]["counts"]
 
     def recv_rows(self, r=None) -> int:
-        return int(self.state[self.team.rank if r is None else r]["recv_rows"].item())
+        return int(self.state[self._r(r)]["recv_rows"].item())
 
     def dest_rows(self, r=None, tokens=None):
-        st = self.state[self.team.rank if r is None else r]
+        st = self.state[self._r(r)]
         return st["dest"][: (tokens if tokens is not None else st["args"].tokens)]
 
     def expert_out(self, r=None):
         """[max_recv, H] bf16 buffer the experts write their outputs into (receive layout)."""
-        return self.state[self.team.rank if r is None else r]["yout"]
+        return self.state[self._r(r)]["yout"]
 
     def combine(self, topk_idx, topk_w, out=None):
         """out[t] = sum_j w[t,j] * y_owner[row(t,j)] (fp32, slot order), bf16."""
