@@ -82,6 +82,25 @@ class RemoteRegion:
         return self.heap.view(self.handle, self.pe, dtype, shape=shape, offset=offset)
 
 
+HANDLE_BLOB = 128
+
+
+def exchange_handles(blob: bytes, group=None) -> bytes:
+    """All-gather one fixed-size IPC handle blob per rank over torch.distributed;
+    returns the concatenation in rank order (what tf_team_open_peers expects).
+    Works on any backend (gloo in the CPU tests, nccl on the GPU box)."""
+    import torch.distributed as dist
+    if len(blob) != HANDLE_BLOB:
+        raise ValueError(f"handle blob must be {HANDLE_BLOB} bytes")
+    world = dist.get_world_size(group)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, blob, group=group)
+    for b in gathered:
+        if not isinstance(b, bytes) or len(b) != HANDLE_BLOB:
+            raise ProtocolError("mismatched handle blobs in team creation")
+    return b"".join(gathered)
+
+
 class Team:
     """Owns a C tf_team.  Local (all PEs in this process) or IPC (one PE here)."""
 
@@ -116,13 +135,10 @@ class Team:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         team = cls(world, heap_bytes=heap_bytes, signal_slots=signal_slots, ipc_rank=rank,
                    ipc_device=torch.cuda.current_device())
-        blob = (C.c_uint8 * 128)()
-        _lib.call("tf_team_export_handle", team.handle, blob, 128)
-        mine = bytes(blob)
-        gathered = [None] * world
-        dist.all_gather_object(gathered, mine, group=group)
-        allb = b"".join(gathered)
-        _lib.call("tf_team_open_peers", team.handle, C.c_char_p(allb), 128)
+        blob = (C.c_uint8 * HANDLE_BLOB)()
+        _lib.call("tf_team_export_handle", team.handle, blob, HANDLE_BLOB)
+        allb = exchange_handles(bytes(blob), group)
+        _lib.call("tf_team_open_peers", team.handle, C.c_char_p(allb), HANDLE_BLOB)
         return team
 
     @property
