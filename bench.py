@@ -167,6 +167,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def max_over_ranks(vals, dev, distributed):
+    """Element-wise max over ranks (device tensor for NCCL, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    if not distributed:
+        return [float(v) for v in vals]
+    if dist.get_backend() == "nccl":
+        t = torch.tensor(vals, dtype=torch.float64, device=f"cuda:{dev}")
+    else:
+        t = torch.tensor(vals, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
 # ------------------------------------------------------------------ MoE EP (config 4)
 MOE_E, MOE_K, MOE_H, MOE_T = 256, 8, 7168, 4096
 
@@ -204,10 +218,7 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
     team.check()
     d_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
     c_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
-    t = torch.tensor([d_ms, c_ms], device=f"cuda:{dev}")
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    d_ms, c_ms = (float(v) for v in t.tolist())
+    d_ms, c_ms = max_over_ranks([d_ms, c_ms], dev, distributed)
     rows = MOE_T * MOE_K
     row_b = MOE_H * 2
     moved = rows * row_b  # token rows delivered by dispatch (and pulled back by combine), per rank
@@ -245,10 +256,17 @@ def main_ours(args):
 
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     distributed = world_env > 1
+    shared_gpus = False
     if distributed:
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        ndev = torch.cuda.device_count()
+        shared_gpus = ndev < world_env  # test mode: several ranks per GPU (NCCL refuses that)
+        dev0 = local % ndev
+        torch.cuda.set_device(dev0)
+        if shared_gpus:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev0}"))
         rank, world = dist.get_rank(), dist.get_world_size()
     else:
         torch.cuda.set_device(0)
@@ -257,6 +275,9 @@ def main_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     dev = torch.cuda.current_device()
     tp = world
+    if shared_gpus and rank == 0:
+        print(f"[bench] {world} ranks share {torch.cuda.device_count()} GPU(s): functional run "
+              "only, numbers are not GPU-scaling measurements", file=sys.stderr)
     m, f_tp = TOKENS, FFN // tp
     mpr = m // tp
     peaks, peaks_kind = load_peaks()
@@ -286,6 +307,8 @@ def main_ours(args):
     def barrier():
         if distributed:
             dist.barrier()
+
+
 
     def step():
         ag(x, w1, h)
@@ -319,16 +342,14 @@ def main_ours(args):
     step_ms = sum(a + b for a, b in zip(ag_ms, rs_ms)) / n_events
     gemm_flops = 2.0 * m * f_tp * HIDDEN  # per GEMM per rank
     # max over ranks
-    t = torch.tensor([step_ms, sum(ag_ms) / n_events, sum(rs_ms) / n_events], device=f"cuda:{dev}")
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_ms, ag_avg, rs_avg = (float(v) for v in t.tolist())
+    step_ms, ag_avg, rs_avg = max_over_ranks(
+        [step_ms, sum(ag_ms) / n_events, sum(rs_ms) / n_events], dev, distributed)
     total_flops = 2 * gemm_flops * world
     value = total_flops / (step_ms * 1e-3) / 1e12
 
     # ---- cuBLAS comparator (same GEMMs, torch.matmul; unfused NCCL at N>1)
     cub_ms = None
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream) if not shared_gpus else torch.cuda.stream(stream):
         xg = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
         hp = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
         def cublas_step():
@@ -340,23 +361,21 @@ def main_ours(args):
             else:
                 hh = torch.matmul(x, w1.t())
                 torch.matmul(hh, w2.t())
-        for _ in range(3):
-            cublas_step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot = 0.0
-        for _ in range(max(3, args.steps // 2)):
-            flush.zero_()
-            e0.record(stream)
-            cublas_step()
-            e1.record(stream)
+        if not shared_gpus:  # NCCL cannot run with several ranks on one GPU
+            for _ in range(3):
+                cublas_step()
             torch.cuda.synchronize()
-            tot += e0.elapsed_time(e1)
-        cub_ms = tot / max(3, args.steps // 2)
-    tc = torch.tensor([cub_ms], device=f"cuda:{dev}")
-    if distributed:
-        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
-    cub_ms = float(tc.item())
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            tot = 0.0
+            for _ in range(max(3, args.steps // 2)):
+                flush.zero_()
+                e0.record(stream)
+                cublas_step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tot += e0.elapsed_time(e1)
+            cub_ms = tot / max(3, args.steps // 2)
+    cub_ms = max_over_ranks([cub_ms], dev, distributed)[0] if cub_ms is not None else None
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -380,10 +399,7 @@ def main_ours(args):
                 e2e_step()
             e1.record(stream)
             torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1) / args.steps], device=f"cuda:{dev}")
-        if distributed:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_ms = float(te.item())
+        e2e_ms = max_over_ranks([e0.elapsed_time(e1) / args.steps], dev, distributed)[0]
         e2e = {"value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                "ms_per_step": round(e2e_ms, 4),
                "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": y.numel() * 2}
@@ -427,11 +443,12 @@ def main_ours(args):
                        "parallelism": f"tp{tp}", "l2": "flushed between steps (256 MiB memset), "
                        "outside the per-step events"},
             "roofline": roof,
-            "comparator": {"impl": "cuBLAS (torch.matmul)" + (" + NCCL all_gather/reduce_scatter"
-                                                           if distributed else ""),
-                           "ms_per_step": round(cub_ms, 4),
-                           "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
-                           "speedup": round(cub_ms / step_ms, 4)},
+            "comparator": None if cub_ms is None else {
+                "impl": "cuBLAS (torch.matmul)" + (" + NCCL all_gather/reduce_scatter"
+                                                   if distributed else ""),
+                "ms_per_step": round(cub_ms, 4),
+                "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
+                "speedup": round(cub_ms / step_ms, 4)},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe,
             "gpu_launches": launches_per_step * args.steps,
         }

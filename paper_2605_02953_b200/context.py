@@ -64,7 +64,10 @@ class WorkloadContext:
 
     @property
     def hw_block_m(self) -> int:
-        # 256 = CTA pair per tile (tcgen05 cta_group::2); smaller = one CTA, 128 rows
+        # 512 / 256 = CTA pair per tile (tcgen05 cta_group::2, two or one M=256
+        # MMA per k-step); smaller = one CTA, 128 rows
+        if self.block_m >= 512:
+            return 512
         return 256 if self.block_m >= 256 else 128
 
 

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "tf_internal.h"
@@ -53,19 +55,33 @@ struct KParams {
   long long slot_ld;
   unsigned long long* err;
   unsigned long long timeout_ns;
+  int dbg_skip_store;                 // experiments only (TF_DEBUG_SKIP_STORE)
+  int tma_store;                      // epilogue 0: stage through smem + TMA bulk store
 };
 
-template <int CG, int BN>
+// CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
+// MH = 128-row A blocks per CTA (1 or 2).  The tile is 128*CG*MH rows x BN columns;
+// with MH = 2 each k-step issues two MMAs (one per 128*CG-row half) that share the
+// B stage, so A+B operand traffic per FLOP drops by 25% (pair tile 512x256).
+template <int CG, int MH, int BN>
 struct Smem {
-  static constexpr int kTileM = 128 * CG;           // rows per (pair) tile
-  static constexpr int kABytes = 128 * BK * 2;      // per CTA: 128 rows of A
-  static constexpr int kBRows = BN / CG;            // per CTA: BN/CG rows of B
+  static constexpr int kTileM = 128 * CG * MH;       // rows per tile
+  static constexpr int kABlock = 128 * BK * 2;       // one 128-row A block (16 KB)
+  static constexpr int kABytes = MH * kABlock;       // per CTA per stage
+  static constexpr int kBRows = BN / CG;             // per CTA: BN/CG rows of B
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (220 * 1024) / kStageBytes > 8 ? 8 : (220 * 1024) / kStageBytes;
+  // epilogue staging: 4 warps x 2 buffers x (32 rows x 128 B), 128-byte swizzled
+  static constexpr int kEpiBuf = 32 * 128;
+  static constexpr int kEpiBytes = 4 * 2 * kEpiBuf;
   static constexpr int kBarBytes = 256;
-  static constexpr int kTotal = 1024 /*align slack*/ + kStages * kStageBytes + kBarBytes;
-  static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int kMaxSmem = 232448;  // 227 KB opt-in per CTA on sm_100
+  static constexpr int kFit = (kMaxSmem - 1024 - kBarBytes - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kFit > 8 ? 8 : kFit;
+  static constexpr int kTotal = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarBytes;
+  static constexpr int kAccCols = MH * BN;           // fp32 columns of one accumulator
+  static constexpr int kAccStages = (2 * kAccCols <= 512) ? 2 : 1;
+  static constexpr int kTmemCols = kAccStages * kAccCols <= 256 ? 256 : 512;
 };
 
 __device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid_m, int& pid_n) {
@@ -80,22 +96,28 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid
   if (p.tile_map) pid_m = __ldg(p.tile_map + pid_m);
 }
 
-// CG = 1: one CTA per 128 x BN tile (tcgen05 cta_group::1).
-// CG = 2: a CTA pair (cluster of 2) per 256 x BN tile (tcgen05 cta_group::2): each
-//         CTA stages 128 rows of A and BN/2 rows of B, the leader issues the
-//         M=256 MMAs, each CTA's TMEM holds its 128 rows of the accumulator.
-template <int CG, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+// Row offset, inside the tile, of this CTA's A block h: MMA h covers tile rows
+// [h*128*CG, (h+1)*128*CG), CTA c of the pair supplies the c-th 128 of them.
+template <int CG>
+__device__ __forceinline__ int block_row(int h, uint32_t cta_rank) {
+  return (h * CG + static_cast<int>(cta_rank)) * 128;
+}
+
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
+                      const __grid_constant__ CUtensorMap tmap_c,
                       const __grid_constant__ KParams p) {
-  using S = Smem<CG, BN>;
+  using S = Smem<CG, MH, BN>;
+  constexpr int ACC = S::kAccStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S::kStages * S::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
+  uint8_t* smem_epi = smem + S::kStages * S::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + S::kEpiBytes);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + S::kStages;
   uint64_t* tfull_bar = bars + 2 * S::kStages;
@@ -124,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
+    if (p.tma_store) tma_prefetch_desc(&tmap_c);
   }
   if (warp == 1) {
     if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, S::kTmemCols);
@@ -144,15 +167,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int step = cluster_id; step < num_tiles; step += num_clusters) {
         int pid_m, pid_n;
         tile_coords(p, step, pid_m, pid_n);
-        const int m0 = pid_m * S::kTileM + 128 * cta_rank;   // this CTA's A rows
+        const int tile_m0 = pid_m * S::kTileM;
         const int n0 = pid_n * BN + S::kBRows * cta_rank;    // this CTA's B rows
         if constexpr (AG_WAIT) {
           // wait(arrival, rank_beg, n) acquire -- ag_gemm.py:87-90 (this CTA's rows)
-          if (m0 < p.m) {
+          bool waited = false;
+#pragma unroll
+          for (int h = 0; h < MH; ++h) {
+            const int m0 = tile_m0 + block_row<CG>(h, cta_rank);
+            if (m0 >= p.m) continue;
             const int r1 = min(m0 + 128, p.m) - 1;
             const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
             const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
-            bool waited = false;
             for (int c = c_beg; c <= c_end; ++c) {
               if (ready_mask & (1u << c)) continue;
               wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
@@ -160,20 +186,28 @@ __global__ void __launch_bounds__(kThreads, 1)
               ready_mask |= 1u << c;
               waited = true;
             }
-            // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
-            if (waited) fence_proxy_async_global();
           }
+          // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
+          if (waited) fence_proxy_async_global();
         }
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem_a + stage * S::kABytes;
+          uint8_t* sb = smem_b + stage * S::kBBytes;
           if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
-            tma_load_2d_pair(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
-            tma_load_2d_pair(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+#pragma unroll
+            for (int h = 0; h < MH; ++h)
+              tma_load_2d_pair(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
+                               tile_m0 + block_row<CG>(h, cta_rank));
+            tma_load_2d_pair(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           } else {
             mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
-            tma_load_2d(smem_a + stage * S::kABytes, &tmap_a, &full_bar[stage], kb * BK, m0);
-            tma_load_2d(smem_b + stage * S::kBBytes, &tmap_b, &full_bar[stage], kb * BK, n0);
+#pragma unroll
+            for (int h = 0; h < MH; ++h)
+              tma_load_2d(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
+                          tile_m0 + block_row<CG>(h, cta_rank));
+            tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           }
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
@@ -181,17 +215,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
-    if (leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(S::kTileM, BN);
+    if (leader && MH == 2) {
+      // Two M-halves per tile share one TMEM allocation (no double buffer).  Each
+      // half has its own full/empty barrier pair, and at tile boundaries the
+      // second half's MMAs lag by L k-blocks: the epilogue drains half 0 while
+      // half 1 finishes, and the next tile's half 0 starts while half 1 drains.
+      constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, BN);
+      constexpr int L = 2;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      auto issue = [&](int st, int h, int kb) {
+        const uint32_t a_addr = smem_u32(smem_a + st * S::kABytes) + h * S::kABlock;
+        const uint32_t b_addr = smem_u32(smem_b + st * S::kBBytes);
+#pragma unroll
+        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+          const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
+          const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
+          if constexpr (CG == 2) umma_bf16_pair(tmem_base + h * BN, ad, bd, idesc, (kb | kk) != 0);
+          else umma_bf16(tmem_base + h * BN, ad, bd, idesc, (kb | kk) != 0);
+        }
+      };
+      auto release = [&](uint64_t* bar) {
+        if constexpr (CG == 2) umma_commit_pair_mc(bar, 0x3);
+        else umma_commit(bar);
+      };
+      for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
+        const uint32_t tph = local & 1;
+        const int nkb = p.num_kb;
+        const bool lagged = nkb >= 2 * L + 1;
+        mbar_wait(&tempty_bar[0], tph ^ 1);
+        if (!lagged) mbar_wait(&tempty_bar[1], tph ^ 1);
+        tc_fence_after();
+        const int s0 = stage;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const bool head = lagged && kb < L;
+          const bool tail = lagged && kb >= nkb - L;
+          if (lane == 0) {
+            issue(stage, 0, kb);
+            if (!head && !tail) {
+              issue(stage, 1, kb);
+              release(&empty_bar[stage]);
+            }
+          }
+          __syncwarp();
+          if (lagged && kb == L - 1) {
+            // catch half 1 up on the held head stages once its accumulator is free
+            mbar_wait(&tempty_bar[1], tph ^ 1);
+            tc_fence_after();
+            if (lane == 0)
+              for (int j = 0; j < L; ++j) {
+                const int st = (s0 + j) % S::kStages;
+                issue(st, 1, j);
+                release(&empty_bar[st]);
+              }
+            __syncwarp();
+          }
+          if (++stage == S::kStages) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) {
+          release(&tfull_bar[0]);  // half 0 complete: its epilogue can start
+          if (lagged)
+            for (int j = nkb - L; j < nkb; ++j) {
+              const int st = (s0 + j) % S::kStages;
+              issue(st, 1, j);
+              release(&empty_bar[st]);
+            }
+          release(&tfull_bar[1]);
+        }
+        __syncwarp();
+      }
+    } else if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, BN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = local % ACC;
+        const uint32_t acc_phase = (local / ACC) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * S::kAccCols;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -200,10 +306,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b_addr = smem_u32(smem_b + stage * S::kBBytes);
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-              const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
               const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
-              if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-              else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+#pragma unroll
+              for (int h = 0; h < MH; ++h) {
+                const uint64_t ad = umma_desc_k_sw128(a_addr + h * S::kABlock + kk * UMMA_K * 2);
+                if constexpr (CG == 2)
+                  umma_bf16_pair(d_tmem + h * BN, ad, bd, idesc, (kb | kk) != 0);
+                else
+                  umma_bf16(d_tmem + h * BN, ad, bd, idesc, (kb | kk) != 0);
+              }
             }
             // smem slot free (in both CTAs) once these MMAs retire
             if constexpr (CG == 2) umma_commit_pair_mc(&empty_bar[stage], 0x3);
@@ -222,95 +333,166 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int quarter = warp & 3;          // TMEM lanes [32*quarter, 32*quarter+32)
-    const int row_in_cta = quarter * 32 + lane;
+    const int row_in_blk = quarter * 32 + lane;
     const uint32_t tempty_leader =
         CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
+    // TMA-store staging: this warp's two 32x128 B buffers (128-byte swizzled)
+    uint8_t* epi_buf = smem_epi + (warp - kEpiWarp0) * 2 * S::kEpiBuf;
+    int epi_slot = 0;
+    constexpr int kColsPerStore = OUT_F32 ? 32 : 64;  // 128 B of one row
     int local = 0;
     for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
       int pid_m, pid_n;
       tile_coords(p, step, pid_m, pid_n);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const int row0 = pid_m * S::kTileM + 128 * cta_rank;
-      const int row = row0 + row_in_cta;
-      const bool row_ok = row < p.m;
-      uint8_t* dst_row = nullptr;
-      if (row_ok) {
-        if constexpr (EPI == 0) {
-          dst_row = static_cast<uint8_t*>(p.c) +
-                    (static_cast<long long>(row) * p.ldc) * (OUT_F32 ? 4 : 2);
-        } else {
-          // slot layout at the owner: [world][rows_per_rank][slot_ld], slot = source rank
-          const int owner = static_cast<int>(row / p.rows_per_rank);
-          const long long orow = row - owner * p.rows_per_rank;
-          dst_row = static_cast<uint8_t*>(p.peer_slots[owner]) +
-                    ((p.rank * p.rows_per_rank + orow) * p.slot_ld) * (OUT_F32 ? 4 : 2);
+      const int acc = local % ACC;
+      const uint32_t acc_phase = (local / ACC) & 1;
+      // MH == 2: one barrier pair per half (tfull[h] / tempty[h]); else per accumulator
+      auto wait_full = [&](int h) {
+        if constexpr (MH == 2) mbar_wait(&tfull_bar[h], local & 1);
+        else mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+      };
+      auto arrive_empty = [&](int h) {
+        tc_fence_before();
+        __syncwarp();
+        const int b = MH == 2 ? h : acc;
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + b * 8);
+          else mbar_arrive(&tempty_bar[b]);
         }
-      }
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
+      };
+      if (EPI == 0 && p.tma_store) {
+        // 32-row x 128-byte boxes: TMEM -> regs -> swizzled smem -> cp.async.bulk.tensor
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + cc, v);
-        tmem_ld_wait();
-        const int col0 = pid_n * BN + cc;
-        if (!row_ok || col0 >= p.n) continue;
-        if (p.vec_ok && col0 + 32 <= p.n) {
-          if constexpr (OUT_F32) {
-            uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 4);
+        for (int h = 0; h < MH; ++h) {
+          if (MH == 2 || h == 0) wait_full(h);
+          const int wrow0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank) + quarter * 32;
+          const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                 acc * S::kAccCols + h * BN;
+#pragma unroll 1
+          for (int cc = 0; cc < BN; cc += kColsPerStore) {
+            uint8_t* buf = epi_buf + epi_slot * S::kEpiBuf;
+            uint32_t v[kColsPerStore];
+            tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            if constexpr (!OUT_F32)
+              tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+            // the store issued from this buffer two rounds ago must have read it
+            if (lane == 0) tma_store_wait_read<1>();
+            __syncwarp();
+            tmem_ld_wait();
+            uint8_t* my_row = buf + lane * 128;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              d[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-            uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 2);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              d[j] = make_uint4(
-                  pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
-                  pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
-                  pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
-                  pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (col0 + j < p.n) {
+            for (int j = 0; j < 8; ++j) {
+              uint4 q;
               if constexpr (OUT_F32) {
-                reinterpret_cast<float*>(dst_row)[col0 + j] = __uint_as_float(v[j]);
+                q = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
               } else {
-                reinterpret_cast<uint16_t*>(dst_row)[col0 + j] =
-                    static_cast<uint16_t>(pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFF);
+                q = make_uint4(
+                    pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+              }
+              *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) = q;
+            }
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0 && wrow0 < p.m && pid_n * BN + cc < p.n && !p.dbg_skip_store) {
+              tma_store_2d(&tmap_c, buf, pid_n * BN + cc, wrow0);
+            }
+            if (lane == 0) tma_store_commit();
+            epi_slot ^= 1;
+          }
+          // this half drained (stores read smem asynchronously, TMEM is free)
+          if (MH == 2 || h == MH - 1) arrive_empty(h);
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int h = 0; h < MH; ++h) {
+        if (MH == 2 || h == 0) wait_full(h);
+        const int row0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank);
+        const int row = row0 + row_in_blk;
+        const bool row_ok = row < p.m;
+        uint8_t* dst_row = nullptr;
+        if (row_ok) {
+          if constexpr (EPI == 0) {
+            dst_row = static_cast<uint8_t*>(p.c) +
+                      (static_cast<long long>(row) * p.ldc) * (OUT_F32 ? 4 : 2);
+          } else {
+            // slot layout at the owner: [world][rows_per_rank][slot_ld], slot = source rank
+            const int owner = static_cast<int>(row / p.rows_per_rank);
+            const long long orow = row - owner * p.rows_per_rank;
+            dst_row = static_cast<uint8_t*>(p.peer_slots[owner]) +
+                      ((p.rank * p.rows_per_rank + orow) * p.slot_ld) * (OUT_F32 ? 4 : 2);
+          }
+        }
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                               acc * S::kAccCols + h * BN;
+#pragma unroll 1
+        for (int cc = 0; cc < BN; cc += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_row + cc, v);
+          tmem_ld_wait();
+          const int col0 = pid_n * BN + cc;
+          if (!row_ok || col0 >= p.n || p.dbg_skip_store) continue;
+          if (p.vec_ok && col0 + 32 <= p.n) {
+            if constexpr (OUT_F32) {
+              uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 4);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                d[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+              uint4* d = reinterpret_cast<uint4*>(dst_row + static_cast<long long>(col0) * 2);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                d[j] = make_uint4(
+                    pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (col0 + j < p.n) {
+                if constexpr (OUT_F32) {
+                  reinterpret_cast<float*>(dst_row)[col0 + j] = __uint_as_float(v[j]);
+                } else {
+                  reinterpret_cast<uint16_t*>(dst_row)[col0 + j] =
+                      static_cast<uint16_t>(pack_bf16x2(__uint_as_float(v[j]), 0.f) & 0xFFFF);
+                }
               }
             }
           }
         }
+        if constexpr (MH == 2) arrive_empty(h);  // this half drained
       }
       // accumulator drained: hand TMEM back to the leader's MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + acc * 8);
-        else mbar_arrive(&tempty_bar[acc]);
-      }
+      if constexpr (MH == 1) arrive_empty(0);
       if constexpr (EPI == 1) {
         // publish: every thread's stores are made visible system-wide, the four
         // epilogue warps meet, then one thread release-adds the owners' counters
         // (one counter per 128-row block of the output).
         fence_sys();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == kEpiWarp0 * 32 && row0 < p.m) {
-          const int r1 = min(row0 + 128, p.m) - 1;
-          const int o0 = static_cast<int>(row0 / p.rows_per_rank);
-          const int o1 = static_cast<int>(r1 / p.rows_per_rank);
-          for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
+        if (threadIdx.x == kEpiWarp0 * 32) {
+#pragma unroll 1
+          for (int h = 0; h < MH; ++h) {
+            const int row0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank);
+            if (row0 >= p.m) continue;
+            const int r1 = min(row0 + 128, p.m) - 1;
+            const int o0 = static_cast<int>(row0 / p.rows_per_rank);
+            const int o1 = static_cast<int>(r1 / p.rows_per_rank);
+            for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
+          }
         }
       }
     }
   }
 
+  if (warp >= kEpiWarp0 && lane == 0) tma_store_wait<0>();
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();
   else __syncthreads();
@@ -341,17 +523,33 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+CUtensorMapL2promotion l2_promotion() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TF_L2_PROMO");  // experiments: 0 none, 1 64B, 2 128B, 3 256B
+    v = e ? atoi(e) : 3;
+  }
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
-                 int box_rows) {
+                 int box_rows, int esz = 2, int box_cols = BK) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+  const CUtensorMapDataType dt =
+      esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = enc(map, dt, 2, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(TF_ERR_INVALID, "cuTensorMapEncodeTiled failed (code " + std::to_string(r) +
@@ -360,22 +558,22 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
   return TF_OK;
 }
 
-template <int CG, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
-int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
-             cudaStream_t stream) {
-  auto kern = gemm_sm100_kernel<CG, BN, OUT_F32, EPI, AG_WAIT>;
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+             const KParams& kp, int grid, cudaStream_t stream) {
+  auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT>;
+  using S = Smem<CG, MH, BN>;
   static uint64_t attr_done = 0;  // per template instance, bit per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_done & (1ull << dev))) {
-    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Smem<CG, BN>::kTotal));
+    TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal));
     attr_done |= 1ull << dev;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Smem<CG, BN>::kTotal;
+  cfg.dynamicSmemBytes = S::kTotal;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -384,23 +582,23 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, kp));
+  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp));
   return TF_OK;
 }
 
-template <int CG, int BN>
-int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, int grid,
-                const GemmLaunch& g, cudaStream_t s) {
+template <int CG, int MH, int BN>
+int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                const KParams& kp, int grid, const GemmLaunch& g, cudaStream_t s) {
   const bool ag = g.chunk_flags != nullptr;
   if (g.epilogue == 0) {
     if (g.out_f32)
-      return ag ? launch_t<CG, BN, true, 0, true>(ta, tb, kp, grid, s)
-                : launch_t<CG, BN, true, 0, false>(ta, tb, kp, grid, s);
-    return ag ? launch_t<CG, BN, false, 0, true>(ta, tb, kp, grid, s)
-              : launch_t<CG, BN, false, 0, false>(ta, tb, kp, grid, s);
+      return ag ? launch_t<CG, MH, BN, true, 0, true>(ta, tb, tc, kp, grid, s)
+                : launch_t<CG, MH, BN, true, 0, false>(ta, tb, tc, kp, grid, s);
+    return ag ? launch_t<CG, MH, BN, false, 0, true>(ta, tb, tc, kp, grid, s)
+              : launch_t<CG, MH, BN, false, 0, false>(ta, tb, tc, kp, grid, s);
   }
-  if (g.out_f32) return launch_t<CG, BN, true, 1, false>(ta, tb, kp, grid, s);
-  return launch_t<CG, BN, false, 1, false>(ta, tb, kp, grid, s);
+  if (g.out_f32) return launch_t<CG, MH, BN, true, 1, false>(ta, tb, tc, kp, grid, s);
+  return launch_t<CG, MH, BN, false, 1, false>(ta, tb, tc, kp, grid, s);
 }
 
 }  // namespace
@@ -417,8 +615,8 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   if (g.m == 0 || g.n == 0) return TF_OK;
   if (g.block_n != 128 && g.block_n != 256)
     return fail(TF_ERR_CONFIG, "block_n must be 128 or 256 on the tcgen05 path");
-  if (g.block_m != 128 && g.block_m != 256)
-    return fail(TF_ERR_CONFIG, "block_m must be 128 (one CTA) or 256 (CTA pair)");
+  if (g.block_m != 128 && g.block_m != 256 && g.block_m != 512)
+    return fail(TF_ERR_CONFIG, "block_m must be 128 (one CTA), 256 (CTA pair) or 512 (CTA pair, two M=256 MMAs)");
   const int tile_m = g.block_m;
   if ((g.lda * 2) % 16 || (g.ldb * 2) % 16)
     return fail(TF_ERR_INVALID, "A/B row strides must be multiples of 16 bytes (K % 8 == 0)");
@@ -462,14 +660,28 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.slot_ld = g.slot_ld;
   kp.err = g.err;
   kp.timeout_ns = g.timeout_ns;
+  kp.dbg_skip_store = getenv("TF_DEBUG_SKIP_STORE") ? 1 : 0;
   if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
 
-  const int cg = tile_m / 128;
+  const int cg = tile_m == 128 ? 1 : 2;
+  const int mh = tile_m == 512 ? 2 : 1;
+  if (mh == 2 && g.block_n != 256)
+    return fail(TF_ERR_CONFIG, "block_m 512 requires block_n 256");
   CUtensorMap ta, tb;
   int rc = make_tmap_2d(&ta, g.a, g.m, g.k, g.lda, 128);
   if (rc) return rc;
   rc = make_tmap_2d(&tb, g.b, g.n, g.k, g.ldb, g.block_n / cg);
   if (rc) return rc;
+  // C through TMA stores when rows are 16-byte aligned (else per-thread stores)
+  CUtensorMap tc;
+  std::memset(&tc, 0, sizeof(tc));
+  kp.tma_store = 0;
+  if (g.epilogue == 0 && kp.vec_ok && !getenv("TF_DEBUG_NO_TMA_STORE")) {
+    const int esz_c = g.out_f32 ? 4 : 2;
+    rc = make_tmap_2d(&tc, g.c, g.m, g.n, g.ldc, 32, esz_c, 128 / esz_c);
+    if (rc) return rc;
+    kp.tma_store = 1;
+  }
 
   const int tiles = kp.num_pid_m * kp.num_pid_n;
   int ctas = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
@@ -477,12 +689,13 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   if (clusters < 1) clusters = 1;
   if (clusters > tiles) clusters = tiles;
   const int grid = clusters * cg;
+  if (mh == 2) return dispatch_bn<2, 2, 256>(ta, tb, tc, kp, grid, g, stream);
   if (cg == 2) {
-    if (g.block_n == 256) return dispatch_bn<2, 256>(ta, tb, kp, grid, g, stream);
-    return dispatch_bn<2, 128>(ta, tb, kp, grid, g, stream);
+    if (g.block_n == 256) return dispatch_bn<2, 1, 256>(ta, tb, tc, kp, grid, g, stream);
+    return dispatch_bn<2, 1, 128>(ta, tb, tc, kp, grid, g, stream);
   }
-  if (g.block_n == 256) return dispatch_bn<1, 256>(ta, tb, kp, grid, g, stream);
-  return dispatch_bn<1, 128>(ta, tb, kp, grid, g, stream);
+  if (g.block_n == 256) return dispatch_bn<1, 1, 256>(ta, tb, tc, kp, grid, g, stream);
+  return dispatch_bn<1, 1, 128>(ta, tb, tc, kp, grid, g, stream);
 }
 
 }  // namespace tf

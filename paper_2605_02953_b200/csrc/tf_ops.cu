@@ -143,8 +143,8 @@ struct StreamJoin {
 int check_gemm_args(const tf_gemm_args* a) {
   if (!a) return fail(TF_ERR_INVALID, "args is NULL");
   if (a->m < 0 || a->n < 0 || a->k < 1) return fail(TF_ERR_INVALID, "bad GEMM shape");
-  if (a->block_m != 0 && a->block_m != 128 && a->block_m != 256)
-    return fail(TF_ERR_CONFIG, "block_m must be 128 (one CTA) or 256 (CTA pair)");
+  if (a->block_m != 0 && a->block_m != 128 && a->block_m != 256 && a->block_m != 512)
+    return fail(TF_ERR_CONFIG, "block_m must be 128 (one CTA), 256 or 512 (CTA pair)");
   if (a->block_n != 0 && a->block_n != 128 && a->block_n != 256)
     return fail(TF_ERR_CONFIG, "block_n must be 128 or 256");
   if (a->block_k != 0 && a->block_k != 64) return fail(TF_ERR_CONFIG, "block_k must be 64");

@@ -192,7 +192,7 @@ def _drive(team: Team, fn_name: str, per_rank_args: dict, ranks):
 
 # ----------------------------------------------------------------- core GEMM
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
-         out_dtype: torch.dtype = torch.bfloat16, block_m: int = 256, block_n: int = 256,
+         out_dtype: torch.dtype = torch.bfloat16, block_m: int = 512, block_n: int = 256,
          group_m: int = 8, num_sms: int = 0, tile_map: torch.Tensor | None = None,
          stream=None) -> torch.Tensor:
     """C = A @ B.T on one GPU with the tcgen05 kernel (bf16 in, fp32 accumulate).
@@ -338,7 +338,7 @@ class AllGatherGemm:
     in the team heap; each call is one epoch."""
 
     def __init__(self, team: Team, m: int, k: int, n_local: int, *, out_dtype=torch.bfloat16,
-                 block_m: int = 256, block_n: int = 256, group_m: int = 8,
+                 block_m: int = 512, block_n: int = 256, group_m: int = 8,
                  num_gemm_sms: int = 0, swizzle: bool = True, nnodes: int = 1):
         if k % 8:
             raise ValueError("K must be a multiple of 8")
@@ -379,7 +379,7 @@ class GemmReduceScatter:
     """Reusable fused GEMM+ReduceScatter for a fixed shape over a team."""
 
     def __init__(self, team: Team, m: int, k_local: int, n: int, *, out_dtype=torch.bfloat16,
-                 block_m: int = 256, block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
+                 block_m: int = 512, block_n: int = 256, group_m: int = 8, num_gemm_sms: int = 0,
                  num_comm_sms: int = 8, swizzle: bool = True, fuse_scatter: bool = True,
                  reduce_order: str = "ascending", nnodes: int = 1):
         if k_local % 8:

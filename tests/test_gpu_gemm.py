@@ -44,12 +44,14 @@ def _bf16(rng, shape, scale=1.0):
     return (torch.from_numpy(rng.standard_normal(shape).astype(np.float32)) * scale).to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("m,n,k,bn", [(128, 256, 64, 256), (256, 512, 1024, 256),
                                       (300, 200, 136, 128), (1000, 1000, 520, 256),
                                       (2048, 1536, 4096, 256), (64, 40, 8, 128)])
 def test_core_gemm_vs_torch_fp32(m, n, k, bn, bm):
     K = _k()
+    if bm == 512 and bn != 256:
+        pytest.skip("the 512-row pair tile is built for block_n 256")
     rng = np.random.default_rng(m * 7 + n)
     a = _bf16(rng, (m, k)).cuda()
     b = _bf16(rng, (n, k)).cuda()
@@ -60,10 +62,12 @@ def test_core_gemm_vs_torch_fp32(m, n, k, bn, bm):
     assert err <= TOL_BF16, err
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("bn", [128, 256])
 def test_core_gemm_exact_lattice_fp32_out(bn, bm):
     K = _k()
+    if bm == 512 and bn != 256:
+        pytest.skip("the 512-row pair tile is built for block_n 256")
     rng = np.random.default_rng(bn)
     m, n, k = 512, 768, 2048
     a = rng.integers(-8, 8, (m, k))
@@ -82,7 +86,7 @@ def test_core_gemm_persistent_grid_and_tile_map_order_irrelevant():
     a = _bf16(rng, (m, k)).cuda()
     b = _bf16(rng, (n, k)).cuda()
     base = K.gemm(a, b)
-    for bm in (128, 256):
+    for bm in (128, 256, 512):
         tm = K.tile_map_tensor(m, 3, 8, 1, "ag_gemm", "cuda", bm)
         for sms in (1, 3, 148):
             out = K.gemm(a, b, num_sms=sms, tile_map=tm, group_m=3, block_m=bm)
@@ -90,7 +94,7 @@ def test_core_gemm_persistent_grid_and_tile_map_order_irrelevant():
             assert torch.equal(out, base)
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("case", range(12))
 def test_ag_gemm_exact_vs_reference_fixture(case, bm):
     K = _k()
@@ -103,14 +107,14 @@ def test_ag_gemm_exact_vs_reference_fixture(case, bm):
 
 
 @pytest.mark.parametrize("case", range(12))
-@pytest.mark.parametrize("variant", ["fused_asc", "fused_ring", "unfused", "fused_pair"])
+@pytest.mark.parametrize("variant", ["fused_asc", "fused_ring", "unfused", "fused_pair", "fused_pair512"])
 def test_gemm_rs_exact_vs_reference_fixture(case, variant):
     K = _k()
     c = G.workloads()[case]
     w = c["world"]
     ctx = _ctx(w, fuse_scatter=variant.startswith("fused"),
                reduce_order="ring" if variant == "fused_ring" else "ascending",
-               block_m=256 if variant == "fused_pair" else 128)
+               block_m={"fused_pair": 256, "fused_pair512": 512}.get(variant, 128))
     run = K.gemm_rs(list(c["rs_x"]), list(c["rs_w"]), ctx)
     for r in range(w):
         assert np.array_equal(run.outputs[r], c["rs_y"][r]), (case, variant, r)
@@ -129,7 +133,7 @@ def test_config1_ag_gemm_world2_1024_exact_digest():
         assert hashlib.sha256(o.astype(np.int64).tobytes()).hexdigest() == meta["sha256_per_rank"][r]
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_ag_gemm_bf16_production_tolerance(world, bm):
     K = _k()
@@ -145,7 +149,7 @@ def test_ag_gemm_bf16_production_tolerance(world, bm):
         assert O.compare(run.outputs[r].float().cpu().numpy(), ref[r]) <= TOL_BF16
 
 
-@pytest.mark.parametrize("bm", [128, 256])
+@pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("fused", [True, False])
 def test_gemm_rs_bf16_production_tolerance(world, fused, bm):

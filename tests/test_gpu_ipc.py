@@ -1,0 +1,33 @@
+"""GPU test of the one-process-per-GPU (torchrun, CUDA IPC) path.  With a
+single GPU both ranks share cuda:0 -- the IPC mapping, epoch flags, barriers and
+fused kernels are the same code as on an 8-GPU box."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("nproc", [2])
+def test_torchrun_ipc_team_parity(nproc):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "tests", "dist", "ipc_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "IPC_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
