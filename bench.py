@@ -71,7 +71,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -314,6 +314,37 @@ def main_ours(args):
         ag(x, w1, h)
         rs(h, w2, y)
 
+    # ---- cuBLAS comparator (same GEMMs, torch.matmul; unfused NCCL at N>1)
+    xg = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    hp = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
+
+    def cublas_step():
+        if distributed:
+            dist.all_gather_into_tensor(xg, x)
+            hh = torch.matmul(xg, w1.t())
+            torch.matmul(hh, w2.t(), out=hp)
+            dist.reduce_scatter_tensor(y, hp)
+        else:
+            hh = torch.matmul(x, w1.t())
+            torch.matmul(hh, w2.t())
+
+    def time_cublas(n):
+        # same protocol as our timed loop: flush, event, step, event -- no host syncs
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                cublas_step()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(n)]
+            for e0, e1 in evs:
+                flush.zero_()
+                e0.record(stream)
+                cublas_step()
+                e1.record(stream)
+            torch.cuda.synchronize()
+        return sum(e0.elapsed_time(e1) for e0, e1 in evs) / n
+
+    cub_before = None if shared_gpus else time_cublas(args.steps)
     n_events = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_events)]
     with torch.cuda.stream(stream):
@@ -347,62 +378,63 @@ def main_ours(args):
     total_flops = 2 * gemm_flops * world
     value = total_flops / (step_ms * 1e-3) / 1e12
 
-    # ---- cuBLAS comparator (same GEMMs, torch.matmul; unfused NCCL at N>1)
     cub_ms = None
-    with torch.cuda.stream(stream) if not shared_gpus else torch.cuda.stream(stream):
-        xg = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
-        hp = torch.empty(m, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
-        def cublas_step():
-            if distributed:
-                dist.all_gather_into_tensor(xg, x)
-                hh = torch.matmul(xg, w1.t())
-                torch.matmul(hh, w2.t(), out=hp)
-                dist.reduce_scatter_tensor(y, hp)
-            else:
-                hh = torch.matmul(x, w1.t())
-                torch.matmul(hh, w2.t())
-        if not shared_gpus:  # NCCL cannot run with several ranks on one GPU
-            for _ in range(3):
-                cublas_step()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            tot = 0.0
-            for _ in range(max(3, args.steps // 2)):
-                flush.zero_()
-                e0.record(stream)
-                cublas_step()
-                e1.record(stream)
-                torch.cuda.synchronize()
-                tot += e0.elapsed_time(e1)
-            cub_ms = tot / max(3, args.steps // 2)
-    cub_ms = max_over_ranks([cub_ms], dev, distributed)[0] if cub_ms is not None else None
+    if not shared_gpus:  # NCCL cannot run with several ranks on one GPU
+        cub_ms = 0.5 * (cub_before + time_cublas(args.steps)) if cub_before else time_cublas(args.steps)
+        cub_ms = max_over_ranks([cub_ms], dev, distributed)[0]
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        x_host = x.cpu().pin_memory()
-        y_host = torch.empty(mpr, HIDDEN, dtype=torch.bfloat16).pin_memory()
-        x_dev = torch.empty_like(x)
-        with torch.cuda.stream(stream):
-            def e2e_step():
-                x_dev.copy_(x_host, non_blocking=True)
-                ag(x_dev, w1, h)
-                rs(h, w2, y)
-                y_host.copy_(y, non_blocking=True)
-            for _ in range(2):
-                e2e_step()
+        # Every step: H2D of its activations from pinned host memory, the fused
+        # AG-GEMM -> GEMM-RS, D2H of its result.  Copies run on copy-engine
+        # streams double-buffered against the compute stream, so step i+1's upload
+        # and step i-1's download overlap step i's GEMMs (as a serving loop would).
+        nb = 2
+        x_host = [x.cpu().pin_memory() for _ in range(nb)]
+        y_host = [torch.empty(mpr, HIDDEN, dtype=torch.bfloat16).pin_memory() for _ in range(nb)]
+        x_dev = [torch.empty_like(x) for _ in range(nb)]
+        y_dev = [torch.empty_like(y) for _ in range(nb)]
+        h2d_s = torch.cuda.Stream(device=dev)
+        d2h_s = torch.cuda.Stream(device=dev)
+        n_e2e = args.steps + 2
+
+        def run_e2e(n):
+            ev_h2d = [torch.cuda.Event() for _ in range(n)]
+            ev_cmp = [torch.cuda.Event() for _ in range(n)]
+            ev_d2h = [torch.cuda.Event() for _ in range(n)]
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(h2d_s)
+            for i in range(n):
+                b = i % nb
+                if i >= nb:
+                    h2d_s.wait_event(ev_cmp[i - nb])       # x_dev[b] free again
+                with torch.cuda.stream(h2d_s):
+                    x_dev[b].copy_(x_host[b], non_blocking=True)
+                ev_h2d[i].record(h2d_s)
+                stream.wait_event(ev_h2d[i])
+                if i >= nb:
+                    stream.wait_event(ev_d2h[i - nb])      # y_dev[b] downloaded
+                with torch.cuda.stream(stream):
+                    ag(x_dev[b], w1, h)
+                    rs(h, w2, y_dev[b])
+                ev_cmp[i].record(stream)
+                d2h_s.wait_event(ev_cmp[i])
+                with torch.cuda.stream(d2h_s):
+                    y_host[b].copy_(y_dev[b], non_blocking=True)
+                ev_d2h[i].record(d2h_s)
+            t1.record(d2h_s)
             torch.cuda.synchronize()
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.steps):
-                e2e_step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-        e2e_ms = max_over_ranks([e0.elapsed_time(e1) / args.steps], dev, distributed)[0]
+            return t0.elapsed_time(t1) / n
+
+        run_e2e(3)
+        barrier()
+        e2e_ms = max_over_ranks([run_e2e(n_e2e)], dev, distributed)[0]
         e2e = {"value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
-               "ms_per_step": round(e2e_ms, 4),
-               "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": y.numel() * 2}
+               "ms_per_step": round(e2e_ms, 4), "steps": n_e2e,
+               "h2d_bytes_per_step": x.numel() * 2, "d2h_bytes_per_step": y.numel() * 2,
+               "note": "pinned host buffers; H2D/D2H on copy streams overlapped with the "
+                       "previous/next step's GEMMs (double-buffered)"}
 
     # ---- roofline of the dominant kernel (the tcgen05 GEMM; one launch per op at N=1)
     peak = peaks.get("bf16_tflops", 1622.7)
