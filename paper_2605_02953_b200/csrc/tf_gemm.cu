@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "tf_internal.h"
@@ -57,6 +58,11 @@ struct KParams {
   unsigned long long timeout_ns;
   int dbg_skip_store;                 // experiments only (TF_DEBUG_SKIP_STORE)
   int tma_store;                      // epilogue 0: stage through smem + TMA bulk store
+  // split-K tail: tiles [tail_base, num_tiles) are cut into split_s K-ranges each;
+  // unit u writes fp32 partials to tile slot u of the workspace, fixed up afterwards
+  int tail_base;
+  int split_s;
+  int total_work;
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -103,11 +109,30 @@ __device__ __forceinline__ int block_row(int h, uint32_t cta_rank) {
   return (h * CG + static_cast<int>(cta_rank)) * 128;
 }
 
+// Work item -> (tile step, k-block range, partial slot or -1).
+__device__ __forceinline__ void decode_work(const KParams& p, int work, int& step, int& kb0,
+                                            int& kb1, int& slot) {
+  if (work < p.tail_base) {
+    step = work;
+    kb0 = 0;
+    kb1 = p.num_kb;
+    slot = -1;
+  } else {
+    const int u = work - p.tail_base;
+    const int j = u % p.split_s;
+    step = p.tail_base + u / p.split_s;
+    kb0 = j * p.num_kb / p.split_s;
+    kb1 = (j + 1) * p.num_kb / p.split_s;
+    slot = u;
+  }
+}
+
 template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_c,
+                      const __grid_constant__ CUtensorMap tmap_p,
                       const __grid_constant__ KParams p) {
   using S = Smem<CG, MH, BN>;
   constexpr int ACC = S::kAccStages;
@@ -147,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
     if (p.tma_store) tma_prefetch_desc(&tmap_c);
+    if (p.split_s > 1) tma_prefetch_desc(&tmap_p);
   }
   if (warp == 1) {
     if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, S::kTmemCols);
@@ -164,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ready_mask = 0;  // AllGather chunks already observed as arrived
-      for (int step = cluster_id; step < num_tiles; step += num_clusters) {
+      for (int work = cluster_id; work < p.total_work; work += num_clusters) {
+        int step, kb0, kb1, slot;
+        decode_work(p, work, step, kb0, kb1, slot);
         int pid_m, pid_n;
         tile_coords(p, step, pid_m, pid_n);
         const int tile_m0 = pid_m * S::kTileM;
@@ -190,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
           if (waited) fence_proxy_async_global();
         }
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem_a + stage * S::kABytes;
           uint8_t* sb = smem_b + stage * S::kBBytes;
@@ -240,9 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (CG == 2) umma_commit_pair_mc(bar, 0x3);
         else umma_commit(bar);
       };
-      for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
+      for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
+        int step, kb0, kb1, slot;
+        decode_work(p, work, step, kb0, kb1, slot);
         const uint32_t tph = local & 1;
-        const int nkb = p.num_kb;
+        const int nkb = kb1 - kb0;
         const bool lagged = nkb >= 2 * L + 1;
         mbar_wait(&tempty_bar[0], tph ^ 1);
         if (!lagged) mbar_wait(&tempty_bar[1], tph ^ 1);
@@ -292,13 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
+      for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
+        int step, kb0, kb1, slot;
+        decode_work(p, work, step, kb0, kb1, slot);
         const int acc = local % ACC;
         const uint32_t acc_phase = (local / ACC) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * S::kAccCols;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = 0; kb < kb1 - kb0; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (lane == 0) {
@@ -341,7 +373,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int epi_slot = 0;
     constexpr int kColsPerStore = OUT_F32 ? 32 : 64;  // 128 B of one row
     int local = 0;
-    for (int step = cluster_id; step < num_tiles; step += num_clusters, ++local) {
+    for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
+      int step, kb0, kb1, slot;
+      decode_work(p, work, step, kb0, kb1, slot);
       int pid_m, pid_n;
       tile_coords(p, step, pid_m, pid_n);
       const int acc = local % ACC;
@@ -361,6 +395,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mbar_arrive(&tempty_bar[b]);
         }
       };
+      if (EPI == 0 && slot >= 0) {
+        // split-K tail unit: fp32 partial tile -> workspace slot (fixed up by tail_fixup_kernel)
+#pragma unroll 1
+        for (int h = 0; h < MH; ++h) {
+          if (MH == 2 || h == 0) wait_full(h);
+          const int prow0 = slot * S::kTileM + block_row<CG>(h, cta_rank) + quarter * 32;
+          const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                 acc * S::kAccCols + h * BN;
+#pragma unroll 1
+          for (int cc = 0; cc < BN; cc += 32) {
+            uint8_t* buf = epi_buf + epi_slot * S::kEpiBuf;
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_row + cc, v);
+            if (lane == 0) tma_store_wait_read<1>();
+            __syncwarp();
+            tmem_ld_wait();
+            uint8_t* my_row = buf + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmap_p, buf, cc, prow0);
+              tma_store_commit();
+            }
+            epi_slot ^= 1;
+          }
+          if (MH == 2 || h == MH - 1) arrive_empty(h);
+        }
+        continue;
+      }
       if (EPI == 0 && p.tma_store) {
         // 32-row x 128-byte boxes: TMEM -> regs -> swizzled smem -> cp.async.bulk.tensor
 #pragma unroll 1
@@ -503,6 +570,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-K tail fix-up: tile i of the tail = sum over parts j (in order) of
+// workspace slots i*split_s + j, converted and stored to C.  One CTA per
+// (tail tile, 32-row band); 256 threads cover 256 columns... of BN.
+template <int TILE_M, int BN, bool OUT_F32>
+__global__ void __launch_bounds__(256) tail_fixup_kernel(const float* __restrict__ ws,
+                                                         const __grid_constant__ KParams p) {
+  // one CTA per (tail tile, 32-row band), one thread per column of the tile
+  const int bands = TILE_M / 32;
+  const int i = blockIdx.x / bands;
+  const int band = blockIdx.x % bands;
+  int pid_m, pid_n;
+  tile_coords(p, p.tail_base + i, pid_m, pid_n);
+  const int c = pid_n * BN + threadIdx.x;
+  for (int r = 0; r < 32; ++r) {
+    const int lrow = band * 32 + r;
+    const int row = pid_m * TILE_M + lrow;
+    if (row >= p.m) break;
+    float acc = 0.f;
+    for (int j = 0; j < p.split_s; ++j)  // fixed order: deterministic
+      acc += ws[(static_cast<long long>(i * p.split_s + j) * TILE_M + lrow) * BN + threadIdx.x];
+    if (c < p.n) {
+      if constexpr (OUT_F32)
+        static_cast<float*>(p.c)[static_cast<long long>(row) * p.ldc + c] = acc;
+      else
+        static_cast<uint16_t*>(p.c)[static_cast<long long>(row) * p.ldc + c] =
+            static_cast<uint16_t>(pack_bf16x2(acc, 0.f) & 0xFFFF);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -560,7 +657,8 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
 
 template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-             const KParams& kp, int grid, cudaStream_t stream) {
+             const CUtensorMap& tp, const KParams& kp, int grid, cudaStream_t stream,
+             const float* tail_ws) {
   auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT>;
   using S = Smem<CG, MH, BN>;
   static uint64_t attr_done = 0;  // per template instance, bit per device
@@ -582,23 +680,51 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, kp));
+  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tp, kp));
+  if (kp.split_s > 1) {
+    const int tail_tiles = (kp.total_work - kp.tail_base) / kp.split_s;
+    tail_fixup_kernel<S::kTileM, BN, OUT_F32>
+        <<<tail_tiles * (S::kTileM / 32), BN, 0, stream>>>(tail_ws, kp);
+    TF_CUDA_TRY(cudaGetLastError());
+  }
   return TF_OK;
 }
 
 template <int CG, int MH, int BN>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                const KParams& kp, int grid, const GemmLaunch& g, cudaStream_t s) {
+                const CUtensorMap& tp, const KParams& kp, int grid, const GemmLaunch& g,
+                cudaStream_t s, const float* ws) {
   const bool ag = g.chunk_flags != nullptr;
   if (g.epilogue == 0) {
     if (g.out_f32)
-      return ag ? launch_t<CG, MH, BN, true, 0, true>(ta, tb, tc, kp, grid, s)
-                : launch_t<CG, MH, BN, true, 0, false>(ta, tb, tc, kp, grid, s);
-    return ag ? launch_t<CG, MH, BN, false, 0, true>(ta, tb, tc, kp, grid, s)
-              : launch_t<CG, MH, BN, false, 0, false>(ta, tb, tc, kp, grid, s);
+      return ag ? launch_t<CG, MH, BN, true, 0, true>(ta, tb, tc, tp, kp, grid, s, ws)
+                : launch_t<CG, MH, BN, true, 0, false>(ta, tb, tc, tp, kp, grid, s, ws);
+    return ag ? launch_t<CG, MH, BN, false, 0, true>(ta, tb, tc, tp, kp, grid, s, ws)
+              : launch_t<CG, MH, BN, false, 0, false>(ta, tb, tc, tp, kp, grid, s, ws);
   }
-  if (g.out_f32) return launch_t<CG, MH, BN, true, 1, false>(ta, tb, tc, kp, grid, s);
-  return launch_t<CG, MH, BN, false, 1, false>(ta, tb, tc, kp, grid, s);
+  if (g.out_f32) return launch_t<CG, MH, BN, true, 1, false>(ta, tb, tc, tp, kp, grid, s, ws);
+  return launch_t<CG, MH, BN, false, 1, false>(ta, tb, tc, tp, kp, grid, s, ws);
+}
+
+// Per-(device, stream) fp32 workspace for split-K tail partials (grown on demand).
+float* tail_workspace(cudaStream_t s, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto& e = bufs[{dev, s}];
+  if (e.second < bytes) {
+    if (e.first) {
+      cudaStreamSynchronize(s);
+      cudaFree(e.first);
+    }
+    e.first = nullptr;
+    e.second = 0;
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) return nullptr;
+    e.second = bytes;
+  }
+  return static_cast<float*>(e.first);
 }
 
 }  // namespace
@@ -689,13 +815,41 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   if (clusters < 1) clusters = 1;
   if (clusters > tiles) clusters = tiles;
   const int grid = clusters * cg;
-  if (mh == 2) return dispatch_bn<2, 2, 256>(ta, tb, tc, kp, grid, g, stream);
-  if (cg == 2) {
-    if (g.block_n == 256) return dispatch_bn<2, 1, 256>(ta, tb, tc, kp, grid, g, stream);
-    return dispatch_bn<2, 1, 128>(ta, tb, tc, kp, grid, g, stream);
+  // Split-K tail: when the last wave is at most half full, cut its tiles into
+  // K-ranges so every cluster gets work (wave quantization on 148 SMs).
+  kp.tail_base = tiles;
+  kp.split_s = 1;
+  kp.total_work = tiles;
+  CUtensorMap tp;
+  std::memset(&tp, 0, sizeof(tp));
+  float* tail_ws = nullptr;
+  {
+    const int rem = tiles % clusters;
+    int split = rem > 0 ? clusters / rem : 1;
+    if (split > 8) split = 8;
+    while (split > 1 && kp.num_kb / split < 4) --split;
+    if (g.epilogue == 0 && tiles > clusters && rem > 0 && split >= 2 && !g.no_tail_split &&
+        !getenv("TF_DEBUG_NO_SPLITK")) {
+      const int tile_m_rows = tile_m;
+      const size_t bytes = static_cast<size_t>(rem) * split * tile_m_rows * g.block_n * 4;
+      tail_ws = tail_workspace(stream, bytes);
+      if (tail_ws) {
+        rc = make_tmap_2d(&tp, tail_ws, static_cast<int64_t>(rem) * split * tile_m_rows,
+                          g.block_n, g.block_n, 32, 4, 32);
+        if (rc) return rc;
+        kp.tail_base = tiles - rem;
+        kp.split_s = split;
+        kp.total_work = kp.tail_base + rem * split;
+      }
+    }
   }
-  if (g.block_n == 256) return dispatch_bn<1, 1, 256>(ta, tb, tc, kp, grid, g, stream);
-  return dispatch_bn<1, 1, 128>(ta, tb, tc, kp, grid, g, stream);
+  if (mh == 2) return dispatch_bn<2, 2, 256>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
+  if (cg == 2) {
+    if (g.block_n == 256) return dispatch_bn<2, 1, 256>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
+    return dispatch_bn<2, 1, 128>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
+  }
+  if (g.block_n == 256) return dispatch_bn<1, 1, 256>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
+  return dispatch_bn<1, 1, 128>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
 }
 
 }  // namespace tf

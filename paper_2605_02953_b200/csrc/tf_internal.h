@@ -52,6 +52,7 @@ struct GemmLaunch {
   int64_t slot_ld = 0;
   unsigned long long* err = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  bool no_tail_split = false;        // disable the split-K tail (e.g. inside fused protocols)
 };
 
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);
