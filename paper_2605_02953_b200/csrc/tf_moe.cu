@@ -38,22 +38,29 @@ namespace {
 constexpr int kChunk = 1024;  // (token, slot) entries per ranking chunk
 
 // ---------------------------------------------------------------- routing
+template <int VPL>  // logits per lane (E <= 32 * VPL)
 __global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, int E, int k,
                             int32_t* __restrict__ idx, float* __restrict__ w) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= tokens) return;
   const float* row = logits + t * E;
-  uint32_t taken = 0;  // bit c: expert lane + 32*c already selected (E <= 1024)
-  float sel_val[16];
-  int sel_idx[16];
+  float v[VPL];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {  // coalesced: lane + 32c
+    const int e = lane + 32 * c;
+    v[c] = e < E ? __ldg(row + e) : -INFINITY;
+  }
+  float sel0 = 0.f, z = 0.f;
+  float my_val = 0.f;
+  int my_idx = 0;
   for (int r = 0; r < k; ++r) {
     float best = -INFINITY;
     int bi = 0x7fffffff;
-    for (int e = lane, c = 0; e < E; e += 32, ++c) {
-      if (taken & (1u << c)) continue;
-      const float v = row[e];
-      if (v > best || (v == best && e < bi)) { best = v; bi = e; }
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int e = lane + 32 * c;
+      if (e < E && (v[c] > best || (v[c] == best && e < bi))) { best = v[c]; bi = e; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -61,17 +68,19 @@ __global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, in
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-    sel_val[r] = best;
-    sel_idx[r] = bi;
-  }
-  if (lane == 0) {
-    float z = 0.f;
-    for (int r = 0; r < k; ++r) z += __expf(sel_val[r] - sel_val[0]);
-    for (int r = 0; r < k; ++r) {
-      idx[t * k + r] = sel_idx[r];
-      w[t * k + r] = __expf(sel_val[r] - sel_val[0]) / z;
+    if ((bi & 31) == lane) {
+#pragma unroll
+      for (int c = 0; c < VPL; ++c)
+        if (c == (bi >> 5)) v[c] = -INFINITY;  // taken (ties resolve to lower id: stable)
     }
+    if (r == 0) sel0 = best;
+    const float ez = __expf(best - sel0);
+    z += ez;
+    if (lane == r) { my_val = ez; my_idx = bi; }
+  }
+  if (lane < k) {
+    idx[t * k + lane] = my_idx;
+    w[t * k + lane] = my_val / z;
   }
 }
 
@@ -94,9 +103,46 @@ __global__ void hist_kernel(const int32_t* __restrict__ idx, int64_t entries, in
     chunk_hist[static_cast<int64_t>(blockIdx.x) * E + e] = h[e];
 }
 
-// one block: per-expert exclusive scan over chunks, totals, and expert bases
-__global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E,
-                            int32_t* __restrict__ counts, int32_t* __restrict__ expert_base) {
+// block-wide exclusive scan of n (<= 1024 * 4) ints in smem, 1024 threads
+__device__ void block_exclusive_scan(int32_t* data, int n) {
+  __shared__ int32_t warp_tot[32];
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(lo + per, n);
+  int32_t local = 0;
+  for (int i = lo; i < hi; ++i) local += data[i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x / 32;
+    int32_t x = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t o = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += o;
+    }
+    if (lane < nw) warp_tot[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  int32_t run = incl - local + (warp > 0 ? warp_tot[warp - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    const int32_t v = data[i];
+    data[i] = run;
+    run += v;
+  }
+  __syncthreads();
+}
+
+// one block of 1024: per-expert exclusive scan over chunks, totals, expert bases
+__global__ void __launch_bounds__(1024) scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks,
+                                                    int E, int32_t* __restrict__ counts,
+                                                    int32_t* __restrict__ expert_base) {
   extern __shared__ int32_t tot[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
@@ -109,13 +155,8 @@ __global__ void scan_kernel(int32_t* __restrict__ chunk_hist, int nchunks, int E
     counts[e] = run;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t run = 0;
-    for (int e = 0; e < E; ++e) {
-      expert_base[e] = run;
-      run += tot[e];
-    }
-  }
+  block_exclusive_scan(tot, E);
+  for (int e = threadIdx.x; e < E; e += blockDim.x) expert_base[e] = tot[e];
 }
 
 // 1024 threads: entry i of the chunk; rank among same-expert entries before it.
@@ -171,25 +212,34 @@ __global__ void wait_flags_kernel(const uint64_t* flags, int n, uint64_t epoch, 
   __syncthreads();
 }
 
-// seg_base[e] = start row, on e's owner, of the segment (expert e, source `rank`)
-__global__ void layout_kernel(const int32_t* __restrict__ mat /* [world][E] */, int world, int E,
-                              int rank, int32_t* __restrict__ seg_base,
-                              int32_t* __restrict__ counts_out, int64_t* __restrict__ recv_rows) {
+// seg_base[e] = start row, on e's owner, of the segment (expert e, source `rank`):
+// exclusive scan of expert totals inside each owner's expert range, plus the rows
+// of lower source ranks for the same expert.  One block of 1024 threads.
+__global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict__ mat, int world,
+                                                      int E, int rank,
+                                                      int32_t* __restrict__ seg_base,
+                                                      int32_t* __restrict__ counts_out,
+                                                      int64_t* __restrict__ recv_rows) {
+  extern __shared__ int32_t tot[];  // [E]
   const int epr = E / world;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int owner = e / epr;
-    int64_t base = 0;
-    for (int e2 = owner * epr; e2 < e; ++e2)
-      for (int s = 0; s < world; ++s) base += mat[s * E + e2];
-    for (int s = 0; s < rank; ++s) base += mat[s * E + e];
-    seg_base[e] = static_cast<int32_t>(base);
+    int32_t t = 0;
+    for (int s = 0; s < world; ++s) t += mat[s * E + e];
+    tot[e] = t;
   }
   for (int i = threadIdx.x; i < world * E; i += blockDim.x) counts_out[i] = mat[i];
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t tot = 0;
-    for (int e = rank * epr; e < (rank + 1) * epr; ++e)
-      for (int s = 0; s < world; ++s) tot += mat[s * E + e];
-    *recv_rows = tot;
+    int64_t mine = 0;
+    for (int e = rank * epr; e < (rank + 1) * epr; ++e) mine += tot[e];
+    *recv_rows = mine;
+  }
+  block_exclusive_scan(tot, E);  // global exclusive prefix over experts
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int owner_first = (e / epr) * epr;
+    int32_t base = tot[e] - tot[owner_first];  // rows of lower experts on the same owner
+    for (int s = 0; s < rank; ++s) base += mat[s * E + e];
+    seg_base[e] = base;
   }
 }
 
@@ -216,12 +266,14 @@ __global__ void __launch_bounds__(256) scatter_kernel(
     const uint4* src = x + t * vec_per_row;
     uint4* dst = static_cast<uint4*>(recv.p[owner]) + row * vec_per_row;
     int64_t v = lane;
-    for (; v + 96 < vec_per_row; v += 128) {  // 4 independent 16-byte loads in flight per lane
-      const uint4 a0 = __ldg(src + v), a1 = __ldg(src + v + 32), a2 = __ldg(src + v + 64),
-                  a3 = __ldg(src + v + 96);
-      dst[v] = a0; dst[v + 32] = a1; dst[v + 64] = a2; dst[v + 96] = a3;
+    for (; v + 7 * 32 < vec_per_row; v += 8 * 32) {  // 8 independent 16-byte loads per lane
+      uint4 r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = __ldg(src + v + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) __stcs(dst + v + 32 * u, r[u]);  // streaming: no L2 reuse
     }
-    for (; v < vec_per_row; v += 32) dst[v] = __ldg(src + v);
+    for (; v < vec_per_row; v += 32) __stcs(dst + v, __ldg(src + v));
   }
 }
 
@@ -288,7 +340,7 @@ int run_count(const int32_t* idx, int64_t entries, int E, int32_t* counts, int32
   if (!ebase) ebase = chunk + static_cast<int64_t>(nchunks) * E;
   if (static_cast<size_t>(32) * E * 4 > 227 * 1024) return fail(TF_ERR_CONFIG, "too many experts");
   hist_kernel<<<nchunks, 256, E * 4, s>>>(idx, entries, E, chunk);
-  scan_kernel<<<1, 1024, E * 4, s>>>(chunk, nchunks, E, counts, ebase);
+  scan_kernel<<<1, 1024, E * 4, s>>>(chunk, nchunks, E, counts, ebase);  // E <= 1024*4 ints
   if (entries > 0) {
     const size_t sm = static_cast<size_t>(32) * E * 4;
     static bool attr = false;
@@ -362,9 +414,11 @@ int tf_moe_topk(const float* logits, int64_t tokens, int n_experts, int k, int32
   if (k < 1 || k > 16 || k > n_experts) return fail(TF_ERR_INVALID, "need 1 <= k <= min(16, E)");
   if (tokens <= 0) return TF_OK;
   const int64_t threads = tokens * 32;
-  tf::topk_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0,
-                    static_cast<cudaStream_t>(stream)>>>(logits, tokens, n_experts, k, topk_idx,
-                                                         topk_w);
+  const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+  auto s = static_cast<cudaStream_t>(stream);
+  if (n_experts <= 64) tf::topk_kernel<2><<<grid, 256, 0, s>>>(logits, tokens, n_experts, k, topk_idx, topk_w);
+  else if (n_experts <= 256) tf::topk_kernel<8><<<grid, 256, 0, s>>>(logits, tokens, n_experts, k, topk_idx, topk_w);
+  else tf::topk_kernel<32><<<grid, 256, 0, s>>>(logits, tokens, n_experts, k, topk_idx, topk_w);
   TF_CUDA_TRY(cudaGetLastError());
   return TF_OK;
 }
@@ -421,15 +475,17 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
       mats.p[p] = t->pes[p].base + m.mat_off;
       flags.p[p] = t->pes[p].sig + sig;
     }
-    tf::push_counts_kernel<<<1, 256, 0, s>>>(own_row, E, mats, flags, w, rank, e);
+    if (w > 1) tf::push_counts_kernel<<<1, 256, 0, s>>>(own_row, E, mats, flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
   if (phase & TF_PHASE_MAIN) {
     const uint64_t e = m.ws->epoch[rank];
-    tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e, t->timeout_ns,
-                                                             t->err_word(rank), 0x5000000ull);
+    if (w > 1)
+      tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e,
+                                                               t->timeout_ns, t->err_word(rank),
+                                                               0x5000000ull);
     const int32_t* mat = reinterpret_cast<const int32_t*>(t->pes[rank].base + m.mat_off);
-    tf::layout_kernel<<<1, 256, 0, s>>>(mat, w, E, rank, seg_base, a->counts, a->recv_rows);
+    tf::layout_kernel<<<1, 1024, E * 4, s>>>(mat, w, E, rank, seg_base, a->counts, a->recv_rows);
     tf::PeerPtrs recv{};
     tf::PeerSig flags{};
     for (int p = 0; p < w; ++p) {
@@ -440,10 +496,10 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
       tf::scatter_kernel<<<tf::grid_for(entries), 256, 0, s>>>(
           static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
           a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank));
-    tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
+    if (w > 1) tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
-  if (phase & TF_PHASE_POST) {
+  if ((phase & TF_PHASE_POST) && w > 1) {
     const uint64_t e = m.ws->epoch[rank];
     tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig + w, w, e,
                                                              t->timeout_ns, t->err_word(rank),
@@ -463,16 +519,17 @@ int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* 
   const int w = t->world;
   const size_t sig = m.ws->sig_base + 2 * w;
   const uint64_t e = m.ws->epoch[rank];  // same epoch as the dispatch it answers
-  if (phase & TF_PHASE_PRE) {
+  if ((phase & TF_PHASE_PRE) && w > 1) {
     tf::PeerSig flags{};
     for (int p = 0; p < w; ++p) flags.p[p] = t->pes[p].sig + sig;
     tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
   if (phase & TF_PHASE_MAIN) {
-    tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e,
-                                                             t->timeout_ns, t->err_word(rank),
-                                                             0x5200000ull);
+    if (w > 1)
+      tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e,
+                                                               t->timeout_ns, t->err_word(rank),
+                                                               0x5200000ull);
     tf::PeerPtrs y{};
     for (int p = 0; p < w; ++p) y.p[p] = t->pes[p].base + m.yout_off;
     if (a->tokens > 0)

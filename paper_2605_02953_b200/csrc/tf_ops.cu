@@ -174,8 +174,10 @@ GemmLaunch base_launch(const tf_gemm_args* a) {
 }
 
 int gemm_grid(const tf_gemm_args* a) {
+  // comm / reduce CTAs are small and co-reside with the 1-CTA/SM GEMM, so the
+  // GEMM keeps every SM unless num_gemm_sms pins it (reference semantics)
   const int sms = num_sms_of_current_device();
-  int g = a->num_gemm_sms > 0 ? a->num_gemm_sms : sms - a->num_comm_sms;
+  int g = a->num_gemm_sms > 0 ? a->num_gemm_sms : sms;
   if (g < 1) g = 1;
   if (g > sms) g = sms;
   return g;
