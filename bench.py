@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--group-m", type=int, default=int(os.environ.get("TF_GROUP_M", "8")))
     p.add_argument("--no-moe", action="store_true")
+    p.add_argument("--no-attn", action="store_true")
     return p.parse_args()
 
 
@@ -244,6 +245,67 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
                            "unit": "GB/s per rank per direction (measured peer copy, B200_PROFILING.md)",
                            "frac": round(ach / 770.0, 4)}
     return out
+
+
+# ------------------------------------------------------------------ SP attention scores (config 3)
+ATT_S, ATT_SP, ATT_HQ, ATT_HKV, ATT_D = 32768, 8, 64, 8, 128
+
+
+def bench_attention(dev, steps, peaks):
+    """Config 3 per-rank work: Q [4096, 64, 128] . K_all [32768, 8, 128]^T with the
+    K AllGather fused (SP=8).  On one GPU the 8 SP ranks are emulated by a local
+    team whose PEs share the device; their fused calls run back to back and the
+    per-rank time is the total / 8.  Scores are bf16 and written to one reused
+    buffer (materialising all ranks' 17.2 GB each is not the point)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2605_02953_b200 import _lib
+    from paper_2605_02953_b200 import kernels as K
+    from paper_2605_02953_b200.attention import _attn_args
+    from paper_2605_02953_b200.shmem import Team
+    sl = ATT_S // ATT_SP
+    g = torch.Generator(device="cpu").manual_seed(99)
+    team = Team(ATT_SP, [dev] * ATT_SP, 2 * ATT_S * ATT_HKV * ATT_D * 2 + (16 << 20), 256)
+    qs = [torch.randn(sl, ATT_HQ, ATT_D, generator=g).to(torch.bfloat16).to(f"cuda:{dev}") for _ in range(ATT_SP)]
+    ks = [torch.randn(sl, ATT_HKV, ATT_D, generator=g).to(torch.bfloat16).to(f"cuda:{dev}") for _ in range(ATT_SP)]
+    out = torch.empty(ATT_HQ, sl, ATT_S, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    maps = [K.tile_map_tensor(ATT_S, r, ATT_SP, 1, "ag_gemm", f"cuda:{dev}", 256) for r in range(ATT_SP)]
+    args = [_attn_args(qs[r], ks[r], out, sl, ATT_HQ, ATT_HKV, ATT_D, torch.bfloat16, 256, 256, 8, 0,
+                       maps[r]) for r in range(ATT_SP)]
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
+            for r in range(ATT_SP):
+                _lib.call("tf_ag_kv_scores", team.handle, r, C.byref(args[r]), phase,
+                          stream.cuda_stream, None)
+
+    step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    team.check()
+    per_rank_ms = e0.elapsed_time(e1) / steps / ATT_SP
+    flops = 2.0 * sl * ATT_S * ATT_D * ATT_HQ
+    score_bytes = sl * ATT_S * ATT_HQ * 2
+    t_tc = flops / (peaks.get("bf16_tflops", 1622.7) * 1e12)
+    t_hbm = score_bytes / (peaks.get("hbm_gbs", 6550.1) * 1e9)
+    t_roof = max(t_tc, t_hbm)
+    team.close()
+    return {"workload": "config 3 per SP rank: Q[4096,64,128] . AG(K)[32768,8,128]^T, GQA 8:1, bf16 "
+                        "scores; SP=8 emulated on one GPU (per-rank = total / 8)",
+            "ms_per_rank": round(per_rank_ms, 4),
+            "tflops_per_rank": round(flops / (per_rank_ms * 1e-3) / 1e12, 2),
+            "roofline": {"bound": "hbm" if t_hbm > t_tc else "tensor",
+                         "t_roof_ms": round(t_roof * 1e3, 4),
+                         "frac": round(t_roof / (per_rank_ms * 1e-3), 4),
+                         "note": "materialised scores (17.2 GB/rank) make QK^T write-bound; flash fusion is next"}}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -462,6 +524,10 @@ def main_ours(args):
         moe = bench_moe(team, dev, world, rank, args.steps, args.warmup, flush, stream,
                         distributed, peaks)
 
+    attn = None
+    if not args.no_attn and world == 1:
+        attn = bench_attention(dev, 3, peaks)
+
     launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
     if rank == 0:
         line = {
@@ -481,7 +547,7 @@ def main_ours(args):
                 "ms_per_step": round(cub_ms, 4),
                 "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
                 "speedup": round(cub_ms / step_ms, 4)},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "attention": attn,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -172,6 +172,25 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
 int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
                void* comm_stream);
 
+/* ------------------------------------------------------------------ SP attention scores
+ * AllGather-KV fused with Q.K^T (BASELINE config 3): structurally
+ * ag_gemm (ag_gemm.py:20-94) with the gathered operand on the N (key) side.
+ * Per rank: q = [s_local, hq, d] queries, k = [s_local, hkv, d] keys (GQA,
+ * hq % hkv == 0); scores[h] = q[:, h, :] . K_all[:, h / (hq/hkv), :]^T, i.e.
+ * scores = [hq, s_local, world * s_local].  The key shards are pulled into the
+ * symmetric workspace with per-chunk flags; every head's GEMM acquire-waits on
+ * the key chunks its tiles cover, in gather-swizzled key-tile order. */
+typedef struct tf_attn_args {
+  const void* q;
+  const void* k;
+  void* scores;
+  int64_t s_local, hq, hkv, d;  /* d % 8 == 0 */
+  int32_t out_dtype, block_m, block_n, group_m, num_gemm_sms, swizzle;
+  const int32_t* key_tile_map;  /* optional device [ceil(S/block_n)] permutation */
+} tf_attn_args;
+int tf_ag_kv_scores(tf_team* t, int rank, const tf_attn_args* a, int phase, void* stream,
+                    void* comm_stream);
+
 /* ------------------------------------------------------------------ MoE (expert parallel)
  * Not in the reference as an all-to-all; what the reference pins
  * is the layout: the [world, E] routing-count matrix (ag_moe.py:28-33) and the

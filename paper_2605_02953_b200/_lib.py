@@ -44,6 +44,14 @@ class MoeArgs(C.Structure):
     ]
 
 
+class AttnArgs(C.Structure):
+    _fields_ = [
+        ("q", vp), ("k", vp), ("scores", vp), ("s_local", i64), ("hq", i64), ("hkv", i64),
+        ("d", i64), ("out_dtype", i32), ("block_m", i32), ("block_n", i32), ("group_m", i32),
+        ("num_gemm_sms", i32), ("swizzle", i32), ("key_tile_map", vp),
+    ]
+
+
 _SIGS = {
     "tf_last_error": (C.c_char_p, []),
     "tf_version": (C.c_char_p, []),
@@ -75,6 +83,7 @@ _SIGS = {
     "tf_gemm": (ci, [C.POINTER(GemmArgs), vp]),
     "tf_ag_gemm": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_gemm_rs": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
+    "tf_ag_kv_scores": (ci, [vp, ci, C.POINTER(AttnArgs), ci, vp, vp]),
     "tf_moe_topk": (ci, [vp, i64, ci, ci, vp, vp, vp]),
     "tf_moe_count_scratch_bytes": (i64, [i64, ci]),
     "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp, vp]),

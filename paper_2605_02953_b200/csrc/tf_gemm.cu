@@ -63,6 +63,9 @@ struct KParams {
   int tail_base;
   int split_s;
   int total_work;
+  // AllGather on the B (N-side) operand instead of A, and an N-tile permutation
+  int wait_on_b;
+  const int32_t* tile_map_n;
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -100,6 +103,7 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid
   pid_m = first_m + r % rows;
   pid_n = r / rows;
   if (p.tile_map) pid_m = __ldg(p.tile_map + pid_m);
+  if (p.tile_map_n) pid_n = __ldg(p.tile_map_n + pid_n);
 }
 
 // Row offset, inside the tile, of this CTA's A block h: MMA h covers tile rows
@@ -202,9 +206,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           bool waited = false;
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
-            const int m0 = tile_m0 + block_row<CG>(h, cta_rank);
-            if (m0 >= p.m) continue;
-            const int r1 = min(m0 + 128, p.m) - 1;
+            // rows of the gathered operand this CTA loads: A blocks, or its B rows
+            const int m0 = p.wait_on_b ? n0 : tile_m0 + block_row<CG>(h, cta_rank);
+            const int lim = p.wait_on_b ? p.n : p.m;
+            const int span = p.wait_on_b ? S::kBRows : 128;
+            if (m0 >= lim || (p.wait_on_b && h > 0)) continue;
+            const int r1 = min(m0 + span, lim) - 1;
             const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
             const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
             for (int c = c_beg; c <= c_end; ++c) {
@@ -752,7 +759,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     return fail(TF_ERR_INVALID, "GEMM dimension exceeds int32");
   if (g.epilogue == 1 && (g.world < 1 || g.world > kMaxWorld || g.rows_per_rank <= 0))
     return fail(TF_ERR_INVALID, "scatter epilogue needs 1 <= world <= TF_MAX_WORLD");
-  if (g.chunk_flags && g.m / g.rows_per_chunk + 1 > 32)
+  if (g.chunk_flags && (g.wait_on_b ? g.n : g.m) / g.rows_per_chunk + 1 > 32)
     return fail(TF_ERR_CONFIG, "AllGather wait supports at most 32 chunks");
   if (g.group_m < 1) return fail(TF_ERR_CONFIG, "group_m must be >= 1");
 
@@ -787,6 +794,8 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.err = g.err;
   kp.timeout_ns = g.timeout_ns;
   kp.dbg_skip_store = getenv("TF_DEBUG_SKIP_STORE") ? 1 : 0;
+  kp.wait_on_b = g.wait_on_b ? 1 : 0;
+  kp.tile_map_n = g.tile_map_n;
   if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
 
   const int cg = tile_m == 128 ? 1 : 2;
@@ -829,6 +838,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     if (split > 8) split = 8;
     while (split > 1 && kp.num_kb / split < 4) --split;
     if (g.epilogue == 0 && tiles > clusters && rem > 0 && split >= 2 && !g.no_tail_split &&
+        !g.wait_on_b &&
         !getenv("TF_DEBUG_NO_SPLITK")) {
       const int tile_m_rows = tile_m;
       const size_t bytes = static_cast<size_t>(rem) * split * tile_m_rows * g.block_n * 4;

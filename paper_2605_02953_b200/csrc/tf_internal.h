@@ -53,6 +53,8 @@ struct GemmLaunch {
   unsigned long long* err = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
   bool no_tail_split = false;        // disable the split-K tail (e.g. inside fused protocols)
+  bool wait_on_b = false;            // chunk flags guard B rows (gathered N-side operand)
+  const int32_t* tile_map_n = nullptr; // device [num_pid_n] permutation or nullptr
 };
 
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);

@@ -402,4 +402,92 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
   return TF_OK;
 }
 
+int tf_ag_kv_scores(tf_team* t, int rank, const tf_attn_args* a, int phase, void* stream,
+                    void* comm_stream) {
+  if (!t || !a || rank < 0 || rank >= t->world) return fail(TF_ERR_INVALID, "bad team/rank/args");
+  if (!t->is_local(rank)) return fail(TF_ERR_INVALID, "rank is not owned by this process");
+  if (a->s_local < 0 || a->hq < 1 || a->hkv < 1 || a->hq % a->hkv)
+    return fail(TF_ERR_INVALID, "need hq % hkv == 0 and positive head counts");
+  if (a->d < 8 || a->d % 8) return fail(TF_ERR_INVALID, "head dim must be a positive multiple of 8");
+  if (a->out_dtype != TF_DTYPE_BF16 && a->out_dtype != TF_DTYPE_F32)
+    return fail(TF_ERR_INVALID, "out_dtype must be TF_DTYPE_BF16 or TF_DTYPE_F32");
+  const int w = t->world;
+  const int64_t sl = a->s_local, st = sl * w;
+  const int64_t krow = a->hkv * a->d;  // one key row: all kv heads
+  const size_t chunk_bytes = static_cast<size_t>(sl) * krow * 2;
+  auto s = static_cast<cudaStream_t>(stream);
+  auto cs = comm_stream ? static_cast<cudaStream_t>(comm_stream) : s;
+  int rc = TF_OK;
+  const std::string key = "agkv:" + std::to_string(st) + "x" + std::to_string(krow);
+  tf::Workspace* ws = t->workspace(key, 2 * chunk_bytes * w, 2 * w, &rc);
+  if (!ws) return rc;
+  if (phase & TF_PHASE_PRE) {
+    const uint64_t e = ++ws->epoch[rank];
+    const int par = static_cast<int>(e & 1);
+    uint8_t* own = t->pes[rank].base + ws->data_off + par * chunk_bytes * w;
+    if (chunk_bytes)
+      TF_CUDA_TRY(cudaMemcpyAsync(own + rank * chunk_bytes, a->k, chunk_bytes, cudaMemcpyDefault, s));
+    rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + rank, e, s);
+    if (rc) return rc;
+    if (w > 1) {
+      rc = tf::team_barrier_arrive(t, rank, s);
+      if (rc) return rc;
+    }
+  }
+  if (phase & TF_PHASE_MAIN) {
+    const uint64_t e = ws->epoch[rank];
+    const int par = static_cast<int>(e & 1);
+    const size_t buf_off = ws->data_off + par * chunk_bytes * w;
+    uint8_t* own = t->pes[rank].base + buf_off;
+    if (w > 1) {
+      rc = tf::team_barrier_wait(t, rank, s);
+      if (rc) return rc;
+      rc = tf::StreamJoin::fork(s, cs);
+      if (rc) return rc;
+      for (int i = 1; i < w; ++i) {
+        const int src = (rank + i) % w;  // pull order of ag_gemm.py:64-69
+        TF_CUDA_TRY(cudaMemcpyAsync(own + src * chunk_bytes,
+                                    t->pes[src].base + buf_off + src * chunk_bytes, chunk_bytes,
+                                    cudaMemcpyDefault, cs));
+        rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + src, e, cs);
+        if (rc) return rc;
+      }
+    }
+    const int64_t group = a->hq / a->hkv;
+    const int esz = a->out_dtype == TF_DTYPE_F32 ? 4 : 2;
+    for (int64_t h = 0; h < a->hq && sl > 0; ++h) {
+      tf::GemmLaunch g;
+      g.a = static_cast<const uint8_t*>(a->q) + h * a->d * 2;  // Q_h: rows stride hq*d
+      g.lda = a->hq * a->d;
+      g.b = own + (h / group) * a->d * 2;                        // K_g: rows stride hkv*d
+      g.ldb = krow;
+      g.m = sl;
+      g.n = st;
+      g.k = a->d;
+      g.block_m = a->block_m ? a->block_m : 256;
+      g.block_n = a->block_n ? a->block_n : 256;
+      g.group_m = a->group_m > 0 ? a->group_m : 8;
+      g.num_sms = a->num_gemm_sms > 0 ? a->num_gemm_sms : tf::num_sms_of_current_device();
+      g.tile_map_n = a->swizzle ? a->key_tile_map : nullptr;
+      g.out_f32 = a->out_dtype == TF_DTYPE_F32;
+      g.c = static_cast<uint8_t*>(a->scores) + static_cast<size_t>(h) * sl * st * esz;
+      g.ldc = st;
+      g.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
+      g.epoch = e;
+      g.rows_per_chunk = sl;
+      g.wait_on_b = true;
+      g.no_tail_split = true;
+      g.err = t->err_word(rank);
+      g.timeout_ns = t->timeout_ns;
+      rc = tf::launch_gemm(g, s);
+      if (rc) return rc;
+    }
+    if (w > 1) {
+      rc = tf::StreamJoin::fork(cs, s);
+      if (rc) return rc;
+    }
+  }
+  return TF_OK;
+}
+
 }  // extern "C"
