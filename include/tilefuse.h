@@ -42,7 +42,8 @@ enum {
 enum { TF_DTYPE_BF16 = 0, TF_DTYPE_F32 = 1 };
 enum { TF_REDUCE_RING = 0, TF_REDUCE_ASCENDING = 1 };
 /* phases of a per-rank collective call */
-enum { TF_PHASE_PRE = 1, TF_PHASE_MAIN = 2, TF_PHASE_POST = 4, TF_PHASE_ALL = 7 };
+enum { TF_PHASE_PRE = 1, TF_PHASE_MAIN = 2, TF_PHASE_POST = 4, TF_PHASE_FINAL = 8,
+       TF_PHASE_ALL = 15 };
 
 typedef struct tf_team tf_team;
 
@@ -171,6 +172,22 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
  * + counter reset. */
 int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* stream,
                void* comm_stream);
+
+/* GEMM+AllReduce (gemm_ar.py:25-153).  Per rank: a = [m, k] and b = [n, k]
+ * partial operands, c = [m, n] = sum over ranks of a_r . b_r^T (same on every rank).
+ * The GEMM writes its partial into the symmetric workspace and bumps a
+ * per-128-row-block counter (epoch-valued, never reset: target = epoch*tiles).
+ * two_shot = 0: every rank pulls every block from all peers and reduces it in
+ *   ascending rank order (gemm_ar.py:95-102).
+ * two_shot = 1: block b is owned by rank b % world; the owner reduces it and
+ *   P2P-stores the result into every peer's result buffer, then releases a
+ *   per-block flag (multimem_st analogue, gemm_ar.py:103-133); every rank copies
+ *   the result once all blocks are flagged.
+ * phases as tf_gemm_rs: PRE = barrier arrive, MAIN = barrier wait + GEMM (+
+ * overlapped reduce when no other rank shares the device), POST = reduce,
+ * FINAL = two-shot result gather (after every rank's POST). */
+int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int phase,
+               void* stream, void* comm_stream);
 
 /* ------------------------------------------------------------------ SP attention scores
  * AllGather-KV fused with Q.K^T (BASELINE config 3): structurally

@@ -14,15 +14,22 @@ __all__ = [
     "WorkloadContext", "WorkloadRun", "reduce_visit_order", "AllocationError", "BuildError",
     "ConfigError", "DeadlockError", "ProtocolError", "VerificationError", "LINK_PROFILES",
     "LinkConfig", "Topology", "build_topology", "local_rank_of", "node_of",
-    "ag_gemm", "gemm_rs", "gemm", "AllGatherGemm", "GemmReduceScatter", "SymmetricHeap", "Team",
+    "ag_gemm", "gemm_rs", "gemm", "gemm_allreduce", "AllGatherGemm", "GemmReduceScatter",
+    "SymmetricHeap", "Team", "ag_moe_group_gemm", "ExpertParallelMoE", "moe_route", "ag_kv_scores",
 ]
 
 
 def __getattr__(name):
     # the operator modules import torch + the CUDA library lazily
-    if name in ("ag_gemm", "gemm_rs", "gemm", "AllGatherGemm", "GemmReduceScatter"):
+    if name in ("ag_gemm", "gemm_rs", "gemm", "gemm_allreduce", "AllGatherGemm", "GemmReduceScatter"):
         from . import kernels
         return getattr(kernels, name)
+    if name in ("ag_moe_group_gemm", "ExpertParallelMoE", "moe_route"):
+        from . import moe
+        return getattr(moe, name)
+    if name in ("ag_kv_scores",):
+        from . import attention
+        return getattr(attention, name)
     if name in ("SymmetricHeap", "Team"):
         from . import shmem
         return getattr(shmem, name)

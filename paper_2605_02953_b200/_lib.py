@@ -18,7 +18,8 @@ HEADER = pathlib.Path(__file__).resolve().parent.parent / "include" / "tilefuse.
 
 TF_DTYPE_BF16, TF_DTYPE_F32 = 0, 1
 TF_REDUCE_RING, TF_REDUCE_ASCENDING = 0, 1
-PHASE_PRE, PHASE_MAIN, PHASE_POST, PHASE_ALL = 1, 2, 4, 7
+PHASE_PRE, PHASE_MAIN, PHASE_POST, PHASE_FINAL = 1, 2, 4, 8  # FINAL: gemm_ar two-shot gather
+PHASE_ALL = 15
 MAX_WORLD = 16
 
 vp = C.c_void_p
@@ -84,6 +85,7 @@ _SIGS = {
     "tf_ag_gemm": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_gemm_rs": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_ag_kv_scores": (ci, [vp, ci, C.POINTER(AttnArgs), ci, vp, vp]),
+    "tf_gemm_ar": (ci, [vp, ci, C.POINTER(GemmArgs), ci, ci, vp, vp]),
     "tf_moe_topk": (ci, [vp, i64, ci, ci, vp, vp, vp]),
     "tf_moe_count_scratch_bytes": (i64, [i64, ci]),
     "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp, vp]),

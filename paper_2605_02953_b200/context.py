@@ -66,7 +66,7 @@ class WorkloadContext:
     def hw_block_m(self) -> int:
         # 512 / 256 = CTA pair per tile (tcgen05 cta_group::2, two or one M=256
         # MMA per k-step); smaller = one CTA, 128 rows
-        if self.block_m >= 512:
+        if self.block_m >= 512 and self.hw_block_n == 256:
             return 512
         return 256 if self.block_m >= 256 else 128
 

@@ -127,6 +127,134 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(
   }
 }
 
+struct PeerBase {
+  const void* p[kMaxWorld];
+};
+struct PeerCnt {
+  const uint64_t* p[kMaxWorld];
+};
+struct PeerOut {
+  void* p[kMaxWorld];
+};
+struct PeerFlag {
+  uint64_t* p[kMaxWorld];
+};
+
+// GEMM+AllReduce reduction.  Work item = (128-row block b, 2048-column chunk).
+// one-shot (bcast == 0): reduce every block into `out` (local).
+// two-shot (bcast == 1): reduce only blocks b % world == rank, store the result
+// into every peer's result buffer and release flag[b] on each peer.
+template <bool IN_F32>
+__global__ void __launch_bounds__(256) ar_reduce_kernel(
+    PeerBase parts, long long ld, int world, int rank, int bcast, void* out, long long out_ld,
+    int out_f32, int out_vec, PeerOut results, PeerFlag flags, long long m, long long n,
+    PeerCnt counters, unsigned long long expected, int col_chunks, unsigned long long epoch,
+    unsigned long long timeout_ns, unsigned long long* err) {
+  const int nblocks = static_cast<int>((m + 127) / 128);
+  const int my_blocks = bcast ? (nblocks - rank + world - 1) / world : nblocks;
+  const int items = my_blocks * col_chunks;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int bi = item / col_chunks;
+    const int cc = item - bi * col_chunks;
+    const int b = bcast ? rank + bi * world : bi;
+    if (threadIdx.x < world)
+      wait_geq_sys(counters.p[threadIdx.x] + b, expected, timeout_ns, err, 0x4000000ull | b);
+    __syncthreads();
+    const long long r0 = static_cast<long long>(b) * 128;
+    const long long r1 = min(r0 + 128, m);
+    const long long c0 = static_cast<long long>(cc) * 2048;
+    const long long c1 = min(c0 + 2048, n);
+    const long long vec_per_row = (c1 - c0 + 7) / 8;
+    const long long total = (r1 - r0) * vec_per_row;
+    for (long long v = threadIdx.x; v < total; v += blockDim.x) {
+      const long long r = r0 + v / vec_per_row;
+      const long long c = c0 + (v % vec_per_row) * 8;
+      const bool full = c + 8 <= n;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int s = 0; s < world; ++s) {  // ascending rank order: deterministic
+        if constexpr (IN_F32) {
+          const float* p = static_cast<const float*>(parts.p[s]) + r * ld + c;
+          if (full) {
+            const float4 x0 = *reinterpret_cast<const float4*>(p);
+            const float4 x1 = *reinterpret_cast<const float4*>(p + 4);
+            acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
+            acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j) acc[j] += p[j];
+          }
+        } else {
+          const uint16_t* p = static_cast<const uint16_t*>(parts.p[s]) + r * ld + c;
+          if (full) {
+            const uint4 x = *reinterpret_cast<const uint4*>(p);
+            const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              acc[2 * j] += __uint_as_float(w4[j] << 16);
+              acc[2 * j + 1] += __uint_as_float(w4[j] & 0xFFFF0000u);
+            }
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j)
+              acc[j] += __uint_as_float(static_cast<uint32_t>(p[j]) << 16);
+          }
+        }
+      }
+      const int ndst = bcast ? world : 1;
+      for (int d = 0; d < ndst; ++d) {
+        void* base = bcast ? results.p[d] : out;
+        const long long oll = bcast ? ld : out_ld;
+        const bool vec = full && (bcast ? true : out_vec);
+        if (out_f32) {
+          float* o = static_cast<float*>(base) + r * oll + c;
+          if (vec) {
+            *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j) o[j] = acc[j];
+          }
+        } else {
+          uint16_t* o = static_cast<uint16_t*>(base) + r * oll + c;
+          if (vec) {
+            *reinterpret_cast<uint4*>(o) =
+                make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                           pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+          } else {
+            for (int j = 0; j < 8 && c + j < n; ++j)
+              o[j] = static_cast<uint16_t>(pack_bf16x2(acc[j], 0.f) & 0xFFFF);
+          }
+        }
+      }
+    }
+    if (bcast) {
+      // publish the block's chunk: stores visible system-wide, then flag every peer
+      fence_sys();
+      __syncthreads();
+      if (threadIdx.x < world) red_add_release_sys(flags.p[threadIdx.x] + b, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// two-shot tail: wait until every block's column chunks have been flagged
+// (target = epoch * col_chunks), then copy the result buffer into `out`.
+__global__ void ar_gather_kernel(const void* result, long long ld, void* out, long long out_ld,
+                                 int esz, long long m, long long n, const uint64_t* flags,
+                                 unsigned long long target, unsigned long long timeout_ns,
+                                 unsigned long long* err) {
+  const int nblocks = static_cast<int>((m + 127) / 128);
+  for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    if (threadIdx.x == 0) wait_geq_sys(flags + b, target, timeout_ns, err, 0x4800000ull | b);
+    __syncthreads();
+    const long long r0 = static_cast<long long>(b) * 128, r1 = min(r0 + 128, m);
+    const long long row_bytes = n * esz;
+    for (long long r = r0; r < r1; ++r) {
+      const uint8_t* src = static_cast<const uint8_t*>(result) + r * ld * esz;
+      uint8_t* dst = static_cast<uint8_t*>(out) + r * out_ld * esz;
+      for (long long i = threadIdx.x; i < row_bytes; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+  }
+}
+
 struct StreamJoin {
   // fork `side` from `main` and join back; no-ops when they are the same stream
   static int fork(cudaStream_t main, cudaStream_t side) {
@@ -398,6 +526,128 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
       rc = launch_reduce(s);
       if (rc) return rc;
     }
+  }
+  return TF_OK;
+}
+
+int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int phase,
+               void* stream, void* comm_stream) {
+  if (!t || rank < 0 || rank >= t->world) return fail(TF_ERR_INVALID, "rank out of range");
+  if (!t->is_local(rank)) return fail(TF_ERR_INVALID, "rank is not owned by this process");
+  int rc = tf::check_gemm_args(args);
+  if (rc) return rc;
+  const int w = t->world;
+  const int64_t m = args->m, n = args->n;
+  const bool f32 = args->out_dtype == TF_DTYPE_F32;
+  const int esz = f32 ? 4 : 2;
+  const int64_t ld = (n + 7) / 8 * 8;
+  const int bn = args->block_n ? args->block_n : 256;
+  const int64_t num_pid_n = (n + bn - 1) / bn;
+  const int64_t nblocks = (m + 127) / 128;
+  const int col_chunks = static_cast<int>((n + 2047) / 2048);
+  const size_t bytes = static_cast<size_t>(m) * ld * esz;
+  // one workspace per protocol: the broadcast flags only advance in two-shot calls,
+  // so their epoch must not be shared with one-shot calls
+  const std::string key = std::string(two_shot ? "ar2:" : "ar1:") + std::to_string(m) + "x" +
+                          std::to_string(n) + (f32 ? "f" : "h") + ":" + std::to_string(bn);
+  // data: partial [m][ld] + result [m][ld]; signals: counters [nblocks] + flags [nblocks]
+  tf::Workspace* ws = t->workspace(key, 2 * bytes, 2 * static_cast<size_t>(nblocks), &rc);
+  if (!ws) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  auto cs = comm_stream ? static_cast<cudaStream_t>(comm_stream) : s;
+  const bool overlap = t->distinct_devices && cs != s && w > 1;
+  if (phase & TF_PHASE_PRE) {
+    ++ws->epoch[rank];
+    rc = tf::team_barrier_arrive(t, rank, s);
+    if (rc) return rc;
+  }
+  const uint64_t e = ws->epoch[rank];
+  auto launch_reduce = [&](cudaStream_t rs) -> int {
+    tf::PeerBase parts{};
+    tf::PeerCnt cnt{};
+    tf::PeerOut res{};
+    tf::PeerFlag flg{};
+    for (int p = 0; p < w; ++p) {
+      parts.p[p] = t->pes[p].base + ws->data_off;
+      cnt.p[p] = t->pes[p].sig + ws->sig_base;
+      res.p[p] = t->pes[p].base + ws->data_off + bytes;
+      flg.p[p] = t->pes[p].sig + ws->sig_base + nblocks;
+    }
+    const int64_t ldc = args->ldc ? args->ldc : n;
+    const int out_vec = ((ldc * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(args->c) % 16 == 0);
+    int grid = overlap ? (args->num_comm_sms > 0 ? args->num_comm_sms * 2 : 16)
+                       : tf::num_sms_of_current_device();
+    const int64_t my_blocks = two_shot ? (nblocks - rank + w - 1) / w : nblocks;
+    if (grid > my_blocks * col_chunks) grid = static_cast<int>(my_blocks * col_chunks);
+    if (grid < 1) grid = 1;
+    const unsigned long long expected = e * static_cast<unsigned long long>(num_pid_n);
+    if (f32)
+      tf::ar_reduce_kernel<true><<<grid, 256, 0, rs>>>(
+          parts, ld, w, rank, two_shot, args->c, ldc, 1, out_vec, res, flg, m, n, cnt, expected,
+          col_chunks, e, t->timeout_ns, t->err_word(rank));
+    else
+      tf::ar_reduce_kernel<false><<<grid, 256, 0, rs>>>(
+          parts, ld, w, rank, two_shot, args->c, ldc, 0, out_vec, res, flg, m, n, cnt, expected,
+          col_chunks, e, t->timeout_ns, t->err_word(rank));
+    TF_CUDA_TRY(cudaGetLastError());
+    return TF_OK;
+  };
+  auto launch_gather = [&](cudaStream_t gs) -> int {
+    const int64_t ldc = args->ldc ? args->ldc : n;
+    int grid = static_cast<int>(std::min<int64_t>(nblocks, tf::num_sms_of_current_device()));
+    tf::ar_gather_kernel<<<std::max(grid, 1), 256, 0, gs>>>(
+        t->pes[rank].base + ws->data_off + bytes, ld, args->c, ldc, esz, m, n,
+        t->pes[rank].sig + ws->sig_base + nblocks, e * static_cast<unsigned long long>(col_chunks),
+        t->timeout_ns, t->err_word(rank));
+    TF_CUDA_TRY(cudaGetLastError());
+    return TF_OK;
+  };
+  if (phase & TF_PHASE_MAIN) {
+    rc = tf::team_barrier_wait(t, rank, s);
+    if (rc) return rc;
+    tf::GemmLaunch g = tf::base_launch(args);
+    g.num_sms = tf::gemm_grid(args);
+    g.epilogue = 1;  // own partial buffer + own counters (single "owner")
+    g.rank = 0;
+    g.world = 1;
+    g.rows_per_rank = m;
+    g.slot_ld = ld;
+    g.out_f32 = f32;
+    g.peer_slots[0] = t->pes[rank].base + ws->data_off;
+    g.peer_counts[0] = t->pes[rank].sig + ws->sig_base;
+    g.err = t->err_word(rank);
+    g.timeout_ns = t->timeout_ns;
+    cudaEvent_t pre = nullptr;
+    if (overlap) {
+      TF_CUDA_TRY(cudaEventCreateWithFlags(&pre, cudaEventDisableTiming));
+      TF_CUDA_TRY(cudaEventRecord(pre, s));
+    }
+    rc = tf::launch_gemm(g, s);
+    if (rc) return rc;
+    if (overlap) {
+      TF_CUDA_TRY(cudaStreamWaitEvent(cs, pre, 0));
+      cudaEventDestroy(pre);
+      rc = launch_reduce(cs);
+      if (rc) return rc;
+      if (two_shot) {
+        rc = launch_gather(cs);
+        if (rc) return rc;
+      }
+      rc = tf::StreamJoin::fork(cs, s);
+      if (rc) return rc;
+    }
+  }
+  if (phase & TF_PHASE_POST) {
+    if (!overlap) {
+      rc = launch_reduce(s);
+      if (rc) return rc;
+    }
+  }
+  // two-shot results are only complete once every owner has broadcast: with shared
+  // devices the gather must follow every rank's POST, so it runs as a 4th phase bit
+  if ((phase & 8) && two_shot && !overlap) {
+    rc = launch_gather(s);
+    if (rc) return rc;
   }
   return TF_OK;
 }

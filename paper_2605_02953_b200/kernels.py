@@ -179,15 +179,16 @@ def _ptr(s) -> int | None:
     return None if s is None else s.cuda_stream
 
 
-def _drive(team: Team, fn_name: str, per_rank_args: dict, ranks):
-    """Run PRE for all local ranks, then MAIN, then POST (single-process teams)."""
-    for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
+def _drive(team: Team, fn_name: str, per_rank_args: dict, ranks, extra=()):
+    """Run PRE for all local ranks, then MAIN, then POST, then FINAL
+    (single-process teams: PEs sharing a stream never wait on later work)."""
+    for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST, _lib.PHASE_FINAL):
         for r in ranks:
             dev = team.devices[r]
             with torch.cuda.device(dev):
                 s, cs = _streams(team, r)
-                _lib.call(fn_name, team.handle, r, C.byref(per_rank_args[r]), phase,
-                          _ptr(s), _ptr(cs))
+                _lib.call(fn_name, team.handle, r, C.byref(per_rank_args[r]), *extra,
+                          phase, _ptr(s), _ptr(cs))
 
 
 # ----------------------------------------------------------------- core GEMM
@@ -418,5 +419,93 @@ class GemmReduceScatter:
         args = {r: self._args(r, x[r], w[r], outs[r]) for r in range(t.world)}
         _drive(t, "tf_gemm_rs", args, range(t.world))
         return outs
+
+    __call__ = forward
+
+
+# ----------------------------------------------------------------- GEMM + AllReduce
+def gemm_allreduce(a_shards, b_shards, ctx: WorkloadContext, use_multimem_st: bool | None = None) -> WorkloadRun:
+    """Per rank: sum_w(a_w @ b_w.T), shape [M, N], identical on every rank
+    (ovs/kernels/gemm_ar.py:25).  use_multimem_st selects the two-shot protocol
+    (owner reduce + P2P broadcast), else one-shot (every rank pull-reduces)."""
+    topo = ctx.topology
+    world = topo.world_size
+    if topo.nnodes != 1:
+        raise ValueError("allreduce workload requires a single node (node-team reduction)")
+    if len(a_shards) != world or len(b_shards) != world:
+        raise ValueError(f"need {world} shards per operand")
+    check_dtype(*a_shards, *b_shards)
+    m, k = a_shards[0].shape
+    n = b_shards[0].shape[0]
+    if n % ctx.block_n != 0:
+        raise ValueError(f"N={n} must be divisible by block_n={ctx.block_n}")
+    for a, b in zip(a_shards, b_shards):
+        if tuple(a.shape) != (m, k) or tuple(b.shape) != (n, k):
+            raise ValueError("ragged shards")
+    two_shot = ctx.use_multimem_st if use_multimem_st is None else use_multimem_st
+    kp = (k + 7) // 8 * 8
+    devices = _devices_for(ctx, a_shards)
+    pa = _prepare(a_shards, devices, kp)
+    pb = _prepare(b_shards, devices, kp)
+    _exact_bound_check(pa, pb, k, extra_terms=world)
+    odt = _out_dtype(ctx.out_dtype, pa)
+    esz = 4 if odt == torch.float32 else 2
+    ld = (n + 7) // 8 * 8
+    nblocks = (m + 127) // 128
+    team = Team(world, devices, 2 * m * ld * esz + (1 << 20), 2 * nblocks + 64)
+    heap = SymmetricHeap(topo, team=team)
+    outs, args = [], {}
+    for r in range(world):
+        out = torch.empty((m, n), dtype=odt, device=f"cuda:{devices[r]}")
+        args[r] = _args(pa.tensors[r], pb.tensors[r], out, m, n, kp, out_dtype=odt,
+                        block_n=ctx.hw_block_n, group_m=ctx.group_m, num_gemm_sms=ctx.num_gemm_sms,
+                        num_comm_sms=ctx.num_comm_sms, swizzle=False, tile_map=None,
+                        block_m=ctx.hw_block_m)
+        outs.append(out)
+    if m > 0 and n > 0:
+        _drive(team, "tf_gemm_ar", args, range(world), extra=(1 if two_shot else 0,))
+    for d in sorted(set(devices)):
+        torch.cuda.synchronize(d)
+    team.check()
+    # teardown like the reference (gemm_ar.py:128-153): every flag reads 0 afterwards
+    tile_ready = SigHandle(base=world + 1, nslots=nblocks)
+    mst_sig = SigHandle(base=world + 1 + nblocks, nslots=nblocks)
+    for r in range(world):
+        with torch.cuda.device(devices[r]):
+            heap.reset_signals(tile_ready, r)
+            heap.reset_signals(mst_sig, r)
+    for d in sorted(set(devices)):
+        torch.cuda.synchronize(d)
+    return WorkloadRun([_finish(o, pa) for o in outs], None, heap,
+                       {"tile_ready": tile_ready, "mst_sig": mst_sig})
+
+
+class GemmAllReduce:
+    """Reusable fused GEMM+AllReduce for a fixed shape over a team (one rank per
+    process, or a single-rank local team)."""
+
+    def __init__(self, team: Team, m: int, k: int, n: int, *, out_dtype=torch.bfloat16,
+                 block_m: int = 512, block_n: int = 256, group_m: int = 8, num_comm_sms: int = 8,
+                 two_shot: bool = False):
+        if k % 8:
+            raise ValueError("K must be a multiple of 8")
+        self.team, self.m, self.k, self.n = team, m, k, n
+        self.out_dtype, self.block_m, self.block_n, self.group_m = out_dtype, block_m, block_n, group_m
+        self.num_comm_sms, self.two_shot = num_comm_sms, two_shot
+
+    def forward(self, a, b, out=None):
+        t = self.team
+        if t.rank is None and t.world != 1:
+            raise ValueError("GemmAllReduce drives one rank per process; use gemm_allreduce() for local teams")
+        r = t.rank or 0
+        if out is None:
+            out = torch.empty((self.m, self.n), dtype=self.out_dtype, device=a.device)
+        g = _args(a, b, out, self.m, self.n, self.k, out_dtype=out.dtype, block_n=self.block_n,
+                  group_m=self.group_m, num_gemm_sms=0, num_comm_sms=self.num_comm_sms,
+                  swizzle=False, tile_map=None, block_m=self.block_m)
+        s, cs = torch.cuda.current_stream(), side_stream(a.device.index)
+        _lib.call("tf_gemm_ar", t.handle, r, C.byref(g), 1 if self.two_shot else 0, _lib.PHASE_ALL,
+                  s.cuda_stream, cs.cuda_stream)
+        return out
 
     __call__ = forward

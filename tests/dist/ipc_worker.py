@@ -57,6 +57,13 @@ def main():
                 torch.cuda.synchronize()
                 want = OC.ref_reduce_scatter(x_all, w_all)[rank]
                 ok &= np.array_equal(y.cpu().numpy().astype(np.int64), want)
+        for two_shot in (False, True):
+            ar = K.GemmAllReduce(team, mpr, k, n, out_dtype=torch.float32, block_m=bm,
+                                 two_shot=two_shot, num_comm_sms=2)
+            for it in range(3):
+                y = ar(bf(a_all[rank]), bf(b_all[rank]))
+                torch.cuda.synchronize()
+                ok &= np.array_equal(y.cpu().numpy().astype(np.int64), OC.ref_allreduce(a_all, b_all))
     team.check()
 
     # MoE EP dispatch / combine

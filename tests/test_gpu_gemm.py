@@ -181,3 +181,63 @@ def test_validation_errors_match_reference():
         K.ag_gemm([x.astype(np.int32) for x in ga], gb, ctx)
     with pytest.raises(ValueError):
         K.gemm_rs([rng.integers(-8, 8, (7, 4)).astype(np.int64) for _ in range(2)], gb, ctx)
+
+
+# -- GEMM + AllReduce (ovs/kernels/gemm_ar.py; reference tests/test_kernels.py:229-282) --------
+
+
+@pytest.mark.parametrize("case", range(12))
+@pytest.mark.parametrize("two_shot", [False, True])
+@pytest.mark.parametrize("bm", [128, 512])
+def test_gemm_ar_exact_vs_reference_fixture(case, two_shot, bm):
+    K = _k()
+    c = G.workloads()[case]
+    w = c["world"]
+    n_ar = c["ar_y"].shape[1]
+    b = [x[:n_ar] for x in c["ag_b"]]
+    run = K.gemm_allreduce(list(c["ag_a"]), b, _ctx(w, block_m=bm, block_n=4 if n_ar % 4 == 0 else 1),
+                           use_multimem_st=two_shot)
+    for r in range(w):
+        assert np.array_equal(run.outputs[r], c["ar_y"]), (case, two_shot, r)
+
+
+def test_gemm_ar_paths_agree_and_flags_reset():
+    K = _k()
+    rng = np.random.default_rng(10)
+    world = 4
+    a = [rng.integers(-8, 8, (300, 40)) for _ in range(world)]
+    b = [rng.integers(-8, 8, (264, 40)) for _ in range(world)]
+    runs = [K.gemm_allreduce(a, b, _ctx(world, block_n=8), use_multimem_st=ts) for ts in (False, True)]
+    want = O.ref_allreduce(a, b)
+    for run in runs:
+        for r in range(world):
+            assert np.array_equal(run.outputs[r], want)
+            assert not run.heap.sig_view(run.handles["tile_ready"], r).any()
+            assert not run.heap.sig_view(run.handles["mst_sig"], r).any()
+
+
+@pytest.mark.parametrize("world", [2, 8])
+@pytest.mark.parametrize("two_shot", [False, True])
+def test_gemm_ar_bf16_tolerance(world, two_shot):
+    K = _k()
+    rng = np.random.default_rng(world)
+    m, n, k = 1000, 768, 512
+    a = [_bf16(rng, (m, k)).cuda() for _ in range(world)]
+    b = [_bf16(rng, (n, k), 1 / 32).cuda() for _ in range(world)]
+    run = K.gemm_allreduce(a, b, _ctx(world, block_n=256), use_multimem_st=two_shot)
+    want = O.ref_allreduce([x.float().cpu().numpy() for x in a], [x.float().cpu().numpy() for x in b])
+    for r in range(world):
+        assert O.compare(run.outputs[r].float().cpu().numpy(), want) <= TOL_BF16
+
+
+def test_gemm_ar_validation():
+    from paper_2605_02953_b200 import WorkloadContext, build_topology
+    K = _k()
+    rng = np.random.default_rng(12)
+    a = [rng.integers(-8, 8, (4, 4)) for _ in range(2)]
+    b = [rng.integers(-8, 8, (6, 4)) for _ in range(2)]
+    with pytest.raises(ValueError):
+        K.gemm_allreduce(a, b, _ctx(2, block_n=4))  # N=6 not divisible by block_n=4
+    multi = WorkloadContext(topology=build_topology(4, 2), devices=[0] * 4)
+    with pytest.raises(ValueError):
+        K.gemm_allreduce([rng.integers(-8, 8, (4, 4))] * 4, [rng.integers(-8, 8, (4, 4))] * 4, multi)
