@@ -259,6 +259,17 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
  * out[t] = sum_j w[t,j] * y[row(t,j)] in fp32 (slot order), bf16 out. */
 int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream);
 
+/* ------------------------------------------------------------------ device tracing
+ * Per-tile device events (%globaltimer ns) from the GEMM kernels on `device`,
+ * the hardware analogue of the reference's Trace / TraceEvent
+ * (simengine.py:56-73, export_chrome_trace :372-389).  Record = 4 x u64:
+ *   [0] kind << 56 | rank << 48 | cta << 32 | tile   (kind 1 wait_chunks, 2 gemm_tile, 3 epilogue)
+ *   [1] t_start  [2] t_end  [3] payload (wait: first_chunk << 32 | num_slots;
+ *   tiles: pid_m << 32 | pid_n).  tf_trace_read copies and clears the buffer. */
+int tf_trace_enable(int device, int64_t capacity);
+int tf_trace_disable(int device);
+int tf_trace_read(int device, uint64_t* host, int64_t capacity, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

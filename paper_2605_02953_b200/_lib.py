@@ -86,6 +86,9 @@ _SIGS = {
     "tf_gemm_rs": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_ag_kv_scores": (ci, [vp, ci, C.POINTER(AttnArgs), ci, vp, vp]),
     "tf_gemm_ar": (ci, [vp, ci, C.POINTER(GemmArgs), ci, ci, vp, vp]),
+    "tf_trace_enable": (ci, [ci, i64]),
+    "tf_trace_disable": (ci, [ci]),
+    "tf_trace_read": (ci, [ci, vp, i64, C.POINTER(i64)]),
     "tf_moe_topk": (ci, [vp, i64, ci, ci, vp, vp, vp]),
     "tf_moe_count_scratch_bytes": (i64, [i64, ci]),
     "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp, vp]),

@@ -66,6 +66,10 @@ struct KParams {
   // AllGather on the B (N-side) operand instead of A, and an N-tile permutation
   int wait_on_b;
   const int32_t* tile_map_n;
+  // optional device event trace (tf_trace_enable): [count, pad, pad, pad][cap][4]
+  unsigned long long* trace;
+  int trace_cap;
+  int trace_rank;
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -129,6 +133,24 @@ __device__ __forceinline__ void decode_work(const KParams& p, int work, int& ste
     kb1 = (j + 1) * p.num_kb / p.split_s;
     slot = u;
   }
+}
+
+// Device trace record (4 x u64): kind|rank|cta|tile, t_start, t_end, payload.
+// Kinds: 1 wait_chunks (payload = first_chunk << 32 | num_slots), 2 gemm_tile
+// (payload = pid_m << 32 | pid_n), 3 epilogue (same payload).  %globaltimer ns.
+__device__ __forceinline__ void trace_rec(const KParams& p, unsigned kind, int tile,
+                                          unsigned long long t0, unsigned long long t1,
+                                          unsigned long long payload) {
+  if (!p.trace) return;
+  const unsigned long long i = atomicAdd(p.trace, 1ull);
+  if (i >= static_cast<unsigned long long>(p.trace_cap)) return;
+  unsigned long long* e = p.trace + 4 + i * 4;
+  e[0] = (static_cast<unsigned long long>(kind) << 56) |
+         (static_cast<unsigned long long>(p.trace_rank & 0xFF) << 48) |
+         (static_cast<unsigned long long>(blockIdx.x & 0xFFFF) << 32) | static_cast<unsigned>(tile);
+  e[1] = t0;
+  e[2] = t1;
+  e[3] = payload;
 }
 
 template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
@@ -214,13 +236,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int r1 = min(m0 + span, lim) - 1;
             const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
             const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
+            const unsigned long long tw0 = p.trace ? globaltimer_ns() : 0;
+            bool this_wait = false;
             for (int c = c_beg; c <= c_end; ++c) {
               if (ready_mask & (1u << c)) continue;
               wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
                            0x1000000ull | static_cast<unsigned long long>(c));
               ready_mask |= 1u << c;
               waited = true;
+              this_wait = true;
             }
+            // wait(arrival, rank_beg, num_slots) as in the reference trace
+            if (this_wait)
+              trace_rec(p, 1, pid_m * p.num_pid_n + pid_n, tw0, globaltimer_ns(),
+                        (static_cast<unsigned long long>(c_beg) << 32) |
+                            static_cast<unsigned>(c_end - c_beg + 1));
           }
           // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
           if (waited) fence_proxy_async_global();
@@ -285,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!lagged) mbar_wait(&tempty_bar[1], tph ^ 1);
         tc_fence_after();
         const int s0 = stage;
+        const unsigned long long tm0 = p.trace ? globaltimer_ns() : 0;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -321,6 +352,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               release(&empty_bar[st]);
             }
           release(&tfull_bar[1]);
+          if (p.trace) {
+            int pm, pn;
+            tile_coords(p, step, pm, pn);
+            trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
+                      (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
+          }
         }
         __syncwarp();
       }
@@ -337,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * S::kAccCols;
+        const unsigned long long tm0 = p.trace ? globaltimer_ns() : 0;
         for (int kb = 0; kb < kb1 - kb0; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -365,6 +403,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {  // accumulator ready for the epilogues
           if constexpr (CG == 2) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
           else umma_commit(&tfull_bar[acc]);
+          if (p.trace) {
+            int pm, pn;
+            tile_coords(p, step, pm, pn);
+            trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
+                      (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
+          }
         }
         __syncwarp();
       }
@@ -378,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMA-store staging: this warp's two 32x128 B buffers (128-byte swizzled)
     uint8_t* epi_buf = smem_epi + (warp - kEpiWarp0) * 2 * S::kEpiBuf;
     int epi_slot = 0;
+    unsigned long long epi_t0 = 0;
     constexpr int kColsPerStore = OUT_F32 ? 32 : 64;  // 128 B of one row
     int local = 0;
     for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
@@ -387,6 +432,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(p, step, pid_m, pid_n);
       const int acc = local % ACC;
       const uint32_t acc_phase = (local / ACC) & 1;
+      if (p.trace && warp == kEpiWarp0 && lane == 0) {
+        // one event per work item: from the epilogue picking it up to its drain (below)
+        epi_t0 = globaltimer_ns();
+      }
       // MH == 2: one barrier pair per half (tfull[h] / tempty[h]); else per accumulator
       auto wait_full = [&](int h) {
         if constexpr (MH == 2) mbar_wait(&tfull_bar[h], local & 1);
@@ -396,6 +445,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto arrive_empty = [&](int h) {
         tc_fence_before();
         __syncwarp();
+        if (p.trace && warp == kEpiWarp0 && lane == 0 && (MH == 1 || h == MH - 1))
+          trace_rec(p, 3, pid_m * p.num_pid_n + pid_n, epi_t0, globaltimer_ns(),
+                    (static_cast<unsigned long long>(pid_m) << 32) | static_cast<unsigned>(pid_n));
         const int b = MH == 2 ? h : acc;
         if (lane == 0) {
           if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + b * 8);
@@ -734,6 +786,13 @@ float* tail_workspace(cudaStream_t s, size_t bytes) {
   return static_cast<float*>(e.first);
 }
 
+struct TraceBuf {
+  unsigned long long* buf = nullptr;
+  int64_t cap = 0;
+};
+std::mutex g_trace_mu;
+std::map<int, TraceBuf> g_trace;
+
 }  // namespace
 
 int num_sms_of_current_device() {
@@ -796,6 +855,19 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.dbg_skip_store = getenv("TF_DEBUG_SKIP_STORE") ? 1 : 0;
   kp.wait_on_b = g.wait_on_b ? 1 : 0;
   kp.tile_map_n = g.tile_map_n;
+  kp.trace = nullptr;
+  kp.trace_cap = 0;
+  kp.trace_rank = g.trace_rank;
+  {
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = g_trace.find(dev);
+    if (it != g_trace.end() && it->second.buf) {
+      kp.trace = it->second.buf;
+      kp.trace_cap = static_cast<int>(it->second.cap);
+    }
+  }
   if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
 
   const int cg = tile_m == 128 ? 1 : 2;
@@ -863,3 +935,62 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
 }
 
 }  // namespace tf
+
+// ---------------------------------------------------------------- trace C ABI
+using tf::fail;
+extern "C" {
+
+int tf_trace_enable(int device, int64_t capacity) {
+  if (capacity < 1 || capacity > (1 << 26)) return fail(TF_ERR_INVALID, "trace capacity out of range");
+  std::lock_guard<std::mutex> lock(tf::g_trace_mu);
+  auto& t = tf::g_trace[device];
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (t.buf) cudaFree(t.buf);
+  t.buf = nullptr;
+  const size_t bytes = (4 + static_cast<size_t>(capacity) * 4) * sizeof(unsigned long long);
+  cudaError_t e = cudaMalloc(&t.buf, bytes);
+  if (e == cudaSuccess) e = cudaMemset(t.buf, 0, bytes);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(TF_ERR_CUDA, std::string("trace buffer: ") + cudaGetErrorString(e));
+  t.cap = capacity;
+  return TF_OK;
+}
+
+int tf_trace_disable(int device) {
+  std::lock_guard<std::mutex> lock(tf::g_trace_mu);
+  auto it = tf::g_trace.find(device);
+  if (it != tf::g_trace.end() && it->second.buf) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    cudaFree(it->second.buf);
+    cudaSetDevice(prev);
+  }
+  tf::g_trace.erase(device);
+  return TF_OK;
+}
+
+int tf_trace_read(int device, uint64_t* host, int64_t capacity, int64_t* count) {
+  std::lock_guard<std::mutex> lock(tf::g_trace_mu);
+  auto it = tf::g_trace.find(device);
+  if (it == tf::g_trace.end() || !it->second.buf) return fail(TF_ERR_INVALID, "tracing is not enabled");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  unsigned long long n = 0;
+  cudaError_t e = cudaMemcpy(&n, it->second.buf, sizeof(n), cudaMemcpyDeviceToHost);
+  if (n > static_cast<unsigned long long>(it->second.cap)) n = it->second.cap;
+  if (n > static_cast<unsigned long long>(capacity)) n = capacity;
+  if (e == cudaSuccess && n)
+    e = cudaMemcpy(host, it->second.buf + 4, n * 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(it->second.buf, 0, sizeof(unsigned long long));
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(TF_ERR_CUDA, std::string("trace read: ") + cudaGetErrorString(e));
+  *count = static_cast<int64_t>(n);
+  return TF_OK;
+}
+
+}  // extern "C"

@@ -55,6 +55,7 @@ struct GemmLaunch {
   bool no_tail_split = false;        // disable the split-K tail (e.g. inside fused protocols)
   bool wait_on_b = false;            // chunk flags guard B rows (gathered N-side operand)
   const int32_t* tile_map_n = nullptr; // device [num_pid_n] permutation or nullptr
+  int trace_rank = 0;                // rank tag for device trace events
 };
 
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);

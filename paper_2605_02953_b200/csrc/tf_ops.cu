@@ -386,6 +386,7 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     g.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
     g.epoch = e;
     g.rows_per_chunk = mpr;
+    g.trace_rank = rank;
     g.err = t->err_word(rank);
     g.timeout_ns = t->timeout_ns;
     rc = tf::launch_gemm(g, s);
@@ -483,6 +484,7 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     if (rc) return rc;
     tf::GemmLaunch g = tf::base_launch(args);
     g.num_sms = tf::gemm_grid(args);
+    g.trace_rank = rank;
     g.epilogue = 1;
     g.rank = rank;
     g.world = w;
@@ -727,6 +729,7 @@ int tf_ag_kv_scores(tf_team* t, int rank, const tf_attn_args* a, int phase, void
       g.rows_per_chunk = sl;
       g.wait_on_b = true;
       g.no_tail_split = true;
+      g.trace_rank = rank;
       g.err = t->err_word(rank);
       g.timeout_ns = t->timeout_ns;
       rc = tf::launch_gemm(g, s);
