@@ -1,0 +1,119 @@
+"""Parity at BASELINE.json's full sizes through size-independent properties.
+
+Config 2 (Llama-3-70B MLP, tokens 8192, hidden 8192, ffn 28672):
+  * checksum of checksums: 1^T C = (1^T A) B^T for AG-GEMM, and the row blocks of
+    GEMM-RS summed over ranks reproduce the full product's column sums;
+  * sampled entries equal fp32 dot products of the same bf16 inputs.
+Config 4 (DeepSeek-V3-like EP=8, 4096 tok/rank, top-8 of 256, hidden 7168):
+  * every routed (token, slot) is delivered exactly once: counts, receive rows
+    and an fp64 checksum of all received rows are conserved;
+  * combine with identity experts returns each token (weights sum to 1).
+Several ranks are emulated on one GPU.  Tolerances: bf16 outputs use the
+north-star rel 2e-2 (max-norm); checksums are compared in fp64 at 1e-2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+TOKENS, HIDDEN, FFN = 8192, 8192, 28672
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def _rel(got, want):
+    got, want = got.double(), want.double()
+    return float((got - want).abs().max() / want.abs().max().clamp_min(1e-30))
+
+
+def _ctx(world, **kw):
+    from paper_2605_02953_b200 import WorkloadContext, build_topology
+    args = dict(block_m=512, block_n=256, group_m=8, num_gemm_sms=0, num_comm_sms=0,
+                devices=[0] * world)
+    args.update(kw)
+    return WorkloadContext(topology=build_topology(world, 1), **args)
+
+
+def test_config2_ag_gemm_full_tp1_checksums():
+    from paper_2605_02953_b200 import kernels as K
+    from paper_2605_02953_b200.shmem import Team
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(TOKENS, HIDDEN, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(FFN, HIDDEN, device="cuda", generator=g) * HIDDEN ** -0.5).to(torch.bfloat16)
+    team = Team(1, [0], heap_bytes=1 << 20, signal_slots=64)
+    h = K.AllGatherGemm(team, TOKENS, HIDDEN, FFN)(x, w)
+    torch.cuda.synchronize()
+    colsum = h.double().sum(0)
+    want = x.double().sum(0) @ w.double().T
+    assert _rel(colsum, want) <= 1e-2
+    rows = torch.randint(0, TOKENS, (64,), device="cuda", generator=g)
+    cols = torch.randint(0, FFN, (64,), device="cuda", generator=g)
+    exact = (x[rows].float() * w[cols].float()).sum(1)
+    assert _rel(h[rows, cols].float(), exact) <= 2e-2
+
+
+def test_config2_tp8_ag_then_rs_emulated_checksums():
+    """TP=8 MLP through the fused drop-ins with the 8 ranks emulated on one GPU."""
+    from paper_2605_02953_b200 import kernels as K
+    tp = 8
+    g = torch.Generator(device="cuda").manual_seed(2)
+    f = FFN // tp
+    xs = [torch.randn(TOKENS // tp, HIDDEN, device="cuda", generator=g).to(torch.bfloat16) for _ in range(tp)]
+    w1 = [(torch.randn(f, HIDDEN, device="cuda", generator=g) * HIDDEN ** -0.5).to(torch.bfloat16)
+          for _ in range(tp)]
+    w2 = [(torch.randn(HIDDEN, f, device="cuda", generator=g) * FFN ** -0.5).to(torch.bfloat16)
+          for _ in range(tp)]
+    hs = K.ag_gemm(xs, w1, _ctx(tp)).outputs
+    x_all = torch.cat(xs)
+    for r in range(tp):  # each rank's h = X_all . W1_r^T
+        want = x_all.double().sum(0) @ w1[r].double().T
+        assert _rel(hs[r].double().sum(0), want) <= 1e-2
+    ys = K.gemm_rs(hs, w2, _ctx(tp, fuse_scatter=True, reduce_order="ascending")).outputs
+    y = torch.cat(ys)  # [TOKENS, HIDDEN] = sum_r h_r . W2_r^T
+    want = sum(hs[r].double().sum(0) @ w2[r].double().T for r in range(tp))
+    assert _rel(y.double().sum(0), want) <= 1e-2
+    rows = torch.randint(0, TOKENS, (32,), device="cuda", generator=g)
+    cols = torch.randint(0, HIDDEN, (32,), device="cuda", generator=g)
+    exact = sum((hs[r][rows].float() * w2[r][cols].float()).sum(1) for r in range(tp))
+    assert _rel(y[rows, cols].float(), exact) <= 2e-2
+
+
+def test_config4_moe_ep8_conservation():
+    from paper_2605_02953_b200 import moe as M
+    from paper_2605_02953_b200.shmem import Team
+    world, e, k, t, h = 8, 256, 8, 4096, 7168
+    g = torch.Generator(device="cuda").manual_seed(4)
+    max_recv = 2 * t * k  # per rank; uniform routing needs ~t*k
+    team = Team(world, [0] * world, heap_bytes=2 * max_recv * h * 2 + (64 << 20), signal_slots=1024)
+    ep = M.ExpertParallelMoE(team, e, h, k, max_tokens=t, max_recv=max_recv)
+    xs = [torch.randn(t, h, device="cuda", generator=g).to(torch.bfloat16) for _ in range(world)]
+    routed = [M.moe_route(torch.randn(t, e, device="cuda", generator=g), k) for _ in range(world)]
+    idx = [r[0] for r in routed]
+    w = [r[1] for r in routed]
+    recv = ep.dispatch(xs, idx)
+    torch.cuda.synchronize()
+    team.check()
+    counts = ep.counts(0).long()
+    assert torch.equal(counts.sum(1).cpu(), torch.full((world,), t * k))
+    for r in range(world):
+        assert torch.equal(ep.counts(r), ep.counts(0))
+    rows = [ep.recv_rows(r) for r in range(world)]
+    assert sum(rows) == world * t * k
+    epr = e // world
+    for r in range(world):
+        assert rows[r] == int(counts[:, r * epr:(r + 1) * epr].sum())
+    sent = sum(float(xs[s].double().sum()) * k for s in range(world))
+    got = sum(float(recv[r][:rows[r]].double().sum()) for r in range(world))
+    assert abs(got - sent) <= 1e-6 * max(1.0, abs(sent)) + 1e-3
+    for r in range(world):  # identity experts
+        ep.expert_out(r)[:rows[r]] = recv[r][:rows[r]]
+    outs = ep.combine(idx, w)
+    torch.cuda.synchronize()
+    team.check()
+    for r in range(world):
+        assert _rel(outs[r].float(), xs[r].float()) <= 2e-2
