@@ -208,6 +208,22 @@ typedef struct tf_attn_args {
 int tf_ag_kv_scores(tf_team* t, int rank, const tf_attn_args* a, int phase, void* stream,
                     void* comm_stream);
 
+/* AG-KV fused with the flash-attention forward (config 3):
+ * O[q, h, :] = softmax(q[q, h, :] . K_all[:, g(h), :]^T * scale) . V_all[:, g(h), :]
+ * for this rank's queries against every rank's keys/values, never
+ * materialising the scores.  q/out: [s_local, hq, 128] bf16; k/v: [s_local, hkv,
+ * 128] bf16 shards; s_local % 128 == 0.  Same phases as tf_ag_gemm. */
+typedef struct tf_attn_fwd_args {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* out;
+  int64_t s_local, hq, hkv, d;
+  float scale;
+} tf_attn_fwd_args;
+int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* a, int phase, void* stream,
+                       void* comm_stream);
+
 /* ------------------------------------------------------------------ MoE (expert parallel)
  * Not in the reference as an all-to-all; what the reference pins
  * is the layout: the [world, E] routing-count matrix (ag_moe.py:28-33) and the

@@ -53,6 +53,13 @@ class AttnArgs(C.Structure):
     ]
 
 
+class AttnFwdArgs(C.Structure):
+    _fields_ = [
+        ("q", vp), ("k", vp), ("v", vp), ("out", vp), ("s_local", i64), ("hq", i64),
+        ("hkv", i64), ("d", i64), ("scale", C.c_float),
+    ]
+
+
 _SIGS = {
     "tf_last_error": (C.c_char_p, []),
     "tf_version": (C.c_char_p, []),
@@ -86,6 +93,7 @@ _SIGS = {
     "tf_gemm_rs": (ci, [vp, ci, C.POINTER(GemmArgs), ci, vp, vp]),
     "tf_ag_kv_scores": (ci, [vp, ci, C.POINTER(AttnArgs), ci, vp, vp]),
     "tf_gemm_ar": (ci, [vp, ci, C.POINTER(GemmArgs), ci, ci, vp, vp]),
+    "tf_ag_kv_attention": (ci, [vp, ci, C.POINTER(AttnFwdArgs), ci, vp, vp]),
     "tf_trace_enable": (ci, [ci, i64]),
     "tf_trace_disable": (ci, [ci]),
     "tf_trace_read": (ci, [ci, vp, i64, C.POINTER(i64)]),

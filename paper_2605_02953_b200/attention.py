@@ -123,3 +123,81 @@ class AllGatherKVScores:
         return out
 
     __call__ = forward
+
+
+# ----------------------------------------------------------------- fused flash attention
+def _fwd_args(q, k, v, out, s_local, hq, hkv, d, scale):
+    a = _lib.AttnFwdArgs()
+    a.q, a.k, a.v, a.out = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+    a.s_local, a.hq, a.hkv, a.d = int(s_local), int(hq), int(hkv), int(d)
+    a.scale = float(scale)
+    return a
+
+
+def ag_kv_attention(q_shards, k_shards, v_shards, ctx: WorkloadContext, scale: float | None = None,
+                    n_kv_heads: int | None = None) -> WorkloadRun:
+    """Per rank r: O_r[:, h] = softmax(Q_r[:, h] . K_all[:, g(h)]^T * scale) . V_all[:, g(h)].
+
+    Shards are torch bf16 CUDA tensors: q [S_local, Hq, 128], k/v [S_local, Hkv, 128]
+    (S_local % 128 == 0).  The K/V AllGather is fused: each CTA waits per key chunk."""
+    topo = ctx.topology
+    world = topo.world_size
+    if not (len(q_shards) == len(k_shards) == len(v_shards) == world):
+        raise ValueError(f"need {world} shards per operand")
+    K.check_dtype(*q_shards, *k_shards, *v_shards)
+    if not K._is_torch(q_shards[0]):
+        raise ValueError("ag_kv_attention takes torch bfloat16 CUDA tensors")
+    sl, hq, d = q_shards[0].shape
+    hkv = k_shards[0].shape[1] if n_kv_heads is None else n_kv_heads
+    for q, k, v in zip(q_shards, k_shards, v_shards):
+        if tuple(q.shape) != (sl, hq, d) or tuple(k.shape) != (sl, hkv, d) or tuple(v.shape) != (sl, hkv, d):
+            raise ValueError("ragged q/k/v shards")
+    if hq % hkv:
+        raise ValueError("query heads must be a multiple of kv heads")
+    if d != 128 or sl % 128:
+        raise ValueError("the fused kernel needs head dim 128 and S_local % 128 == 0")
+    scale = float(scale if scale is not None else d ** -0.5)
+    devices = [t.device.index for t in q_shards]
+    st = sl * world
+    team = Team(world, devices, 2 * 2 * st * hkv * d * 2 + (1 << 20), 4 * world + 64)
+    heap = SymmetricHeap(topo, team=team)
+    outs = [torch.empty_like(q) for q in q_shards]
+    args = {r: _fwd_args(q_shards[r].contiguous(), k_shards[r].contiguous(), v_shards[r].contiguous(),
+                         outs[r], sl, hq, hkv, d, scale) for r in range(world)}
+    keep = [(q_shards[r].contiguous(), k_shards[r].contiguous(), v_shards[r].contiguous()) for r in range(world)]
+    for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
+        for r in range(world):
+            with torch.cuda.device(devices[r]):
+                s, cs = K._streams(team, r)
+                _lib.call("tf_ag_kv_attention", team.handle, r, C.byref(args[r]), phase, K._ptr(s), K._ptr(cs))
+    for dd in sorted(set(devices)):
+        torch.cuda.synchronize(dd)
+    team.check()
+    del keep
+    return WorkloadRun(outs, None, heap, {})
+
+
+class AllGatherKVAttention:
+    """Reusable fused AG-KV flash-attention forward (one rank per process, or a
+    single-rank local team)."""
+
+    def __init__(self, team: Team, s_local: int, hq: int, hkv: int, d: int = 128,
+                 scale: float | None = None):
+        if d != 128 or s_local % 128 or hq % hkv:
+            raise ValueError("need d == 128, S_local % 128 == 0 and hq % hkv == 0")
+        self.team, self.sl, self.hq, self.hkv, self.d = team, s_local, hq, hkv, d
+        self.scale = float(scale if scale is not None else d ** -0.5)
+
+    def forward(self, q, k, v, out=None):
+        t = self.team
+        if t.rank is None and t.world != 1:
+            raise ValueError("use ag_kv_attention() for multi-rank local teams")
+        r = t.rank or 0
+        out = torch.empty_like(q) if out is None else out
+        a = _fwd_args(q, k, v, out, self.sl, self.hq, self.hkv, self.d, self.scale)
+        s, cs = torch.cuda.current_stream(), K.side_stream(q.device.index)
+        _lib.call("tf_ag_kv_attention", t.handle, r, C.byref(a), _lib.PHASE_ALL, s.cuda_stream,
+                  cs.cuda_stream)
+        return out
+
+    __call__ = forward

@@ -64,3 +64,44 @@ def test_ag_kv_scores_validation():
         ag_kv_scores(q, k, _ctx(2))  # 3 query heads over 2 kv heads
     with pytest.raises(ValueError):
         ag_kv_scores(q[:1], k, _ctx(2))
+
+
+# -- fused AG-KV flash-attention forward ------------------------------
+
+
+@pytest.mark.parametrize("world,sl,hq,hkv", [(1, 128, 1, 1), (1, 256, 2, 1), (2, 128, 4, 2),
+                                             (4, 256, 8, 1), (8, 128, 8, 8)])
+def test_ag_kv_attention_vs_oracle(world, sl, hq, hkv):
+    from paper_2605_02953_b200.attention import ag_kv_attention
+    rng = np.random.default_rng(world * 7 + sl + hq)
+    d = 128
+    mk = lambda *s: torch.from_numpy(rng.standard_normal(s).astype(np.float32)).to(torch.bfloat16).cuda()
+    q = [mk(sl, hq, d) for _ in range(world)]
+    k = [mk(sl, hkv, d) for _ in range(world)]
+    v = [mk(sl, hkv, d) for _ in range(world)]
+    run = ag_kv_attention(q, k, v, _ctx(world))
+    want = OA.ref_ag_kv_attention([x.float().cpu().numpy() for x in q], [x.float().cpu().numpy() for x in k],
+                                  [x.float().cpu().numpy() for x in v], hkv, d ** -0.5)
+    for r in range(world):
+        got = run.outputs[r].float().cpu().numpy()
+        assert np.isfinite(got).all()
+        assert OC.compare(got, want[r]) <= 2e-2, r
+
+
+def test_ag_kv_attention_peaked_scores_rescaling():
+    """Large, growing logits force the online-softmax rescale path every tile."""
+    from paper_2605_02953_b200.attention import ag_kv_attention
+    rng = np.random.default_rng(11)
+    world, sl, hq, hkv, d = 2, 256, 2, 1, 128
+    q = [torch.from_numpy(rng.standard_normal((sl, hq, d)).astype(np.float32) * 3).to(torch.bfloat16).cuda()
+         for _ in range(world)]
+    ramp = np.linspace(0.2, 4.0, sl * world).astype(np.float32)
+    kk = rng.standard_normal((sl * world, hkv, d)).astype(np.float32) * ramp[:, None, None]
+    k = [torch.from_numpy(kk[r * sl:(r + 1) * sl]).to(torch.bfloat16).cuda() for r in range(world)]
+    v = [torch.from_numpy(rng.standard_normal((sl, hkv, d)).astype(np.float32)).to(torch.bfloat16).cuda()
+         for _ in range(world)]
+    run = ag_kv_attention(q, k, v, _ctx(world))
+    want = OA.ref_ag_kv_attention([x.float().cpu().numpy() for x in q], [x.float().cpu().numpy() for x in k],
+                                  [x.float().cpu().numpy() for x in v], hkv, d ** -0.5)
+    for r in range(world):
+        assert OC.compare(run.outputs[r].float().cpu().numpy(), want[r]) <= 2e-2
