@@ -252,34 +252,33 @@ ATT_S, ATT_SP, ATT_HQ, ATT_HKV, ATT_D = 32768, 8, 64, 8, 128
 
 
 def bench_attention(dev, steps, peaks):
-    """Config 3 per-rank work: Q [4096, 64, 128] . K_all [32768, 8, 128]^T with the
-    K AllGather fused (SP=8).  On one GPU the 8 SP ranks are emulated by a local
-    team whose PEs share the device; their fused calls run back to back and the
-    per-rank time is the total / 8.  Scores are bf16 and written to one reused
-    buffer (materialising all ranks' 17.2 GB each is not the point)."""
+    """Config 3 per SP rank: fused AG-KV flash-attention forward, Q [4096, 64, 128]
+    against K/V gathered to [32768, 8, 128] (GQA 8:1, non-causal, bf16).  On one
+    GPU the 8 SP ranks are emulated by a local team whose PEs share the device;
+    their fused calls run back to back and the per-rank time is total / 8."""
     import ctypes as C
 
     import torch
 
     from paper_2605_02953_b200 import _lib
-    from paper_2605_02953_b200 import kernels as K
-    from paper_2605_02953_b200.attention import _attn_args
+    from paper_2605_02953_b200.attention import _fwd_args
     from paper_2605_02953_b200.shmem import Team
     sl = ATT_S // ATT_SP
     g = torch.Generator(device="cpu").manual_seed(99)
-    team = Team(ATT_SP, [dev] * ATT_SP, 2 * ATT_S * ATT_HKV * ATT_D * 2 + (16 << 20), 256)
-    qs = [torch.randn(sl, ATT_HQ, ATT_D, generator=g).to(torch.bfloat16).to(f"cuda:{dev}") for _ in range(ATT_SP)]
-    ks = [torch.randn(sl, ATT_HKV, ATT_D, generator=g).to(torch.bfloat16).to(f"cuda:{dev}") for _ in range(ATT_SP)]
-    out = torch.empty(ATT_HQ, sl, ATT_S, dtype=torch.bfloat16, device=f"cuda:{dev}")
-    maps = [K.tile_map_tensor(ATT_S, r, ATT_SP, 1, "ag_gemm", f"cuda:{dev}", 256) for r in range(ATT_SP)]
-    args = [_attn_args(qs[r], ks[r], out, sl, ATT_HQ, ATT_HKV, ATT_D, torch.bfloat16, 256, 256, 8, 0,
-                       maps[r]) for r in range(ATT_SP)]
+    team = Team(ATT_SP, [dev] * ATT_SP, 4 * ATT_S * ATT_HKV * ATT_D * 2 + (16 << 20), 256)
+    mk = lambda *s: torch.randn(*s, generator=g).to(torch.bfloat16).to(f"cuda:{dev}")
+    qs = [mk(sl, ATT_HQ, ATT_D) for _ in range(ATT_SP)]
+    ks = [mk(sl, ATT_HKV, ATT_D) for _ in range(ATT_SP)]
+    vs = [mk(sl, ATT_HKV, ATT_D) for _ in range(ATT_SP)]
+    outs = [torch.empty_like(q) for q in qs]
+    args = [_fwd_args(qs[r], ks[r], vs[r], outs[r], sl, ATT_HQ, ATT_HKV, ATT_D, ATT_D ** -0.5)
+            for r in range(ATT_SP)]
     stream = torch.cuda.current_stream(dev)
 
     def step():
         for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
             for r in range(ATT_SP):
-                _lib.call("tf_ag_kv_scores", team.handle, r, C.byref(args[r]), phase,
+                _lib.call("tf_ag_kv_attention", team.handle, r, C.byref(args[r]), phase,
                           stream.cuda_stream, None)
 
     step()
@@ -292,20 +291,17 @@ def bench_attention(dev, steps, peaks):
     torch.cuda.synchronize()
     team.check()
     per_rank_ms = e0.elapsed_time(e1) / steps / ATT_SP
-    flops = 2.0 * sl * ATT_S * ATT_D * ATT_HQ
-    score_bytes = sl * ATT_S * ATT_HQ * 2
+    flops = 4.0 * sl * ATT_S * ATT_D * ATT_HQ  # QK^T + PV
     t_tc = flops / (peaks.get("bf16_tflops", 1622.7) * 1e12)
-    t_hbm = score_bytes / (peaks.get("hbm_gbs", 6550.1) * 1e9)
-    t_roof = max(t_tc, t_hbm)
     team.close()
-    return {"workload": "config 3 per SP rank: Q[4096,64,128] . AG(K)[32768,8,128]^T, GQA 8:1, bf16 "
-                        "scores; SP=8 emulated on one GPU (per-rank = total / 8)",
+    return {"workload": "config 3 per SP rank: fused AG-KV flash-attention forward, Q[4096,64,128] vs "
+                        "K/V[32768,8,128] (GQA 8:1, non-causal, bf16); SP=8 emulated on one GPU "
+                        "(per-rank = total / 8)",
             "ms_per_rank": round(per_rank_ms, 4),
             "tflops_per_rank": round(flops / (per_rank_ms * 1e-3) / 1e12, 2),
-            "roofline": {"bound": "hbm" if t_hbm > t_tc else "tensor",
-                         "t_roof_ms": round(t_roof * 1e3, 4),
-                         "frac": round(t_roof / (per_rank_ms * 1e-3), 4),
-                         "note": "materialised scores (17.2 GB/rank) make QK^T write-bound; flash fusion is next"}}
+            "roofline": {"bound": "tensor", "t_roof_ms": round(t_tc * 1e3, 4),
+                         "frac": round(t_tc / (per_rank_ms * 1e-3), 4),
+                         "peak": peaks.get("bf16_tflops", 1622.7), "unit": "TFLOP/s"}}
 
 
 # ------------------------------------------------------------------ GPU arm
