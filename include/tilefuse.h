@@ -275,6 +275,26 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
  * out[t] = sum_j w[t,j] * y[row(t,j)] in fp32 (slot order), bf16 out. */
 int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream);
 
+/* ------------------------------------------------------------------ task-level megakernel
+ * Executor for the reference's task graphs (ovs/megakernel/):
+ * queues = int32 [slots][num_sms][30] task records (encoding.py:20-166),
+ * counts = int32 [num_sms], deps = int32 [n][3] (producer, first tile, end),
+ * layer_cfg = int32 [layers][4] (op 0 linear / 1 add / 2 allreduce, block_m,
+ * block_n, block_rows), all device pointers.  Scoreboard flags live in every PE's
+ * signal space at flag_base + task * max_tiles + tile and are set to `epoch`.
+ * All ranks of the (local, single-device) team run co-resident in one launch:
+ * world * num_sms CTAs.  Tensors: fp32 [rows, cols] at each io slot's offset. */
+typedef struct tf_mega_args {
+  const int32_t* queues;
+  const int32_t* counts;
+  const int32_t* deps;
+  const int32_t* task_ops; /* reserved */
+  const int32_t* layer_cfg;
+  int32_t num_sms, slots, max_tiles, num_layers;
+  uint64_t flag_base, epoch, timeout_ns;
+} tf_mega_args;
+int tf_megakernel_run(tf_team* t, const tf_mega_args* a, void* stream);
+
 /* ------------------------------------------------------------------ device tracing
  * Per-tile device events (%globaltimer ns) from the GEMM kernels on `device`,
  * the hardware analogue of the reference's Trace / TraceEvent

@@ -357,6 +357,13 @@ int tf_team_check(tf_team* t) {
       unsigned long long z = 0;
       cudaMemcpy(t->err_word(p), &z, sizeof(z), cudaMemcpyHostToDevice);
       const unsigned kind = static_cast<unsigned>(w >> 24);
+      if (kind == 9)
+        return fail(TF_ERR_PROTOCOL, "double release of scoreboard slot " + std::to_string(w & 0xFFFFFF) +
+                                         " on PE " + std::to_string(p));
+      if (kind == 8)
+        return fail(TF_ERR_TIMEOUT, "device spin timed out on PE " + std::to_string(p) +
+                                        ": scoreboard task slot " + std::to_string(w & 0xFFFFFF) +
+                                        " (task = slot / max_tiles_per_op)");
       const char* what = kind == 1 ? "AllGather chunk flag" : kind == 2 ? "signal wait"
                        : kind == 3 ? "barrier_all" : kind == 4 ? "reduce-scatter tile counter"
                        : kind == 5 ? "moe dispatch flag" : "device wait";

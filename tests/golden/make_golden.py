@@ -205,8 +205,51 @@ def make_config1(kern, topo_mod):
          "sha256_per_rank": digests}, indent=1) + "\n")
 
 
+def make_megakernel(topo_mod):
+    """Reference task graphs: queue bytes, dependency tables and DAG text."""
+    from overlapsim.megakernel import (MegaProgram, dump_task_graph, encode_work_queues,
+                                       queues_to_bytes, deps_to_bytes)
+    out, texts = {}, {}
+    progs = {}
+    # the MLP of tests/test_megakernel.py:48-61 and the allreduce graph of :374-384
+    topo = topo_mod.build_topology(2, 1, num_sms=8)
+    prog = MegaProgram(topo)
+    x = prog.tensor("x", (32, 16), np.int64)
+    w1 = prog.tensor("w1", (24, 16), np.int64)
+    h1 = prog.tensor("h1", (32, 24), np.int64)
+    bias = prog.tensor("bias", (32, 24), np.int64)
+    h2 = prog.tensor("h2", (32, 24), np.int64)
+    w2 = prog.tensor("w2", (16, 24), np.int64)
+    y = prog.tensor("y", (32, 16), np.int64)
+    prog.layer("linear", [x, w1], [h1], block_m=16, block_n=16)
+    prog.layer("add", [h1, bias], [h2], block_rows=16)
+    prog.layer("linear", [h2, w2], [y], block_m=16, block_n=16)
+    progs["mlp"] = prog
+    topo = topo_mod.build_topology(4, 1, num_sms=4)
+    prog = MegaProgram(topo)
+    a = prog.tensor("a", (8, 6), np.int64)
+    w = prog.tensor("w", (6, 6), np.int64)
+    pp = prog.tensor("p", (8, 6), np.int64)
+    red = prog.tensor("red", (8, 6), np.int64)
+    prog.layer("linear", [a, w], [pp], block_m=4, block_n=3)
+    prog.layer("allreduce", [pp], [red], block_rows=4)
+    progs["allreduce"] = prog
+    for name, prog in progs.items():
+        built = prog.build()
+        for nsm in (1, 3, 8):
+            q, c = encode_work_queues(built.tasks, nsm)
+            out[f"{name}_q{nsm}"] = np.frombuffer(queues_to_bytes(q), dtype=np.uint8)
+            out[f"{name}_c{nsm}"] = c
+        out[f"{name}_deps"] = np.frombuffer(deps_to_bytes(built.dep_table), dtype=np.uint8)
+        out[f"{name}_meta"] = np.array([built.max_task_id, built.max_tiles_per_op], np.int64)
+        texts[name] = dump_task_graph(built.tasks, built.dep_table)
+    np.savez_compressed(OUT / "megakernel.npz", **out)
+    (OUT / "megakernel_dags.json").write_text(json.dumps(texts, indent=1) + "\n")
+
+
 def main():
     kern, swz, topo_mod = _import_ref()
+    make_megakernel(topo_mod)
     make_render(swz)
     nmaps = make_tile_maps(swz)
     nmoe = make_moe(swz)
