@@ -295,6 +295,30 @@ typedef struct tf_mega_args {
 } tf_mega_args;
 int tf_megakernel_run(tf_team* t, const tf_mega_args* a, void* stream);
 
+/* ------------------------------------------------------------------ fused-layer megakernel (bf16)
+ * Same task records / queues / dependency rows / scoreboard as tf_megakernel_run
+ * (ovs/megakernel/encoding.py:20-166, builders.py:105-162, scoreboard.py:33-56),
+ * for the bf16 transformer-layer ops (BASELINE config 5): layer_cfg = int32
+ * [layers][16] = {op (1 rmsnorm, 2 linear, 3 attention, 4 allreduce_residual),
+ * block_m, block_n, block_rows, epilogue (0 none, 1 rope, 2 silu_mul), tensor map
+ * of A / qkv, tensor map of B, heads_q, heads_kv, seq_len, softmax scale (f32
+ * bits), rms eps (f32 bits), causal, rope columns, output io slot, 0}.
+ * map_specs (HOST) = int64 [num_maps][8] {heap offset, ndims, dims[3] innermost
+ * first, box[3]}: bf16 128-byte-swizzled TMA maps encoded against every launched
+ * rank's heap base.  Local team: rank = -1, every rank co-scheduled on one
+ * device (world * num_sms CTAs).  IPC team: rank = this process's rank (num_sms
+ * CTAs; peers reached through the IPC-mapped heaps). */
+typedef struct tf_layer_args {
+  const int32_t* queues;
+  const int32_t* counts;
+  const int32_t* deps;
+  const int32_t* layer_cfg;
+  const int64_t* map_specs;
+  int32_t num_maps, num_sms, max_tiles, num_layers;
+  uint64_t flag_base, epoch, timeout_ns;
+} tf_layer_args;
+int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args* a, void* stream);
+
 /* ------------------------------------------------------------------ device tracing
  * Per-tile device events (%globaltimer ns) from the GEMM kernels on `device`,
  * the hardware analogue of the reference's Trace / TraceEvent

@@ -95,6 +95,7 @@ _SIGS = {
     "tf_gemm_ar": (ci, [vp, ci, C.POINTER(GemmArgs), ci, ci, vp, vp]),
     "tf_ag_kv_attention": (ci, [vp, ci, C.POINTER(AttnFwdArgs), ci, vp, vp]),
     "tf_megakernel_run": (ci, [vp, vp, vp]),
+    "tf_layer_megakernel_run": (ci, [vp, ci, vp, vp]),
     "tf_trace_enable": (ci, [ci, i64]),
     "tf_trace_disable": (ci, [ci]),
     "tf_trace_read": (ci, [ci, vp, i64, C.POINTER(i64)]),

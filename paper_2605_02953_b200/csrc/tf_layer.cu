@@ -1,0 +1,828 @@
+// Task-level megakernel for a fused transformer layer in bf16 (BASELINE config 5;
+// SURVEY §8(f) #1).  Same wire contract as the reference's executor
+// (ovs/megakernel/encoding.py:20-166, builders.py:105-162, scoreboard.py:33-56,
+// runner.py:120-195): 30-word task records in [slot][sm] queues, dependency rows
+// (producer task, first tile, one-past-last tile), scoreboard slot
+// task * max_tiles + tile, release-stored with the call epoch.
+//
+// One persistent launch, one CTA per SM, 192 threads with fixed roles; every role
+// walks the CTA's queue in order and does its share of each task:
+//
+//   task          warp 0 (TMA)            warp 1 (MMA, one lane)     warps 2-5 (128 thr)
+//   linear        wait deps, A/B boxes    tcgen05 128x256x16 into    TMEM -> epilogue (plain |
+//                 into a 4-stage ring     a double-buffered TMEM     RoPE | SiLU*up) -> bf16,
+//                                         accumulator                release the tile flag
+//   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
+//                 tiles (2 stages)        (V MN-major)               mask), O / l -> bf16
+//   rmsnorm       -                       -                          wait deps, y = x*rstd*g
+//   allreduce_    -                       -                          wait deps on every PE,
+//   residual                                                         y = sum_pe x_pe + res (P2P)
+//
+// The linear ring (4 x 48 KB) and the attention buffers (Q, 2 x K/V, P) alias the
+// same 192 KB of shared memory and TMEM columns [0, 512); when consecutive tensor
+// tasks of a CTA change class, all six warps meet at a named barrier first, by
+// which point every TMA load has been consumed and every MMA has retired.
+// Elementwise tasks only involve warps 2-5, so warps 0-1 keep prefetching the
+// next GEMM tile while they run.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tf_internal.h"
+#include "tf_ptx.cuh"
+#include "tf_team.h"
+
+namespace tf {
+namespace {
+
+constexpr int kLThreads = 192;
+constexpr int kRing = 4;
+constexpr int kHalfBox = 16384;               // 128 rows x 128 B
+constexpr int kAStage = 128 * 64 * 2;         // 16 KB
+constexpr int kBStage = 256 * 64 * 2;         // 32 KB
+constexpr int kStage = kAStage + kBStage;     // 48 KB
+constexpr int kRegion = kRing * kStage;       // 192 KB
+constexpr int kQOff = 0;                      // attention aliases
+constexpr int kKVOff = 2 * kHalfBox;          // 2 stages x (K 32 KB + V 32 KB)
+constexpr int kKVStage = 4 * kHalfBox;
+constexpr int kPOff = kKVOff + 2 * kKVStage;  // 160 KB
+constexpr int kLayerSmem = 1024 + kRegion + 512;
+constexpr int kCfgInts = 16;
+constexpr int kIntPerTask = 30;
+
+enum { OP_RMSNORM = 1, OP_LINEAR = 2, OP_ATTENTION = 3, OP_ALLREDUCE_RES = 4 };
+enum { EPI_NONE = 0, EPI_ROPE = 1, EPI_SILU_MUL = 2 };
+enum { CLS_ELEM = 0, CLS_LINEAR = 1, CLS_ATTN = 2 };
+
+struct LayerParams {
+  const int32_t* queues;
+  const int32_t* counts;
+  const int32_t* deps;
+  const int32_t* cfg;        // [layers][16]
+  const CUtensorMap* maps;   // [ranks in launch][num_maps]
+  int num_maps;
+  int num_sms, max_tiles;
+  int fixed_rank;            // IPC: this process's rank; local team: -1 (rank = cta / num_sms)
+  int world;
+  uint64_t flag_base;
+  unsigned long long epoch;
+  unsigned long long timeout_ns;
+  uint8_t* base[kMaxWorld];
+  uint64_t* sig[kMaxWorld];
+  unsigned long long* err[kMaxWorld];
+};
+
+struct Rec {
+  int task_id, tile, dep0, dep1;
+  int off[4];
+  int d0[4], d1[4];
+};
+
+__device__ __forceinline__ void load_rec(const LayerParams& p, int idx, int sm, Rec& r) {
+  const int32_t* q = p.queues + (static_cast<long long>(idx) * p.num_sms + sm) * kIntPerTask;
+  r.task_id = __ldg(q + 2);
+  r.tile = __ldg(q + 3);
+  r.dep0 = __ldg(q + 4);
+  r.dep1 = __ldg(q + 5);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    r.off[i] = __ldg(q + 6 + 6 * i);
+    r.d0[i] = __ldg(q + 8 + 6 * i);
+    r.d1[i] = __ldg(q + 9 + 6 * i);
+  }
+}
+
+__device__ __forceinline__ int op_class(int op) {
+  return op == OP_LINEAR ? CLS_LINEAR : op == OP_ATTENTION ? CLS_ATTN : CLS_ELEM;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Acquire-wait every dependency flag of the record, spread over `nt` threads
+// (thread t takes flattened entries t, t + nt, ...); npe > 1 waits on every PE's
+// scoreboard (allreduce).  Returns true if this thread waited on anything.
+__device__ __forceinline__ bool wait_deps(const LayerParams& p, const Rec& r, int rank, int npe,
+                                          int t, int nt) {
+  bool any = false;
+  int base = 0;
+  for (int row = r.dep0; row < r.dep1; ++row) {
+    const int prod = __ldg(p.deps + row * 3), lo = __ldg(p.deps + row * 3 + 1),
+              hi = __ldg(p.deps + row * 3 + 2);
+    const int cnt = (hi - lo) * npe;
+    int e = base + ((t - base) % nt + nt) % nt;
+    for (; e < base + cnt; e += nt) {
+      const int i = e - base;
+      const int tile = lo + i / npe;
+      const int pe = npe == 1 ? rank : i % npe;
+      const uint64_t slot = static_cast<uint64_t>(prod) * p.max_tiles + tile;
+      wait_geq_sys(p.sig[pe] + p.flag_base + slot, p.epoch, p.timeout_ns, p.err[rank],
+                   0x8000000ull | slot);
+      any = true;
+    }
+    base += cnt;
+  }
+  return any;
+}
+
+__device__ __forceinline__ void release_flag(const LayerParams& p, int rank, const Rec& r) {
+  uint64_t* f = p.sig[rank] + p.flag_base + static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile;
+  if (ld_acquire_sys(f) >= p.epoch)  // double release (scoreboard.py:50-56)
+    atomicCAS(p.err[rank], 0ull,
+              0x9000000ull | (static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile));
+  fence_sys();
+  st_release_sys(f, p.epoch);
+}
+
+__device__ __forceinline__ void tma_load_3d_l(void* smem_dst, const void* tmap, uint64_t* bar,
+                                              int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// 32 fp32 values -> 32 bf16 at dst (64 B, 16-byte aligned), masked by `ncols` valid
+__device__ __forceinline__ void store_bf16x32(uint16_t* dst, const float (&f)[32], int ncols) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(f[2 * i], f[2 * i + 1]);
+  if (ncols >= 32) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+  } else {
+    uint32_t* d2 = reinterpret_cast<uint32_t*>(dst);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // ncols is a multiple of 8 (checked on the host)
+      if (2 * i < ncols) d2[i] = pk[i];
+    }
+  }
+}
+
+struct AttnGeom {
+  int n_kv, kv0, hq, hkv, g, h, q_row0;
+};
+
+__device__ __forceinline__ AttnGeom attn_geom(const int* cfg, const Rec& r) {
+  AttnGeom a;
+  a.hq = cfg[7];
+  a.hkv = cfg[8];
+  const int seq = cfg[9];
+  const int causal = cfg[12];
+  const int i = r.tile / a.hq;
+  a.h = r.tile % a.hq;
+  a.g = a.h / (a.hq / a.hkv);
+  a.q_row0 = i * 128;
+  const int tiles_per_seq = seq / 128;
+  a.kv0 = (i / tiles_per_seq) * tiles_per_seq;
+  a.n_kv = causal ? i - a.kv0 + 1 : tiles_per_seq;
+  return a;
+}
+
+__global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_constant__ LayerParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRegion);
+  uint64_t* full_bar = bars;            // [4]
+  uint64_t* empty_bar = bars + 4;       // [4]
+  uint64_t* tfull = bars + 8;           // [2]
+  uint64_t* tempty = bars + 10;         // [2]
+  uint64_t* q_full = bars + 12;
+  uint64_t* q_empty = bars + 13;
+  uint64_t* kv_full = bars + 14;        // [2]
+  uint64_t* kv_empty = bars + 16;       // [2]
+  uint64_t* s_full = bars + 18;         // [2]
+  uint64_t* s_empty = bars + 20;        // [2]
+  uint64_t* p_full = bars + 22;
+  uint64_t* pv_done = bars + 23;
+  uint64_t* o_empty = bars + 24;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = p.fixed_rank >= 0 ? p.fixed_rank : static_cast<int>(blockIdx.x) / p.num_sms;
+  const int sm = static_cast<int>(blockIdx.x) % p.num_sms;
+  const CUtensorMap* maps = p.maps + (p.fixed_rank >= 0 ? 0 : rank) * p.num_maps;
+  uint8_t* my_base = p.base[rank];
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    mbar_init(o_empty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tasks = p.counts[sm];
+  int last_cls = -1;
+
+  if (warp == 0) {
+    // =========================================================== TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    int kv_it = 0, att_it = 0;
+    for (int idx = 0; idx < n_tasks; ++idx) {
+      Rec r;
+      load_rec(p, idx, sm, r);
+      const int* cfg = p.cfg + r.task_id * kCfgInts;
+      const int op = __ldg(cfg);
+      const int cls = op_class(op);
+      if (cls == CLS_ELEM) continue;
+      if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+      last_cls = cls;
+      const bool waited = __any_sync(0xffffffffu, wait_deps(p, r, rank, 1, lane, 32));
+      __syncwarp();
+      if (cls == CLS_LINEAR) {
+        const int m = r.d0[0], k = r.d1[0], n = r.d0[1];
+        (void)m;
+        const int ntn = (n + 255) / 256;
+        const int r0 = (r.tile / ntn) * 128, c0 = (r.tile % ntn) * 256;
+        const CUtensorMap* ma = maps + __ldg(cfg + 5);
+        const CUtensorMap* mb = maps + __ldg(cfg + 6);
+        if (lane == 0) {
+          if (waited) fence_proxy_async_global();
+          for (int kb = 0; kb < k / 64; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * kStage;
+            mbar_arrive_expect_tx(&full_bar[stage], kStage);
+            tma_load_2d(sa, ma, &full_bar[stage], kb * 64, r0);
+            tma_load_2d(sa + kAStage, mb, &full_bar[stage], kb * 64, c0);
+            if (++stage == kRing) { stage = 0; phase ^= 1; }
+          }
+        }
+        __syncwarp();
+      } else {
+        const AttnGeom a = attn_geom(cfg, r);
+        const CUtensorMap* mq = maps + __ldg(cfg + 5);
+        if (lane == 0) {
+          if (waited) fence_proxy_async_global();
+          mbar_wait(q_empty, (att_it & 1) ^ 1);
+          mbar_arrive_expect_tx(q_full, 2 * kHalfBox);
+          tma_load_3d_l(smem + kQOff, mq, q_full, 0, a.h, a.q_row0);
+          tma_load_3d_l(smem + kQOff + kHalfBox, mq, q_full, 64, a.h, a.q_row0);
+          for (int j = 0; j < a.n_kv; ++j) {
+            const int gi = kv_it + j, st = gi & 1;
+            mbar_wait(&kv_empty[st], ((gi >> 1) & 1) ^ 1);
+            uint8_t* kb = smem + kKVOff + st * kKVStage;
+            const int row = (a.kv0 + j) * 128;
+            mbar_arrive_expect_tx(&kv_full[st], kKVStage);
+            tma_load_3d_l(kb, mq, &kv_full[st], 0, a.hq + a.g, row);
+            tma_load_3d_l(kb + kHalfBox, mq, &kv_full[st], 64, a.hq + a.g, row);
+            tma_load_3d_l(kb + 2 * kHalfBox, mq, &kv_full[st], 0, a.hq + a.hkv + a.g, row);
+            tma_load_3d_l(kb + 3 * kHalfBox, mq, &kv_full[st], 64, a.hq + a.hkv + a.g, row);
+          }
+        }
+        __syncwarp();
+        kv_it += a.n_kv;
+        ++att_it;
+      }
+    }
+  } else if (warp == 1) {
+    // =========================================================== MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int lin_it = 0, kv_it = 0, att_it = 0;
+    constexpr uint32_t idesc_lin = umma_idesc_bf16(128, 256);
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // B (V) MN-major
+    const uint32_t t_o = tmem + 256;
+    for (int idx = 0; idx < n_tasks; ++idx) {
+      Rec r;
+      load_rec(p, idx, sm, r);
+      const int* cfg = p.cfg + r.task_id * kCfgInts;
+      const int op = __ldg(cfg);
+      const int cls = op_class(op);
+      if (cls == CLS_ELEM) continue;
+      if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+      last_cls = cls;
+      if (cls == CLS_LINEAR) {
+        const int k = r.d1[0];
+        const int acc = lin_it & 1;
+        mbar_wait(&tempty[acc], ((lin_it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * 256;
+        for (int kb = 0; kb < k / 64; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smem + stage * kStage);
+            const uint32_t b_addr = a_addr + kAStage;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(d, umma_desc_k_sw128(a_addr + kk * 32), umma_desc_k_sw128(b_addr + kk * 32),
+                        idesc_lin, (kb | kk) != 0);
+            umma_commit(&empty_bar[stage]);
+          }
+          __syncwarp();
+          if (++stage == kRing) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit(&tfull[acc]);
+        __syncwarp();
+        ++lin_it;
+      } else {
+        const AttnGeom a = attn_geom(cfg, r);
+        const int n = a.n_kv;
+        mbar_wait(q_full, att_it & 1);
+        mbar_wait(o_empty, (att_it & 1) ^ 1);
+        tc_fence_after();
+        auto issue_pv = [&](int gi, int jl) {
+          const int st = gi & 1;
+          mbar_wait(p_full, gi & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t pa = smem_u32(smem + kPOff);
+            const uint32_t vb = smem_u32(smem + kKVOff + st * kKVStage + 2 * kHalfBox);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_bf16(t_o, umma_desc_k_sw128(pa + (kk >> 2) * kHalfBox + (kk & 3) * 32),
+                        desc_mn_sw128(vb + kk * 2048, kHalfBox), idesc_pv, (jl | kk) != 0);
+            umma_commit(&kv_empty[st]);
+            umma_commit(pv_done);
+          }
+          __syncwarp();
+        };
+        for (int j = 0; j < n; ++j) {
+          const int gi = kv_it + j, st = gi & 1;
+          mbar_wait(&kv_full[st], (gi >> 1) & 1);
+          mbar_wait(&s_empty[st], ((gi >> 1) & 1) ^ 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t qa = smem_u32(smem + kQOff);
+            const uint32_t kb = smem_u32(smem + kKVOff + st * kKVStage);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t off = (kk >> 2) * kHalfBox + (kk & 3) * 32;
+              umma_bf16(tmem + st * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off),
+                        idesc_s, kk != 0);
+            }
+            umma_commit(&s_full[st]);
+            if (j == n - 1) umma_commit(q_empty);
+          }
+          __syncwarp();
+          if (j > 0) issue_pv(gi - 1, j - 1);
+        }
+        issue_pv(kv_it + n - 1, n - 1);
+        kv_it += n;
+        ++att_it;
+      }
+    }
+  } else {
+    // =========================================================== epilogue / softmax / elementwise
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;                 // TMEM lane = tile row
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const int et = threadIdx.x - 64;                     // 0..127
+    const int ew = warp - 2;                             // 0..3
+    int lin_it = 0, kv_it = 0;
+    for (int idx = 0; idx < n_tasks; ++idx) {
+      Rec r;
+      load_rec(p, idx, sm, r);
+      const int* cfg = p.cfg + r.task_id * kCfgInts;
+      const int op = __ldg(cfg);
+      const int cls = op_class(op);
+      if (cls != CLS_ELEM) {
+        if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+        last_cls = cls;
+      }
+      if (op == OP_LINEAR) {
+        const int m = r.d0[0], n = r.d0[1];
+        const int epi = __ldg(cfg + 4);
+        const int out_slot = __ldg(cfg + 14);
+        const int ntn = (n + 255) / 256;
+        const int r0 = (r.tile / ntn) * 128, c0 = (r.tile % ntn) * 256;
+        const int ldy = out_slot == 3 ? r.d1[3] : r.d1[2];
+        uint16_t* y = reinterpret_cast<uint16_t*>(my_base + (out_slot == 3 ? r.off[3] : r.off[2]));
+        const int acc = lin_it & 1;
+        mbar_wait(&tfull[acc], (lin_it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t t_acc = tmem + lane_off + acc * 256;
+        const int grow = r0 + row;
+        const bool row_ok = grow < m;
+        if (epi == EPI_SILU_MUL) {
+          // tile columns [0,128) = gate rows, [128,256) = matching up rows -> 128 outputs
+          uint16_t* dst = y + static_cast<long long>(grow) * ldy + (c0 >> 1);
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t gv[32], uv[32];
+            tmem_ld_32x32b_x32(t_acc + c * 32, gv);
+            tmem_ld_32x32b_x32(t_acc + 128 + c * 32, uv);
+            tmem_ld_wait();
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float g = __uint_as_float(gv[i]);
+              o[i] = g / (1.f + __expf(-g)) * __uint_as_float(uv[i]);
+            }
+            if (row_ok) store_bf16x32(dst + c * 32, o, min(32, ldy - (c0 >> 1) - c * 32));
+          }
+        } else if (epi == EPI_ROPE) {
+          const int seq = __ldg(cfg + 9);
+          const int rope_cols = __ldg(cfg + 13);
+          const float* rope = reinterpret_cast<const float*>(my_base + r.off[2]);
+          const float* cs = rope + static_cast<long long>((row_ok ? grow : 0) % seq) * 128;
+          uint16_t* dst = y + static_cast<long long>(grow) * ldy + c0;
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            const bool rot = c0 + hh * 128 < rope_cols;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              uint32_t x1[32], x2[32];
+              tmem_ld_32x32b_x32(t_acc + hh * 128 + c * 32, x1);
+              tmem_ld_32x32b_x32(t_acc + hh * 128 + 64 + c * 32, x2);
+              tmem_ld_wait();
+              float o1[32], o2[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float a1 = __uint_as_float(x1[i]), a2 = __uint_as_float(x2[i]);
+                const float co = rot ? __ldg(cs + c * 32 + i) : 1.f;
+                const float si = rot ? __ldg(cs + 64 + c * 32 + i) : 0.f;
+                o1[i] = rot ? a1 * co - a2 * si : a1;
+                o2[i] = rot ? a2 * co + a1 * si : a2;
+              }
+              if (row_ok) {
+                const int cb = c0 + hh * 128 + c * 32;
+                store_bf16x32(dst + hh * 128 + c * 32, o1, min(32, ldy - cb));
+                store_bf16x32(dst + hh * 128 + 64 + c * 32, o2, min(32, ldy - cb - 64));
+              }
+            }
+          }
+        } else {
+          uint16_t* dst = y + static_cast<long long>(grow) * ldy + c0;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(t_acc + c * 32, v);
+            tmem_ld_wait();
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]);
+            if (row_ok && c0 + c * 32 < ldy) store_bf16x32(dst + c * 32, o, min(32, ldy - c0 - c * 32));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        ++lin_it;
+      } else if (op == OP_ATTENTION) {
+        const AttnGeom a = attn_geom(cfg, r);
+        const int n = a.n_kv;
+        const int causal = __ldg(cfg + 12);
+        const float scale_log2 = __int_as_float(__ldg(cfg + 10)) * 1.4426950408889634f;
+        const uint32_t t_o = tmem + 256;
+        float mrow = -INFINITY, l = 0.f;
+        uint8_t* prow = smem + kPOff + row * 128;
+        for (int j = 0; j < n; ++j) {
+          const int gi = kv_it + j, st = gi & 1;
+          mbar_wait(&s_full[st], (gi >> 1) & 1);
+          tc_fence_after();
+          uint32_t sv[4][32];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + lane_off + st * 128 + c * 32, sv[c]);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_empty[st]);
+          const bool diag = causal && j == n - 1;
+          float mx = mrow;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              float s = __uint_as_float(sv[c][i]) * scale_log2;
+              if (diag && c * 32 + i > row) s = -INFINITY;
+              sv[c][i] = __float_as_uint(s);
+              mx = fmaxf(mx, s);
+            }
+          const float alpha = exp2f(mrow - mx);
+          float sum = 0.f;
+          uint32_t pk[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float p0 = exp2f(__uint_as_float(sv[c][2 * i]) - mx);
+              const float p1 = exp2f(__uint_as_float(sv[c][2 * i + 1]) - mx);
+              sum += p0 + p1;
+              pk[c][i] = pack_bf16x2(p0, p1);
+            }
+          l = l * alpha + sum;
+          mrow = mx;
+          if (j > 0) {
+            mbar_wait(pv_done, (gi - 1) & 1);
+            tc_fence_after();
+            if (__any_sync(0xffffffffu, alpha < 1.f)) {
+#pragma unroll 1
+              for (int c = 0; c < 4; ++c) {
+                uint32_t ov[32];
+                tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                tmem_st_x32(t_o + lane_off + c * 32, ov);
+              }
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int chunk = c * 4 + q;
+              const int half = chunk >> 3, jj = chunk & 7;
+              *reinterpret_cast<uint4*>(prow + half * kHalfBox + ((jj ^ (row & 7)) << 4)) =
+                  make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+            }
+          fence_proxy_async_shared();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full);
+        }
+        mbar_wait(pv_done, (kv_it + n - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.f / l;
+        const int ldo = r.d1[1];
+        uint16_t* dst = reinterpret_cast<uint16_t*>(my_base + r.off[1]) +
+                        static_cast<long long>(a.q_row0 + row) * ldo + a.h * 128;
+        const bool row_ok = a.q_row0 + row < r.d0[1];
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
+          tmem_ld_wait();
+          float o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(ov[i]) * inv;
+          if (row_ok) store_bf16x32(dst + c * 32, o, 32);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_empty);
+        kv_it += n;
+      } else {
+        // ------------------------------------------------ elementwise tasks (128 threads)
+        const int npe = op == OP_ALLREDUCE_RES ? p.world : 1;
+        wait_deps(p, r, rank, npe, et, 128);
+        named_bar(2, 128);
+        const int br = __ldg(cfg + 3);
+        if (op == OP_RMSNORM) {
+          const int rows = r.d0[0], cols = r.d1[0];
+          const float eps = __int_as_float(__ldg(cfg + 11));
+          const uint16_t* x = reinterpret_cast<const uint16_t*>(my_base + r.off[0]);
+          const uint16_t* g = reinterpret_cast<const uint16_t*>(my_base + r.off[1]);
+          uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]);
+          const int r0 = r.tile * br, r1 = min(r0 + br, rows);
+          for (int rr = r0 + ew; rr < r1; rr += 4) {
+            const uint16_t* xr = x + static_cast<long long>(rr) * cols;
+            float ss = 0.f;
+            for (int c = lane * 8; c < cols; c += 256) {
+              const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float a0 = bf16lo(w[i]), a1 = bf16hi(w[i]);
+                ss += a0 * a0 + a1 * a1;
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const float rstd = rsqrtf(ss / static_cast<float>(cols) + eps);
+            uint16_t* yr = y + static_cast<long long>(rr) * cols;
+            for (int c = lane * 8; c < cols; c += 256) {
+              const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
+              const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g + c));
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+              const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+              uint32_t o[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                o[i] = pack_bf16x2(bf16lo(w[i]) * rstd * bf16lo(gw[i]), bf16hi(w[i]) * rstd * bf16hi(gw[i]));
+              *reinterpret_cast<uint4*>(yr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+          }
+        } else if (op == OP_ALLREDUCE_RES) {
+          // y = (x_0 + x_1 + ... + x_{w-1}) + res, fp32 in ascending PE order, bf16 out
+          const int rows = r.d0[0], cols = r.d1[0];
+          const int r0 = r.tile * br, r1 = min(r0 + br, rows);
+          const long long lo = static_cast<long long>(r0) * cols / 8, hi = static_cast<long long>(r1) * cols / 8;
+          const uint4* res = reinterpret_cast<const uint4*>(my_base + r.off[1]);
+          uint4* y = reinterpret_cast<uint4*>(my_base + r.off[2]);
+          for (long long i = lo + et; i < hi; i += 128) {
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+            for (int pe = 0; pe < p.world; ++pe) {
+              const uint4 v = reinterpret_cast<const uint4*>(p.base[pe] + r.off[0])[i];
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                acc[2 * e] += bf16lo(w[e]);
+                acc[2 * e + 1] += bf16hi(w[e]);
+              }
+            }
+            const uint4 rv = res[i];
+            const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = pack_bf16x2(acc[2 * e] + bf16lo(w[e]), acc[2 * e + 1] + bf16hi(w[e]));
+            y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      }
+      // every task of warps 2-5 ends with its scoreboard release
+      named_bar(2, 128);
+      if (et == 0) release_flag(p, rank, r);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  });
+  return fn;
+}
+
+// spec (8 x int64): heap offset, ndims (2|3), dims[3] (innermost first), box[3]; bf16, 128B swizzle
+int encode_spec(CUtensorMap* m, uint8_t* base, const int64_t* s) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return fail(TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int nd = static_cast<int>(s[1]);
+  if (nd != 2 && nd != 3) return fail(TF_ERR_INVALID, "tensor map spec needs 2 or 3 dims");
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], estr[3] = {1, 1, 1};
+  for (int i = 0; i < nd; ++i) {
+    dims[i] = static_cast<cuuint64_t>(s[2 + i]);
+    box[i] = static_cast<cuuint32_t>(s[5 + i]);
+  }
+  strides[0] = dims[0] * 2;
+  if (nd == 3) strides[1] = dims[0] * dims[1] * 2;
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, nd, base + s[0], dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(TF_ERR_INVALID, "layer tensor map encode failed (code " + std::to_string(r) + ")");
+  return TF_OK;
+}
+
+struct MapCache {
+  std::string key;
+  void* dev = nullptr;
+};
+std::mutex g_map_mu;
+std::map<std::pair<const tf_team*, int>, MapCache> g_maps;
+
+}  // namespace
+}  // namespace tf
+
+using tf::fail;
+
+extern "C" int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args* a, void* stream) {
+  if (!t || !a) return fail(TF_ERR_INVALID, "NULL argument");
+  if (a->num_sms < 1) return fail(TF_ERR_INVALID, "num_sms must be >= 1");
+  if (a->num_maps < 0 || (a->num_maps > 0 && !a->map_specs))
+    return fail(TF_ERR_INVALID, "bad tensor map specs");
+  int first = 0, nranks = t->world, fixed = -1;
+  if (t->ipc) {
+    if (rank != t->my_rank) return fail(TF_ERR_INVALID, "IPC team: rank must be this process's rank");
+    first = rank;
+    nranks = 1;
+    fixed = rank;
+  } else {
+    if (rank >= 0) {
+      if (t->world != 1 || rank != 0)
+        return fail(TF_ERR_CONFIG, "local team: pass rank -1 (all ranks co-scheduled in one launch)");
+    }
+    for (int pe = 1; pe < t->world; ++pe)
+      if (t->pes[pe].device != t->pes[0].device)
+        return fail(TF_ERR_CONFIG, "the co-scheduled megakernel needs every PE on one device");
+  }
+  tf::DeviceGuard guard(t->pes[first].device);
+  const int grid = nranks * a->num_sms;
+  if (grid > tf::num_sms_of_current_device())
+    return fail(TF_ERR_CONFIG, "ranks * num_sms CTAs must be co-resident (<= SM count)");
+  // tensor maps per launched rank, cached per (team, rank) by spec content
+  std::string key(reinterpret_cast<const char*>(a->map_specs),
+                  static_cast<size_t>(a->num_maps) * 8 * sizeof(int64_t));
+  for (int rr = 0; rr < nranks; ++rr)  // a recycled team address must not reuse stale maps
+    key.append(reinterpret_cast<const char*>(&t->pes[first + rr].base), sizeof(void*));
+  void* dmaps = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(tf::g_map_mu);
+    auto& mc = tf::g_maps[{t, rank}];
+    if (mc.dev == nullptr || mc.key != key) {
+      std::vector<CUtensorMap> host(static_cast<size_t>(nranks) * std::max(a->num_maps, 1));
+      for (int rr = 0; rr < nranks; ++rr)
+        for (int i = 0; i < a->num_maps; ++i) {
+          int rc = tf::encode_spec(&host[static_cast<size_t>(rr) * a->num_maps + i],
+                                   t->pes[first + rr].base, a->map_specs + 8 * i);
+          if (rc) return rc;
+        }
+      if (mc.dev) cudaFree(mc.dev);
+      mc.dev = nullptr;
+      TF_CUDA_TRY(cudaMalloc(&mc.dev, host.size() * sizeof(CUtensorMap)));
+      TF_CUDA_TRY(cudaMemcpy(mc.dev, host.data(), host.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      mc.key = key;
+    }
+    dmaps = mc.dev;
+  }
+  tf::LayerParams p{};
+  p.queues = a->queues;
+  p.counts = a->counts;
+  p.deps = a->deps;
+  p.cfg = a->layer_cfg;
+  p.maps = static_cast<const CUtensorMap*>(dmaps);
+  p.num_maps = a->num_maps;
+  p.num_sms = a->num_sms;
+  p.max_tiles = a->max_tiles;
+  p.fixed_rank = fixed;
+  p.world = t->world;
+  p.flag_base = a->flag_base;
+  p.epoch = a->epoch ? a->epoch : 1;
+  p.timeout_ns = a->timeout_ns ? a->timeout_ns : t->timeout_ns;
+  for (int pe = 0; pe < t->world; ++pe) {
+    p.base[pe] = t->pes[pe].base;
+    p.sig[pe] = t->pes[pe].sig;
+    p.err[pe] = t->err_word(pe);
+  }
+  static uint64_t attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_done & (1ull << dev))) {
+    TF_CUDA_TRY(cudaFuncSetAttribute(tf::layer_megakernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tf::kLayerSmem));
+    attr_done |= 1ull << dev;
+  }
+  tf::layer_megakernel<<<grid, tf::kLThreads, tf::kLayerSmem, static_cast<cudaStream_t>(stream)>>>(p);
+  TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}

@@ -412,6 +412,8 @@ def run_megakernel(program: MegaProgram, built: BuiltGraph, num_sms: int, *, que
     world = topo.world_size
     if num_sms < 1 or num_sms > topo.num_sms:
         raise ValueError(f"num_sms must be in [1, {topo.num_sms}]")
+    if any(_layer.is_bf16(t) for t in program.tensors):
+        return _run_bf16(program, built, num_sms, queues, counts, inputs or {}, devices, timeout_s)
     if queues is None:
         queues, counts = encode_work_queues(built.tasks, num_sms)
     elif counts is None:
@@ -487,3 +489,39 @@ def run_megakernel(program: MegaProgram, built: BuiltGraph, num_sms: int, *, que
 def _handle(t: MkTensor):
     from .shmem import SymmHandle
     return SymmHandle(offset=t.offset, nbytes=t.nbytes)
+
+
+def _run_bf16(program, built, num_sms, queues, counts, inputs, devices, timeout_s) -> MegaRun:
+    """bf16 programs (transformer-layer ops) run on the fused-layer kernel."""
+    import torch
+    if torch.cuda.device_count() == 0:
+        raise RuntimeError("no CUDA device: the megakernel has no CPU path")
+    world = program.topology.world_size
+    dev = 0 if devices is None else devices[0]
+    if devices is not None and len(set(devices)) != 1:
+        raise ValueError("the single-process megakernel co-schedules all ranks on one device")
+    if queues is not None and counts is None:
+        raise ValueError("explicit queues need explicit counts")
+    runner = _layer.LayerRunner(program, built, num_sms, device=dev, queues=queues, counts=counts,
+                                timeout_s=timeout_s)
+    for name, value in inputs.items():
+        t = runner.by_name[name]
+        per_rank = value if isinstance(value, (list, tuple)) else [value] * world
+        if len(per_rank) != world:
+            raise ValueError(f"input {name!r} needs {world} per-rank arrays")
+        for r, arr in enumerate(per_rank):
+            v = runner.view(name, r)
+            src = torch.as_tensor(np.asarray(arr, dtype=np.float32).reshape(t.shape))
+            v.copy_(src.to(v.dtype).to(v.device))
+    torch.cuda.synchronize(dev)
+    runner.run()
+    torch.cuda.synchronize(dev)
+    runner.check()
+    outputs = {t.name: [runner.view(t.name, r).float().cpu().numpy() for r in range(world)]
+               for t in program.tensors}
+    boards = [Scoreboard(runner.heap, runner.flags, runner.built.dep_table, runner.built.max_task_id,
+                         runner.built.max_tiles_per_op, r) for r in range(world)]
+    return MegaRun(outputs, None, runner.heap, boards)
+
+
+from . import layer as _layer  # noqa: E402  (registers the bf16 layer ops)
