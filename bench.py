@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--group-m", type=int, default=int(os.environ.get("TF_GROUP_M", "8")))
     p.add_argument("--no-moe", action="store_true")
     p.add_argument("--no-attn", action="store_true")
+    p.add_argument("--no-layer", action="store_true")
+    p.add_argument("--only-layer", action="store_true")
     return p.parse_args()
 
 
@@ -304,6 +306,119 @@ def bench_attention(dev, steps, peaks):
                          "peak": peaks.get("bf16_tflops", 1622.7), "unit": "TFLOP/s"}}
 
 
+# ------------------------------------------------------------------ fused layer (config 5)
+LAY_T, LAY_H, LAY_HQ, LAY_HKV, LAY_F = 8192, 8192, 64, 8, 28672
+
+
+def layer_flops(tokens, hidden, hq, hkv, ffn, tp=1):
+    """Algorithmic FLOPs of one Llama layer shard (causal attention counted at T^2/2)."""
+    hq, hkv, f = hq // tp, hkv // tp, ffn // tp
+    qkv = 2.0 * tokens * hidden * (hq + 2 * hkv) * 128
+    att = 4.0 * tokens * tokens * 128 * hq / 2
+    o = 2.0 * tokens * hq * 128 * hidden
+    mlp = 2.0 * tokens * hidden * 2 * f + 2.0 * tokens * f * hidden
+    return qkv + att + o + mlp
+
+
+def bench_layer(dev, steps, warmup, peaks, flush, tp_emulated=1):
+    """Config 5 on one GPU: the Llama-3-70B layer (8192 tokens, hidden 8192, 64/8
+    heads, ffn 28672, one causal sequence) as ONE persistent megakernel launch
+    (rmsnorm -> QKV+RoPE -> attention -> O -> allreduce+residual -> rmsnorm ->
+    gate/up+SiLU -> down -> allreduce+residual).  TP=1 here (the allreduce tasks
+    reduce a single partial); the unfused comparator is cuBLAS GEMMs + cuDNN/flash
+    SDPA + torch elementwise on the same bf16 tensors."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2605_02953_b200 import build_topology
+    from paper_2605_02953_b200 import layer as L
+    T, H, HQ, HKV, FF = LAY_T, LAY_H, LAY_HQ, LAY_HKV, LAY_F
+    prog = L.llama_layer_program(build_topology(1, 1), T, H, HQ, HKV, FF, seq_len=T)
+    runner = L.LayerRunner(prog, device=dev)
+    g = torch.Generator(device="cpu").manual_seed(55)
+    mk = lambda *s, sc=1.0: (torch.randn(*s, generator=g) * sc).to(torch.bfloat16).to(f"cuda:{dev}")
+    qkv_n = (HQ + 2 * HKV) * 128
+    x = mk(T, H)
+    w = {"w_qkv": mk(qkv_n, H, sc=H ** -0.5), "w_o": mk(H, HQ * 128, sc=(HQ * 128) ** -0.5),
+         "w_gate_up": mk(2 * FF, H, sc=H ** -0.5), "w_down": mk(H, FF, sc=FF ** -0.5)}
+    g1 = (1 + 0.1 * torch.randn(1, H, generator=g)).to(torch.bfloat16).to(f"cuda:{dev}")
+    g2 = (1 + 0.1 * torch.randn(1, H, generator=g)).to(torch.bfloat16).to(f"cuda:{dev}")
+    rope = torch.from_numpy(L.rope_table(T)).to(f"cuda:{dev}")
+    for name, val in [("x", x), ("g_attn", g1), ("g_mlp", g2), ("rope", rope), *w.items()]:
+        runner.view(name).copy_(val)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        runner.run(stream)
+    torch.cuda.synchronize(dev)
+    runner.check()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record(stream)
+        runner.run(stream)
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    runner.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    flops = layer_flops(T, H, HQ, HKV, FF)
+    out_fused = runner.view("out").clone()
+
+    # ---- unfused comparator on the same tensors (gate/up de-interleaved for torch)
+    wgu = w["w_gate_up"].view(FF // 128, 2, 128, H)
+    wg, wu = wgu[:, 0].reshape(FF, H).contiguous(), wgu[:, 1].reshape(FF, H).contiguous()
+    cos = rope[:, :64].to(torch.float32)
+    sin = rope[:, 64:].to(torch.float32)
+
+    def rms(t, gg):
+        tf = t.float()
+        return (tf * torch.rsqrt(tf.pow(2).mean(-1, keepdim=True) + 1e-5) * gg.float()).to(torch.bfloat16)
+
+    def rot(t):  # [T, heads, 128]
+        tf = t.float()
+        a1, a2 = tf[..., :64], tf[..., 64:]
+        c, s_ = cos[:, None, :], sin[:, None, :]
+        return torch.cat([a1 * c - a2 * s_, a2 * c + a1 * s_], -1).to(torch.bfloat16)
+
+    def unfused():
+        xn = rms(x, g1)
+        qkv = xn @ w["w_qkv"].t()
+        q = rot(qkv[:, :HQ * 128].view(T, HQ, 128))
+        k = rot(qkv[:, HQ * 128:(HQ + HKV) * 128].view(T, HKV, 128))
+        v = qkv[:, (HQ + HKV) * 128:].view(T, HKV, 128)
+        att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                             v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
+        att = att[0].transpose(0, 1).reshape(T, HQ * 128)
+        h = att @ w["w_o"].t() + x
+        hn = rms(h, g2)
+        act = F.silu(hn @ wg.t()) * (hn @ wu.t())
+        return act @ w["w_down"].t() + h
+
+    ref = None
+    for _ in range(2):
+        ref = unfused()
+    torch.cuda.synchronize(dev)
+    cevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for e0, e1 in cevs:
+        flush.zero_()
+        e0.record(stream)
+        unfused()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    cms = sum(a.elapsed_time(b) for a, b in cevs) / steps
+    rel = float((out_fused.float() - ref.float()).abs().max() / ref.float().abs().max())
+    runner.close()
+    peak = peaks.get("bf16_tflops", 1622.7)
+    return {"workload": f"config 5: Llama-3-70B layer, {T} tokens (one causal sequence), hidden {H}, "
+                        f"{HQ}/{HKV} heads, ffn {FF}, TP=1, bf16, one persistent megakernel launch",
+            "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2),
+            "flops": flops, "tasks": len(runner.built.tasks),
+            "roofline": {"bound": "tensor", "frac": round(flops / (ms * 1e-3) / 1e12 / peak, 4),
+                         "peak": peak, "unit": "TFLOP/s"},
+            "comparator": {"impl": "unfused cuBLAS GEMMs + torch SDPA (causal, GQA) + torch elementwise",
+                           "ms": round(cms, 4), "speedup": round(cms / ms, 4)},
+            "max_rel_err_vs_unfused": round(rel, 5)}
+
+
 # ------------------------------------------------------------------ GPU arm
 def main_ours(args):
     import torch
@@ -312,6 +427,11 @@ def main_ours(args):
     from paper_2605_02953_b200 import kernels as K
     from paper_2605_02953_b200.shmem import Team
 
+    if args.only_layer:  # probe: config 5 only
+        torch.cuda.set_device(0)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
+        print(json.dumps(bench_layer(0, args.steps, args.warmup, load_peaks()[0], flush)), flush=True)
+        return
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     distributed = world_env > 1
     shared_gpus = False
@@ -524,6 +644,10 @@ def main_ours(args):
     if not args.no_attn and world == 1:
         attn = bench_attention(dev, 3, peaks)
 
+    layer = None
+    if not args.no_layer and world == 1:
+        layer = bench_layer(dev, max(3, args.steps // 4), 2, peaks, flush)
+
     launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
     if rank == 0:
         line = {
@@ -543,7 +667,7 @@ def main_ours(args):
                 "ms_per_step": round(cub_ms, 4),
                 "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
                 "speedup": round(cub_ms / step_ms, 4)},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "attention": attn,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "attention": attn, "layer": layer,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -80,7 +80,7 @@ struct LayerParams {
 
 struct Rec {
   int task_id, tile, dep0, dep1;
-  int off[4];
+  long long off[4];  // bytes; tag bits 8-11 = shift of the encoded offset (heaps > 2 GiB)
   int d0[4], d1[4];
 };
 
@@ -92,7 +92,7 @@ __device__ __forceinline__ void load_rec(const LayerParams& p, int idx, int sm, 
   r.dep1 = __ldg(q + 5);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    r.off[i] = __ldg(q + 6 + 6 * i);
+    r.off[i] = static_cast<long long>(__ldg(q + 6 + 6 * i)) << ((__ldg(q + 7 + 6 * i) >> 8) & 0xF);
     r.d0[i] = __ldg(q + 8 + 6 * i);
     r.d1[i] = __ldg(q + 9 + 6 * i);
   }

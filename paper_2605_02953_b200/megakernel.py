@@ -45,6 +45,7 @@ INT_PER_DEPS = 3
 DTYPE_TAGS = {np.dtype(np.float32): 0, np.dtype(np.int64): 1}
 TAG_DTYPES = {v: k for k, v in DTYPE_TAGS.items()}
 _INT32 = (-(2 ** 31), 2 ** 31 - 1)
+OFFSET_SHIFT = 4
 
 
 def _i32(v: int, what: str) -> int:
@@ -98,8 +99,13 @@ def encode_task(task: TaskRecord) -> np.ndarray:
         slot = task.io[i]
         if not 1 <= len(slot.dims) <= MAX_NUM_TENSOR_DIMS or min(slot.dims) < 1:
             raise ValueError(f"io tensor needs 1..{MAX_NUM_TENSOR_DIMS} dims >= 1, got {slot.dims}")
-        w[base] = _i32(slot.offset, "io offset")
-        w[base + 1] = _i32(slot.dtype_tag, "dtype tag")
+        off, tag = slot.offset, slot.dtype_tag
+        if off > _INT32[1] and off % 16 == 0:
+            # extension for heaps past 2 GiB (the reference's are < 2 GiB, where the
+            # encoding is unchanged): offset in 16-byte units, shift in tag bits 8-11
+            off, tag = off >> OFFSET_SHIFT, tag | (OFFSET_SHIFT << 8)
+        w[base] = _i32(off, "io offset")
+        w[base + 1] = _i32(tag, "dtype tag")
         w[base + 2:base + 2 + len(slot.dims)] = [_i32(d, "dim") for d in slot.dims]
     return w
 
@@ -112,7 +118,8 @@ def decode_task(words) -> TaskRecord:
         if int(words[base]) < 0:
             continue
         dims = tuple(int(d) for d in words[base + 2:base + 2 + MAX_NUM_TENSOR_DIMS] if d != 0)
-        io.append(IoSlot(int(words[base]), int(words[base + 1]), dims))
+        tag = int(words[base + 1])
+        io.append(IoSlot(int(words[base]) << ((tag >> 8) & 0xF), tag & 0xFF, dims))
     return TaskRecord(*(int(words[o]) for o in range(IO_TENSORS_OFFSET)), io=tuple(io))
 
 
