@@ -316,6 +316,12 @@ typedef struct tf_layer_args {
   const int64_t* map_specs;
   int32_t num_maps, num_sms, max_tiles, num_layers;
   uint64_t flag_base, epoch, timeout_ns;
+  /* optional device trace, [ctas][slots][4] u64 (NULL = off): per task the
+   * %globaltimer ns when warp 0 (tensor tasks) / warps 2-5 (elementwise) picked
+   * it up, when its dependencies were satisfied, when its flag was released,
+   * and task_id << 32 | tile */
+  uint64_t* trace;
+  int32_t trace_slots; /* queue slots per CTA in the trace layout */
 } tf_layer_args;
 int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args* a, void* stream);
 

@@ -76,6 +76,8 @@ struct LayerParams {
   uint8_t* base[kMaxWorld];
   uint64_t* sig[kMaxWorld];
   unsigned long long* err[kMaxWorld];
+  unsigned long long* trace;  // [ctas][slots][4] or nullptr
+  int slots;
 };
 
 struct Rec {
@@ -139,6 +141,10 @@ __device__ __forceinline__ void release_flag(const LayerParams& p, int rank, con
               0x9000000ull | (static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile));
   fence_sys();
   st_release_sys(f, p.epoch);
+}
+
+__device__ __forceinline__ unsigned long long* trace_at(const LayerParams& p, int idx) {
+  return p.trace + (static_cast<long long>(blockIdx.x) * p.slots + idx) * 4;
 }
 
 __device__ __forceinline__ void tma_load_3d_l(void* smem_dst, const void* tmap, uint64_t* bar,
@@ -282,8 +288,14 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       if (cls == CLS_ELEM) continue;
       if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
       last_cls = cls;
+      const unsigned long long t_fetch = p.trace ? globaltimer_ns() : 0;
       const bool waited = __any_sync(0xffffffffu, wait_deps(p, r, rank, 1, lane, 32));
       __syncwarp();
+      if (p.trace && lane == 0) {
+        unsigned long long* tr = trace_at(p, idx);
+        tr[0] = t_fetch;
+        tr[1] = globaltimer_ns();
+      }
       if (cls == CLS_LINEAR) {
         const int m = r.d0[0], k = r.d1[0], n = r.d0[1];
         (void)m;
@@ -613,76 +625,124 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       } else {
         // ------------------------------------------------ elementwise tasks (128 threads)
         const int npe = op == OP_ALLREDUCE_RES ? p.world : 1;
+        const unsigned long long t_fetch = p.trace ? globaltimer_ns() : 0;
         wait_deps(p, r, rank, npe, et, 128);
         named_bar(2, 128);
+        if (p.trace && et == 0) {
+          unsigned long long* tr = trace_at(p, idx);
+          tr[0] = t_fetch;
+          tr[1] = globaltimer_ns();
+        }
         const int br = __ldg(cfg + 3);
         if (op == OP_RMSNORM) {
+          // one warp per row; 8 x 16-byte loads in flight per lane, second pass hits L1/L2
           const int rows = r.d0[0], cols = r.d1[0];
           const float eps = __int_as_float(__ldg(cfg + 11));
           const uint16_t* x = reinterpret_cast<const uint16_t*>(my_base + r.off[0]);
           const uint16_t* g = reinterpret_cast<const uint16_t*>(my_base + r.off[1]);
           uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]);
           const int r0 = r.tile * br, r1 = min(r0 + br, rows);
+          constexpr int U = 8;
           for (int rr = r0 + ew; rr < r1; rr += 4) {
             const uint16_t* xr = x + static_cast<long long>(rr) * cols;
             float ss = 0.f;
-            for (int c = lane * 8; c < cols; c += 256) {
-              const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            for (int c0 = lane * 8; c0 < cols; c0 += 256 * U) {
+              uint4 v[U];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float a0 = bf16lo(w[i]), a1 = bf16hi(w[i]);
-                ss += a0 * a0 + a1 * a1;
+              for (int u = 0; u < U; ++u)
+                v[u] = c0 + u * 256 < cols ? *reinterpret_cast<const uint4*>(xr + c0 + u * 256)
+                                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float a0 = bf16lo(w[i]), a1 = bf16hi(w[i]);
+                  ss += a0 * a0 + a1 * a1;
+                }
               }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
             const float rstd = rsqrtf(ss / static_cast<float>(cols) + eps);
             uint16_t* yr = y + static_cast<long long>(rr) * cols;
-            for (int c = lane * 8; c < cols; c += 256) {
-              const uint4 v = *reinterpret_cast<const uint4*>(xr + c);
-              const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g + c));
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-              const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
-              uint32_t o[4];
+            for (int c0 = lane * 8; c0 < cols; c0 += 256 * U) {
+              uint4 v[U], gv[U];
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                o[i] = pack_bf16x2(bf16lo(w[i]) * rstd * bf16lo(gw[i]), bf16hi(w[i]) * rstd * bf16hi(gw[i]));
-              *reinterpret_cast<uint4*>(yr + c) = make_uint4(o[0], o[1], o[2], o[3]);
+              for (int u = 0; u < U; ++u)
+                if (c0 + u * 256 < cols) {
+                  v[u] = *reinterpret_cast<const uint4*>(xr + c0 + u * 256);
+                  gv[u] = __ldg(reinterpret_cast<const uint4*>(g + c0 + u * 256));
+                }
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (c0 + u * 256 < cols) {
+                  const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                  const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+                  uint32_t o[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    o[i] = pack_bf16x2(bf16lo(w[i]) * rstd * bf16lo(gw[i]), bf16hi(w[i]) * rstd * bf16hi(gw[i]));
+                  *reinterpret_cast<uint4*>(yr + c0 + u * 256) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
             }
           }
         } else if (op == OP_ALLREDUCE_RES) {
-          // y = (x_0 + x_1 + ... + x_{w-1}) + res, fp32 in ascending PE order, bf16 out
+          // y = (x_0 + x_1 + ... + x_{w-1}) + res, fp32 in ascending PE order, bf16 out;
+          // 4 chunks of 8 elements per thread per round (loads of all PEs in flight)
           const int rows = r.d0[0], cols = r.d1[0];
           const int r0 = r.tile * br, r1 = min(r0 + br, rows);
           const long long lo = static_cast<long long>(r0) * cols / 8, hi = static_cast<long long>(r1) * cols / 8;
           const uint4* res = reinterpret_cast<const uint4*>(my_base + r.off[1]);
           uint4* y = reinterpret_cast<uint4*>(my_base + r.off[2]);
-          for (long long i = lo + et; i < hi; i += 128) {
-            float acc[8];
+          constexpr int U = 4;
+          for (long long i0 = lo + et; i0 < hi; i0 += 128 * U) {
+            float acc[U][8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
             for (int pe = 0; pe < p.world; ++pe) {
-              const uint4 v = reinterpret_cast<const uint4*>(p.base[pe] + r.off[0])[i];
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+              const uint4* src = reinterpret_cast<const uint4*>(p.base[pe] + r.off[0]);
+              uint4 v[U];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                acc[2 * e] += bf16lo(w[e]);
-                acc[2 * e + 1] += bf16hi(w[e]);
+              for (int u = 0; u < U; ++u) v[u] = i0 + u * 128 < hi ? src[i0 + u * 128] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  acc[u][2 * e] += bf16lo(w[e]);
+                  acc[u][2 * e + 1] += bf16hi(w[e]);
+                }
               }
             }
-            const uint4 rv = res[i];
-            const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
-            uint32_t o[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) o[e] = pack_bf16x2(acc[2 * e] + bf16lo(w[e]), acc[2 * e + 1] + bf16hi(w[e]));
-            y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+            for (int u = 0; u < U; ++u) {
+              const long long i = i0 + u * 128;
+              if (i < hi) {
+                const uint4 rv = res[i];
+                const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  o[e] = pack_bf16x2(acc[u][2 * e] + bf16lo(w[e]), acc[u][2 * e + 1] + bf16hi(w[e]));
+                y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+              }
+            }
           }
         }
       }
       // every task of warps 2-5 ends with its scoreboard release
       named_bar(2, 128);
-      if (et == 0) release_flag(p, rank, r);
+      if (et == 0) {
+        release_flag(p, rank, r);
+        if (p.trace) {
+          unsigned long long* tr = trace_at(p, idx);
+          tr[2] = globaltimer_ns();
+          tr[3] = (static_cast<unsigned long long>(r.task_id) << 32) | static_cast<unsigned>(r.tile);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -814,6 +874,8 @@ extern "C" int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args
     p.sig[pe] = t->pes[pe].sig;
     p.err[pe] = t->err_word(pe);
   }
+  p.trace = reinterpret_cast<unsigned long long*>(a->trace);
+  p.slots = a->trace_slots;
   static uint64_t attr_done = 0;
   int dev = 0;
   cudaGetDevice(&dev);

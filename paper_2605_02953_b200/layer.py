@@ -91,8 +91,15 @@ def plan_linear_bf16(io, config) -> MK.LayerPlan:
         raise BuildError("linear takes (x, w)")
     tm_n, tn_n = -(-m // BLOCK_M), -(-n // BLOCK_N)
     tiles = []
-    for tm in range(tm_n):
-        for tn in range(tn_n):
+    # emission order = grouped raster (swizzle_2d, ovs/swizzle.py:76-88) so the tiles one
+    # wave of round-robin queues runs share group_m A panels and ~grid/group_m B panels in
+    # L2; tile ids stay row-major (the dependency contract)
+    gm = max(1, int(cfg.get("group_m", 16)))
+    for step in range(tm_n * tn_n):
+        grp, r = divmod(step, gm * tn_n)
+        rows = min(tm_n - grp * gm, gm)
+        tm, tn = grp * gm + r % rows, r // rows
+        if True:
             deps = [MK.InputDependencyDesc(x, start_indices=(tm * BLOCK_M, 0),
                                            data_sizes=(min(BLOCK_M, m - tm * BLOCK_M), k)),
                     MK.InputDependencyDesc(w, start_indices=(tn * BLOCK_N, 0),
@@ -244,7 +251,8 @@ class LayerArgs(C.Structure):
     _fields_ = [("queues", C.c_void_p), ("counts", C.c_void_p), ("deps", C.c_void_p),
                 ("layer_cfg", C.c_void_p), ("map_specs", C.c_void_p), ("num_maps", C.c_int32),
                 ("num_sms", C.c_int32), ("max_tiles", C.c_int32), ("num_layers", C.c_int32),
-                ("flag_base", C.c_uint64), ("epoch", C.c_uint64), ("timeout_ns", C.c_uint64)]
+                ("flag_base", C.c_uint64), ("epoch", C.c_uint64), ("timeout_ns", C.c_uint64),
+                ("trace", C.c_void_p), ("trace_slots", C.c_int32)]
 
 
 class LayerRunner:
@@ -315,6 +323,23 @@ class LayerRunner:
         dt = torch.bfloat16 if is_bf16(t) else np.dtype(t.dtype)
         return self.heap.view(self.handles[name], pe, dt, t.shape)
 
+    def enable_trace(self, on: bool = True) -> None:
+        """Per-task device timestamps (fetch, deps satisfied, released) for the next runs."""
+        import torch
+        ctas = self.num_sms * (self.world if self.rank < 0 else 1)
+        self._trace = (torch.zeros(ctas, self.queues.shape[0], 4, dtype=torch.int64,
+                                   device=f"cuda:{self.device}") if on else None)
+
+    def trace(self):
+        """[(cta, task_id, tile, t_fetch, t_deps_ok, t_done)] of the last traced run (ns)."""
+        t = self._trace.cpu().numpy()
+        out = []
+        for cta in range(t.shape[0]):
+            for idx in range(int(self.counts[cta % self.num_sms])):
+                f, d, e, tt = (int(v) for v in t[cta, idx])
+                out.append((cta, tt >> 32, tt & 0xFFFFFFFF, f, d, e))
+        return out
+
     def run(self, stream=None) -> None:
         import torch
 
@@ -322,10 +347,12 @@ class LayerRunner:
         if not self.built.tasks:
             return
         self.epoch += 1
+        tr = getattr(self, "_trace", None)
         args = LayerArgs(self._tq.data_ptr(), self._tc.data_ptr(), self._td.data_ptr(),
                          self._tcfg.data_ptr(), self.specs.ctypes.data, len(self.specs), self.num_sms,
                          self.built.max_tiles_per_op, len(self.built.layer_ops), self.flags.base,
-                         self.epoch, self.timeout_ns)
+                         self.epoch, self.timeout_ns, 0 if tr is None else tr.data_ptr(),
+                         self.queues.shape[0])
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
             _lib.call("tf_layer_megakernel_run", self.team.handle, int(self.rank), C.byref(args),
