@@ -9,16 +9,18 @@
 // walks the CTA's queue in order and does its share of each task:
 //
 //   task          warp 0 (TMA)            warp 1 (MMA, one lane)     warps 2-5 (128 thr)
-//   linear        wait deps, A/B boxes    tcgen05 128x256x16 into    TMEM -> epilogue (plain |
-//                 into a 4-stage ring     a double-buffered TMEM     RoPE | SiLU*up) -> bf16,
-//                                         accumulator                release the tile flag
+//   linear        wait deps, A (2 x 128   tcgen05 128x256x16 per     TMEM -> epilogue (plain |
+//   (256 x 256)   rows) + B (256 rows)    M-half into TMEM [0,256)   RoPE | SiLU*up) -> bf16
+//                 boxes, 3-stage ring     and [256,512); half 1      per half, release the
+//                                         lags 2 k-blocks at tile    tile flag
+//                                         edges (drain overlaps)
 //   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
 //                 tiles (2 stages)        (V MN-major)               mask), O / l -> bf16
 //   rmsnorm       -                       -                          wait deps, y = x*rstd*g
 //   allreduce_    -                       -                          wait deps on every PE,
 //   residual                                                         y = sum_pe x_pe + res (P2P)
 //
-// The linear ring (4 x 48 KB) and the attention buffers (Q, 2 x K/V, P) alias the
+// The linear ring (3 x 64 KB) and the attention buffers (Q, 2 x K/V, P) alias the
 // same 192 KB of shared memory and TMEM columns [0, 512); when consecutive tensor
 // tasks of a CTA change class, all six warps meet at a named barrier first, by
 // which point every TMA load has been consumed and every MMA has retired.
@@ -42,12 +44,13 @@ namespace tf {
 namespace {
 
 constexpr int kLThreads = 192;
-constexpr int kRing = 4;
+constexpr int kRing = 3;
 constexpr int kHalfBox = 16384;               // 128 rows x 128 B
-constexpr int kAStage = 128 * 64 * 2;         // 16 KB
+constexpr int kAStage = 2 * 128 * 64 * 2;     // two 128-row A blocks, 32 KB
 constexpr int kBStage = 256 * 64 * 2;         // 32 KB
-constexpr int kStage = kAStage + kBStage;     // 48 KB
+constexpr int kStage = kAStage + kBStage;     // 64 KB
 constexpr int kRegion = kRing * kStage;       // 192 KB
+constexpr int kLag = 2;                       // k-blocks the second M-half trails at tile edges
 constexpr int kQOff = 0;                      // attention aliases
 constexpr int kKVOff = 2 * kHalfBox;          // 2 stages x (K 32 KB + V 32 KB)
 constexpr int kKVStage = 4 * kHalfBox;
@@ -141,6 +144,16 @@ __device__ __forceinline__ void release_flag(const LayerParams& p, int rank, con
               0x9000000ull | (static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile));
   fence_sys();
   st_release_sys(f, p.epoch);
+}
+
+// bulk L2 prefetch of [ptr, ptr + bytes) in 64 KB pieces, spread over the calling threads
+__device__ __forceinline__ void prefetch_l2(const void* ptr, long long bytes, int t, int nt) {
+  const char* c = static_cast<const char*>(ptr);
+  for (long long o = static_cast<long long>(t) << 16; o < bytes; o += static_cast<long long>(nt) << 16) {
+    const long long n = min(bytes - o, 65536ll);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c + o), "r"(static_cast<uint32_t>(n & ~15ll))
+                 : "memory");
+  }
 }
 
 __device__ __forceinline__ unsigned long long* trace_at(const LayerParams& p, int idx) {
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
   uint8_t* my_base = p.base[rank];
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kRing; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const int m = r.d0[0], k = r.d1[0], n = r.d0[1];
         (void)m;
         const int ntn = (n + 255) / 256;
-        const int r0 = (r.tile / ntn) * 128, c0 = (r.tile % ntn) * 256;
+        const int r0 = (r.tile / ntn) * 256, c0 = (r.tile % ntn) * 256;
         const CUtensorMap* ma = maps + __ldg(cfg + 5);
         const CUtensorMap* mb = maps + __ldg(cfg + 6);
         if (lane == 0) {
@@ -310,6 +323,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
             uint8_t* sa = smem + stage * kStage;
             mbar_arrive_expect_tx(&full_bar[stage], kStage);
             tma_load_2d(sa, ma, &full_bar[stage], kb * 64, r0);
+            tma_load_2d(sa + kHalfBox, ma, &full_bar[stage], kb * 64, r0 + 128);
             tma_load_2d(sa + kAStage, mb, &full_bar[stage], kb * 64, c0);
             if (++stage == kRing) { stage = 0; phase ^= 1; }
           }
@@ -360,27 +374,61 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
       last_cls = cls;
       if (cls == CLS_LINEAR) {
-        const int k = r.d1[0];
-        const int acc = lin_it & 1;
-        mbar_wait(&tempty[acc], ((lin_it >> 1) & 1) ^ 1);
+        // two M=128 halves per 256x256 tile share each B stage; half h accumulates in
+        // TMEM columns [256h, 256h + 256) with its own full/empty pair.  At tile edges
+        // half 1 trails by kLag k-blocks so the epilogue drains half 0 while half 1
+        // finishes, and the next tile's half 0 starts while half 1 drains.
+        const int nkb = r.d1[0] / 64;
+        const uint32_t tph = lin_it & 1;
+        const bool lagged = nkb >= 2 * kLag + 1;
+        auto issue = [&](int st, int h, int kb) {
+          const uint32_t a_addr = smem_u32(smem + st * kStage) + h * kHalfBox;
+          const uint32_t b_addr = smem_u32(smem + st * kStage) + kAStage;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(tmem + h * 256, umma_desc_k_sw128(a_addr + kk * 32),
+                      umma_desc_k_sw128(b_addr + kk * 32), idesc_lin, (kb | kk) != 0);
+        };
+        mbar_wait(&tempty[0], tph ^ 1);
+        if (!lagged) mbar_wait(&tempty[1], tph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * 256;
-        for (int kb = 0; kb < k / 64; ++kb) {
+        const int s0 = stage;
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          const bool head = lagged && kb < kLag;
+          const bool tail = lagged && kb >= nkb - kLag;
           if (lane == 0) {
-            const uint32_t a_addr = smem_u32(smem + stage * kStage);
-            const uint32_t b_addr = a_addr + kAStage;
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d, umma_desc_k_sw128(a_addr + kk * 32), umma_desc_k_sw128(b_addr + kk * 32),
-                        idesc_lin, (kb | kk) != 0);
-            umma_commit(&empty_bar[stage]);
+            issue(stage, 0, kb);
+            if (!head && !tail) {
+              issue(stage, 1, kb);
+              umma_commit(&empty_bar[stage]);
+            }
           }
           __syncwarp();
+          if (lagged && kb == kLag - 1) {
+            mbar_wait(&tempty[1], tph ^ 1);
+            tc_fence_after();
+            if (lane == 0)
+              for (int j = 0; j < kLag; ++j) {
+                const int st = (s0 + j) % kRing;
+                issue(st, 1, j);
+                umma_commit(&empty_bar[st]);
+              }
+            __syncwarp();
+          }
           if (++stage == kRing) { stage = 0; phase ^= 1; }
         }
-        if (lane == 0) umma_commit(&tfull[acc]);
+        if (lane == 0) {
+          umma_commit(&tfull[0]);
+          if (lagged)
+            for (int j = nkb - kLag; j < nkb; ++j) {
+              const int st = (s0 + j) % kRing;
+              issue(st, 1, j);
+              umma_commit(&empty_bar[st]);
+            }
+          umma_commit(&tfull[1]);
+        }
         __syncwarp();
         ++lin_it;
       } else {
@@ -453,14 +501,15 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const int epi = __ldg(cfg + 4);
         const int out_slot = __ldg(cfg + 14);
         const int ntn = (n + 255) / 256;
-        const int r0 = (r.tile / ntn) * 128, c0 = (r.tile % ntn) * 256;
+        const int c0 = (r.tile % ntn) * 256;
         const int ldy = out_slot == 3 ? r.d1[3] : r.d1[2];
         uint16_t* y = reinterpret_cast<uint16_t*>(my_base + (out_slot == 3 ? r.off[3] : r.off[2]));
-        const int acc = lin_it & 1;
-        mbar_wait(&tfull[acc], (lin_it >> 1) & 1);
+#pragma unroll 1
+        for (int hf = 0; hf < 2; ++hf) {
+        mbar_wait(&tfull[hf], lin_it & 1);
         tc_fence_after();
-        const uint32_t t_acc = tmem + lane_off + acc * 256;
-        const int grow = r0 + row;
+        const uint32_t t_acc = tmem + lane_off + hf * 256;
+        const int grow = (r.tile / ntn) * 256 + hf * 128 + row;
         const bool row_ok = grow < m;
         if (epi == EPI_SILU_MUL) {
           // tile columns [0,128) = gate rows, [128,256) = matching up rows -> 128 outputs
@@ -525,7 +574,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) mbar_arrive(&tempty[hf]);
+        }
         ++lin_it;
       } else if (op == OP_ATTENTION) {
         const AttnGeom a = attn_geom(cfg, r);
@@ -642,6 +692,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           const uint16_t* g = reinterpret_cast<const uint16_t*>(my_base + r.off[1]);
           uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]);
           const int r0 = r.tile * br, r1 = min(r0 + br, rows);
+          prefetch_l2(x + static_cast<long long>(r0) * cols, static_cast<long long>(r1 - r0) * cols * 2, et, 128);
           constexpr int U = 8;
           for (int rr = r0 + ew; rr < r1; rr += 4) {
             const uint16_t* xr = x + static_cast<long long>(rr) * cols;
@@ -695,7 +746,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           const long long lo = static_cast<long long>(r0) * cols / 8, hi = static_cast<long long>(r1) * cols / 8;
           const uint4* res = reinterpret_cast<const uint4*>(my_base + r.off[1]);
           uint4* y = reinterpret_cast<uint4*>(my_base + r.off[2]);
-          constexpr int U = 4;
+          for (int pe = 0; pe < p.world; ++pe)
+            prefetch_l2(reinterpret_cast<const uint4*>(p.base[pe] + r.off[0]) + lo, (hi - lo) * 16, et, 128);
+          prefetch_l2(res + lo, (hi - lo) * 16, et, 128);
+          constexpr int U = 8;
           for (long long i0 = lo + et; i0 < hi; i0 += 128 * U) {
             float acc[U][8];
 #pragma unroll

@@ -47,7 +47,7 @@ if bfloat16 is not None:
 LAYER_OP_CODES = {"rmsnorm": 1, "linear": 2, "attention": 3, "allreduce_residual": 4}
 EPILOGUES = {"none": 0, "rope": 1, "silu_mul": 2}
 HEAD_DIM = 128
-BLOCK_M, BLOCK_N = 128, 256
+BLOCK_M, BLOCK_N = 256, 256
 CFG_INTS = 16
 
 
@@ -61,7 +61,8 @@ def _f32_bits(v: float) -> int:
 
 # ---------------------------------------------------------------------- planners
 def plan_linear_bf16(io, config) -> MK.LayerPlan:
-    """bf16 linear: y[m, n] = x[m, k] . w[n, k]^T on 128 x 256 tcgen05 tiles.
+    """bf16 linear: y[m, n] = x[m, k] . w[n, k]^T on 256 x 256 tiles (two tcgen05
+    M=128 x N=256 halves sharing each B stage).
     epilogue "rope": third input = rope table [seq, 128] fp32 (cos | sin), RoPE on
     output columns [0, rope_cols); "silu_mul": w rows interleaved per 128 (gate
     block, up block), y[m, n/2] = silu(gate) * up."""
@@ -71,7 +72,7 @@ def plan_linear_bf16(io, config) -> MK.LayerPlan:
     n, wk = w.shape
     cfg = {"block_m": BLOCK_M, "block_n": BLOCK_N, "block_k": 64, "epilogue": "none", **config}
     if (cfg["block_m"], cfg["block_n"]) != (BLOCK_M, BLOCK_N):
-        raise BuildError("bf16 linear tiles are 128 x 256 (tcgen05 M=128, N=256)")
+        raise BuildError("bf16 linear tiles are 256 x 256 (two tcgen05 M=128, N=256 halves)")
     epi = cfg["epilogue"]
     if epi not in EPILOGUES:
         raise BuildError(f"unknown linear epilogue {epi!r}")
@@ -225,7 +226,7 @@ def layer_tables(program: MK.MegaProgram, built: MK.BuiltGraph):
             n = w.shape[0]
             row[1], row[2] = BLOCK_M, BLOCK_N
             row[4] = EPILOGUES[c["epilogue"]]
-            row[5] = map_id((x.offset, 2, k, m, 0, 64, BLOCK_M, 0))
+            row[5] = map_id((x.offset, 2, k, m, 0, 64, 128, 0))
             row[6] = map_id((w.offset, 2, k, n, 0, 64, BLOCK_N, 0))
             if c["epilogue"] == "rope":
                 row[9] = ins[2].shape[0]
