@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-attn", action="store_true")
     p.add_argument("--no-layer", action="store_true")
     p.add_argument("--only-layer", action="store_true")
+    p.add_argument("--only-attn", action="store_true")
     return p.parse_args()
 
 
@@ -427,6 +428,10 @@ def main_ours(args):
     from paper_2605_02953_b200 import kernels as K
     from paper_2605_02953_b200.shmem import Team
 
+    if args.only_attn:  # probe: config 3 only
+        torch.cuda.set_device(0)
+        print(json.dumps(bench_attention(0, max(args.steps, 3), load_peaks()[0])), flush=True)
+        return
     if args.only_layer:  # probe: config 5 only
         torch.cuda.set_device(0)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")

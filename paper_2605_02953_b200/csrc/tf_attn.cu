@@ -9,17 +9,19 @@
 // head); it walks the key tiles starting at its own chunk (gather order) and
 // acquire-waits a chunk's flag before its first TMA load of that chunk.
 //
-// Per CTA (192 threads):
-//   warp 0      TMA: Q tile once, then K/V tiles (128 keys x 128 dims each) into a
-//               2-stage ring.
-//   warp 1      MMA (one lane): S_j = Q K_j^T (M=128, N=128, K=d) into a
-//               double-buffered TMEM S; O += P_j V_j (A = P from smem, K-major;
-//               B = V from smem, MN-major) into TMEM O.
-//   warps 2-5   softmax, one query row per thread: S row from TMEM, online
-//               max/sum in fp32 (exp2 with the scale folded in), O row rescaled
-//               in TMEM when the max grows, P row written to smem as bf16
-//               (128-byte swizzled K-major), final O / l stored as bf16.
-// TMEM: S0 [0,128), S1 [128,256), O [256,384) fp32 columns.
+// Per CTA (320 threads, two 128-query tiles A and B of one head):
+//   warp 0      TMA: Q_A and Q_B once, then K_j and V_j (128 keys x 128 dims each)
+//               through a 3-slot ring (K0 V0 K1 V1 ...).
+//   warp 1      MMA (one lane): S_t = Q_t K_j^T (M=128, N=128, K=d) for t = A, B,
+//               then O_t += P_t V_j (A = P_t from smem, K-major; B = V from smem,
+//               MN-major).
+//   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B, one query row per
+//               thread: S row from TMEM, online max/sum in fp32 (ex2.approx with
+//               the scale folded into an FFMA), lazy rescale -- the running max
+//               may lag the true max by up to 2^8 before O is rescaled in TMEM --
+//               P row to smem as bf16 (128-byte swizzled K-major), O / l as bf16.
+// While one warpgroup is on the ALUs/SFU the tensor pipe works on the other
+// tile's QK^T and PV.  TMEM: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -33,11 +35,10 @@
 namespace tf {
 namespace {
 
-constexpr int kQT = 128;      // queries per CTA
+constexpr int kQT = 128;      // queries per tile (two tiles per CTA)
 constexpr int kKT = 128;      // keys per tile
 constexpr int kD = 128;       // head dim (fixed for this kernel)
 constexpr int kHalf = 16384;  // one 128-row x 64-col bf16 box (128-byte rows)
-constexpr int kAttnThreads = 192;
 
 struct AttnParams {
   int s_local, s_total, hq, hkv;
@@ -52,14 +53,19 @@ struct AttnParams {
   unsigned long long timeout_ns;
 };
 
+// Two 128-query tiles (A, B) per CTA share every K/V tile; each has its own
+// softmax warpgroup, S and O in TMEM, and P buffer in smem, so the tensor pipe
+// runs one tile's QK^T / PV while the other tile's softmax is on the ALUs.
 struct AttnSmem {
-  static constexpr int kQ = 2 * kHalf;        // 32 KB
-  static constexpr int kKV = 4 * kHalf;       // K (2 halves) + V (2 halves) = 64 KB
-  static constexpr int kStages = 2;
-  static constexpr int kP = 2 * kHalf;        // 32 KB
+  static constexpr int kQ = 2 * kHalf;        // one Q tile, 32 KB
+  static constexpr int kSlot = 2 * kHalf;     // one K or V tile (128 keys x 128 dims), 32 KB
+  static constexpr int kSlots = 3;            // ring K0 V0 K1 V1 ...
+  static constexpr int kP = 2 * kHalf;        // one P tile, 32 KB
   static constexpr int kBars = 256;
-  static constexpr int kTotal = 1024 + kQ + kStages * kKV + kP + kBars;
+  static constexpr int kTotal = 1024 + 2 * kQ + kSlots * kSlot + 2 * kP + kBars;
 };
+constexpr int kAttnThreads2 = 320;            // TMA, MMA, 2 x 4 softmax warps
+constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag (FA4)
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
                                             int32_t c0, int32_t c1, int32_t c2) {
@@ -98,60 +104,69 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __maxnreg__(168)
     ag_attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ AttnParams p) {
   using S = AttnSmem;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sq = smem;
-  uint8_t* skv = sq + S::kQ;                 // stage s: K at s*kKV, V at s*kKV + 2*kHalf
-  uint8_t* sp = skv + S::kStages * S::kKV;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + S::kP);
+  uint8_t* sq = smem;                               // Q_A, Q_B
+  uint8_t* sring = sq + 2 * S::kQ;                  // 3 slots
+  uint8_t* sp = sring + S::kSlots * S::kSlot;       // P_A, P_B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * S::kP);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;    // [2]
-  uint64_t* kv_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* s_empty = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* r_full = bars + 1;     // [3]
+  uint64_t* r_empty = bars + 4;    // [3]
+  uint64_t* s_full = bars + 7;     // [2] per Q tile
+  uint64_t* s_empty = bars + 9;    // [2]
+  uint64_t* p_full = bars + 11;    // [2]
+  uint64_t* p_free = bars + 13;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q_tile = blockIdx.x;
+  const int q0 = blockIdx.x * 2 * kQT;
+  const bool has_b = q0 + kQT < p.s_local;
+  const int nq = has_b ? 2 : 1;
   const int h = blockIdx.y;
   const int g = h / (p.hq / p.hkv);
   const int n = p.n_tiles;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_free[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem + 256;
+  const uint32_t tmem = *tmem_slot;  // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, S::kQ);
-      tma_load_3d(sq, &tq, q_full, 0, h, q_tile * kQT);
-      tma_load_3d(sq + kHalf, &tq, q_full, 64, h, q_tile * kQT);
+      mbar_arrive_expect_tx(q_full, nq * S::kQ);
+      for (int t = 0; t < nq; ++t) {
+        tma_load_3d(sq + t * S::kQ, &tq, q_full, 0, h, q0 + t * kQT);
+        tma_load_3d(sq + t * S::kQ + kHalf, &tq, q_full, 64, h, q0 + t * kQT);
+      }
       uint32_t ready = 0;
       for (int j = 0; j < n; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
         const int chunk = kt / p.tiles_per_chunk;
         if (p.chunk_flags && !(ready & (1u << chunk))) {
@@ -160,144 +175,165 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           fence_proxy_async_global();
           ready |= 1u << chunk;
         }
-        uint8_t* kb = skv + st * S::kKV;
-        mbar_arrive_expect_tx(&kv_full[st], S::kKV);
-        tma_load_3d(kb, &tk, &kv_full[st], 0, g, kt * kKT);
-        tma_load_3d(kb + kHalf, &tk, &kv_full[st], 64, g, kt * kKT);
-        tma_load_3d(kb + 2 * kHalf, &tv, &kv_full[st], 0, g, kt * kKT);
-        tma_load_3d(kb + 3 * kHalf, &tv, &kv_full[st], 64, g, kt * kKT);
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {           // K_j then V_j
+          const int c = 2 * j + kv, sl = c % 3;
+          mbar_wait(&r_empty[sl], ((c / 3) & 1) ^ 1);
+          uint8_t* dst = sring + sl * S::kSlot;
+          const CUtensorMap* m = kv ? &tv : &tk;
+          mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
+          tma_load_3d(dst, m, &r_full[sl], 0, g, kt * kKT);
+          tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, kt * kKT);
+        }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(kQT, kKT);                    // K-major A and B
-    constexpr uint32_t idesc_pv = umma_idesc_bf16(kQT, kD) | (1u << 16);      // B (V) MN-major
+    constexpr uint32_t idesc_s = umma_idesc_bf16(kQT, kKT);
+    constexpr uint32_t idesc_pv = umma_idesc_bf16(kQT, kD) | (1u << 16);  // B (V) MN-major
     mbar_wait(q_full, 0);
     tc_fence_after();
     auto issue_pv = [&](int jj) {
-      const int st = jj & 1;
-      mbar_wait(p_full, jj & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t pa = smem_u32(sp);
-        const uint32_t vb = smem_u32(skv + st * S::kKV + 2 * kHalf);
+      const int c = 2 * jj + 1, sl = c % 3;
+      mbar_wait(&r_full[sl], (c / 3) & 1);
+      for (int t = 0; t < nq; ++t) {
+        mbar_wait(&p_full[t], jj & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t pa = smem_u32(sp + t * S::kP);
+          const uint32_t vb = smem_u32(sring + sl * S::kSlot);
 #pragma unroll
-        for (int kk = 0; kk < kKT / 16; ++kk) {
-          const uint64_t ad = umma_desc_k_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32);
-          const uint64_t bd = umma_desc_mn_sw128(vb + kk * 2048, kHalf);
-          umma_bf16(t_o, ad, bd, idesc_pv, (jj | kk) != 0);
+          for (int kk = 0; kk < kKT / 16; ++kk)
+            umma_bf16(tmem + 256 + t * 128, umma_desc_k_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32),
+                      umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (jj | kk) != 0);
+          umma_commit(&p_free[t]);
         }
-        umma_commit(&kv_empty[st]);
-        umma_commit(pv_done);
+        __syncwarp();
       }
+      if (lane == 0) umma_commit(&r_empty[sl]);
       __syncwarp();
     };
     for (int j = 0; j < n; ++j) {
-      const int st = j & 1;
-      mbar_wait(&kv_full[st], (j >> 1) & 1);
-      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t qa = smem_u32(sq);
-        const uint32_t kb = smem_u32(skv + st * S::kKV);
+      const int c = 2 * j, sl = c % 3;
+      mbar_wait(&r_full[sl], (c / 3) & 1);
+      for (int t = 0; t < nq; ++t) {
+        mbar_wait(&s_empty[t], (j & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t qa = smem_u32(sq + t * S::kQ);
+          const uint32_t kb = smem_u32(sring + sl * S::kSlot);
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          umma_bf16(tmem + st * kKT, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off),
-                    idesc_s, kk != 0);
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+            umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off), idesc_s,
+                      kk != 0);
+          }
+          umma_commit(&s_full[t]);
         }
-        umma_commit(&s_full[st]);
+        __syncwarp();
       }
+      if (lane == 0) umma_commit(&r_empty[sl]);
       __syncwarp();
       if (j > 0) issue_pv(j - 1);
     }
     issue_pv(n - 1);
   } else {
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    uint8_t* prow = sp + row * 128;
-    for (int j = 0; j < n; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + lane_off + st * kKT + c * 32, sv[c]);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[st]);
-      float mx = m;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sv[c][i]) * p.scale_log2);
-      const float alpha = exp2f(m - mx);  // 0 on the first tile (m = -inf)
-      float sum = 0.f;
-      uint32_t pk[4][16];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float p0 = exp2f(__uint_as_float(sv[c][2 * i]) * p.scale_log2 - mx);
-          const float p1 = exp2f(__uint_as_float(sv[c][2 * i + 1]) * p.scale_log2 - mx);
-          sum += p0 + p1;
-          pk[c][i] = pack_bf16x2(p0, p1);
-        }
-      l = l * alpha + sum;
-      m = mx;
-      if (j > 0) {
-        // P buffer and O are free once P_{j-1} V_{j-1} has completed
-        mbar_wait(pv_done, (j - 1) & 1);
+    const int t = (warp - 2) >> 2;                 // Q tile of this warpgroup
+    if (t < nq) {
+      const int quarter = warp & 3;
+      const int row = quarter * 32 + lane;
+      const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+      const uint32_t t_s = tmem + lane_off + t * 128;
+      const uint32_t t_o = tmem + lane_off + 256 + t * 128;
+      float m = -INFINITY, l = 0.f;
+      uint8_t* prow = sp + t * S::kP + row * 128;
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(&s_full[t], j & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha < 1.f)) {
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t ov[32];
-            tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
-            tmem_ld_wait();
+        uint32_t sv[4][32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st_32x32b_x32(t_o + lane_off + c * 32, ov);
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[t]);
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            mx0 = fmaxf(mx0, __uint_as_float(sv[c][i]));
+            mx1 = fmaxf(mx1, __uint_as_float(sv[c][i + 1]));
           }
-          tmem_st_wait();
+        const float mt = fmaxf(mx0, mx1) * p.scale_log2;
+        // lazy rescale: keep a stale running max unless the new one exceeds it by > 8
+        float alpha = 1.f;
+        if (mt > m + kLazyRescale) {
+          alpha = ex2(m - mt);
+          m = mt;
         }
-      }
-      // P row -> smem, 128-byte swizzled K-major (halves of 64 keys, 16 KB apart)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = c * 4 + q;            // 16-byte chunk of the 256-byte row
-          const int half = chunk >> 3, jj = chunk & 7;
-          *reinterpret_cast<uint4*>(prow + half * kHalf + ((jj ^ (row & 7)) << 4)) =
-              make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
-        }
-      fence_proxy_async_shared();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    // epilogue: O / l -> bf16 [q, h, :]
-    mbar_wait(pv_done, (n - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const int q = q_tile * kQT + row;
-    uint16_t* dst = static_cast<uint16_t*>(p.out) + (static_cast<long long>(q) * p.hq + h) * kD;
+        if (j > 0) {
+          // P buffer and O_t are free once P_{j-1} V_{j-1} has completed
+          mbar_wait(&p_free[t], (j - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t ov[32];
-      tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
-      tmem_ld_wait();
-      if (q < p.s_local) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+            for (int c = 0; c < 4; ++c) {
+              uint32_t ov[32];
+              tmem_ld_32x32b_x32(t_o + c * 32, ov);
+              tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
-                             pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
-                             pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
-                             pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st_32x32b_x32(t_o + c * 32, ov);
+            }
+            tmem_st_wait();
+          }
+        }
+        // P row -> smem chunk by chunk (128-byte swizzled K-major, halves of 64 keys)
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m));
+            const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m));
+            s0 += p0;
+            s1 += p1;
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = c * 4 + q;
+            const int half = chunk >> 3, jj = chunk & 7;
+            *reinterpret_cast<uint4*>(prow + half * kHalf + ((jj ^ (row & 7)) << 4)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        }
+        l = l * alpha + (s0 + s1);
+        fence_proxy_async_shared();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+      mbar_wait(&p_free[t], (n - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const int q = q0 + t * kQT + row;
+      uint16_t* dst = static_cast<uint16_t*>(p.out) + (static_cast<long long>(q) * p.hq + h) * kD;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ov[32];
+        tmem_ld_32x32b_x32(t_o + c * 32, ov);
+        tmem_ld_wait();
+        if (q < p.s_local) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            d4[i] = make_uint4(pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+        }
       }
     }
   }
@@ -432,9 +468,19 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
                                        tf::AttnSmem::kTotal));
       attr_done |= 1ull << dev;
     }
-    dim3 grid(static_cast<unsigned>(sl / tf::kQT), static_cast<unsigned>(a->hq));
-    tf::ag_attn_fwd_kernel<<<grid, tf::kAttnThreads, tf::AttnSmem::kTotal, s>>>(tq, tk, tv, p);
-    TF_CUDA_TRY(cudaGetLastError());
+    dim3 grid(static_cast<unsigned>((sl + 2 * tf::kQT - 1) / (2 * tf::kQT)), static_cast<unsigned>(a->hq));
+    tf::ag_attn_fwd_kernel<<<grid, tf::kAttnThreads2, tf::AttnSmem::kTotal, s>>>(tq, tk, tv, p);
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, tf::ag_attn_fwd_kernel);
+      return fail(TF_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(le) +
+                                   " (regs " + std::to_string(fa.numRegs) + ", max threads " +
+                                   std::to_string(fa.maxThreadsPerBlock) + ", static smem " +
+                                   std::to_string(fa.sharedSizeBytes) + ", max dyn smem " +
+                                   std::to_string(fa.maxDynamicSharedSizeBytes) + ", dyn " +
+                                   std::to_string(tf::AttnSmem::kTotal) + ")");
+    }
     if (w > 1 && cs != s) {
       cudaEvent_t ev;
       TF_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
