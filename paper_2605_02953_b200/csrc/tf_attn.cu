@@ -100,8 +100,38 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+
+// position of K_j (kv = 0) / V_j (kv = 1) in the ring's load sequence K0 K1 V0 K2 V1 ...
+__device__ __forceinline__ int ring_index(int j, int kv, int n) {
+  if (!kv) return j == 0 ? 0 : 2 * j - 1;
+  return j <= n - 2 ? 2 * j + 2 : 2 * n - 1;
+}
+__device__ __forceinline__ void ring_decode(int c, int n, int& j, int& kv) {
+  if (c == 0) { j = 0; kv = 0; return; }
+  if (c == 2 * n - 1) { j = n - 1; kv = 1; return; }
+  if (c & 1) { j = (c + 1) / 2; kv = 0; } else { j = (c - 2) / 2; kv = 1; }
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -165,26 +195,27 @@ __global__ void __maxnreg__(168)
         tma_load_3d(sq + t * S::kQ, &tq, q_full, 0, h, q0 + t * kQT);
         tma_load_3d(sq + t * S::kQ + kHalf, &tq, q_full, 64, h, q0 + t * kQT);
       }
+      // load order K0 K1 V0 K2 V1 ... K_{n-1} V_{n-2} V_{n-1}: K runs one tile ahead, so a
+      // slot is refilled two MMA steps before it is consumed (hides the TMA latency)
       uint32_t ready = 0;
-      for (int j = 0; j < n; ++j) {
+      for (int c = 0; c < 2 * n; ++c) {
+        int j, kv;
+        ring_decode(c, n, j, kv);
         const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
         const int chunk = kt / p.tiles_per_chunk;
-        if (p.chunk_flags && !(ready & (1u << chunk))) {
+        if (!kv && p.chunk_flags && !(ready & (1u << chunk))) {
           wait_geq_sys(p.chunk_flags + chunk, p.epoch, p.timeout_ns, p.err,
                        0x1000000ull | static_cast<unsigned>(chunk));
           fence_proxy_async_global();
           ready |= 1u << chunk;
         }
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {           // K_j then V_j
-          const int c = 2 * j + kv, sl = c % 3;
-          mbar_wait(&r_empty[sl], ((c / 3) & 1) ^ 1);
-          uint8_t* dst = sring + sl * S::kSlot;
-          const CUtensorMap* m = kv ? &tv : &tk;
-          mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
-          tma_load_3d(dst, m, &r_full[sl], 0, g, kt * kKT);
-          tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, kt * kKT);
-        }
+        const int sl = c % 3;
+        mbar_wait(&r_empty[sl], ((c / 3) & 1) ^ 1);
+        uint8_t* dst = sring + sl * S::kSlot;
+        const CUtensorMap* m = kv ? &tv : &tk;
+        mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
+        tma_load_3d(dst, m, &r_full[sl], 0, g, kt * kKT);
+        tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, kt * kKT);
       }
     }
   } else if (warp == 1) {
@@ -193,7 +224,7 @@ __global__ void __maxnreg__(168)
     mbar_wait(q_full, 0);
     tc_fence_after();
     auto issue_pv = [&](int jj) {
-      const int c = 2 * jj + 1, sl = c % 3;
+      const int c = ring_index(jj, 1, n), sl = c % 3;
       mbar_wait(&r_full[sl], (c / 3) & 1);
       for (int t = 0; t < nq; ++t) {
         mbar_wait(&p_full[t], jj & 1);
@@ -213,7 +244,7 @@ __global__ void __maxnreg__(168)
       __syncwarp();
     };
     for (int j = 0; j < n; ++j) {
-      const int c = 2 * j, sl = c % 3;
+      const int c = ring_index(j, 0, n), sl = c % 3;
       mbar_wait(&r_full[sl], (c / 3) & 1);
       for (int t = 0; t < nq; ++t) {
         mbar_wait(&s_empty[t], (j & 1) ^ 1);
@@ -271,45 +302,46 @@ __global__ void __maxnreg__(168)
           alpha = ex2(m - mt);
           m = mt;
         }
-        if (j > 0) {
-          // P buffer and O_t are free once P_{j-1} V_{j-1} has completed
-          mbar_wait(&p_free[t], (j - 1) & 1);
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-              uint32_t ov[32];
-              tmem_ld_32x32b_x32(t_o + c * 32, ov);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-              tmem_st_32x32b_x32(t_o + c * 32, ov);
-            }
-            tmem_st_wait();
-          }
-        }
-        // P row -> smem chunk by chunk (128-byte swizzled K-major, halves of 64 keys)
+        // exponentials into registers first: they overlap P_{j-1} V_{j-1} on the tensor pipe
         float s0 = 0.f, s1 = 0.f;
+        uint32_t pk[4][16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m));
             const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m));
             s0 += p0;
             s1 += p1;
-            pk[i] = pack_bf16x2(p0, p1);
+            pk[c][i] = pack_bf16x2(p0, p1);
           }
+        l = l * alpha + (s0 + s1);
+        if (j > 0) {
+          // P buffer and O_t are free once P_{j-1} V_{j-1} has completed
+          mbar_wait(&p_free[t], (j - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              uint32_t ov[16];
+              tmem_ld_32x32b_x16(t_o + c * 16, ov);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st_32x32b_x16(t_o + c * 16, ov);
+            }
+            tmem_st_wait();
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int chunk = c * 4 + q;
             const int half = chunk >> 3, jj = chunk & 7;
             *reinterpret_cast<uint4*>(prow + half * kHalf + ((jj ^ (row & 7)) << 4)) =
-                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
           }
-        }
-        l = l * alpha + (s0 + s1);
         fence_proxy_async_shared();
         tc_fence_before();
         __syncwarp();
