@@ -15,7 +15,8 @@
 //                                         lags 2 k-blocks at tile    tile flag
 //                                         edges (drain overlaps)
 //   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
-//                 tiles (2 stages)        (V MN-major)               mask), O / l -> bf16
+//                 tiles through a 4-slot  (V MN-major)               mask, lazy rescale),
+//                 ring, K one tile ahead                             O / l -> bf16
 //   rmsnorm       -                       -                          wait deps, y = x*rstd*g
 //   allreduce_    -                       -                          wait deps on every PE,
 //   residual                                                         y = sum_pe x_pe + res (P2P)
@@ -52,9 +53,11 @@ constexpr int kStage = kAStage + kBStage;     // 64 KB
 constexpr int kRegion = kRing * kStage;       // 192 KB
 constexpr int kLag = 2;                       // k-blocks the second M-half trails at tile edges
 constexpr int kQOff = 0;                      // attention aliases
-constexpr int kKVOff = 2 * kHalfBox;          // 2 stages x (K 32 KB + V 32 KB)
-constexpr int kKVStage = 4 * kHalfBox;
-constexpr int kPOff = kKVOff + 2 * kKVStage;  // 160 KB
+constexpr int kKVOff = 2 * kHalfBox;          // ring of 4 K-or-V slots (32 KB each)
+constexpr int kKVSlot = 2 * kHalfBox;
+constexpr int kKVSlots = 4;
+constexpr int kPOff = kKVOff + kKVSlots * kKVSlot;  // 160 KB
+constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag before O is rescaled
 constexpr int kLayerSmem = 1024 + kRegion + 512;
 constexpr int kCfgInts = 16;
 constexpr int kIntPerTask = 30;
@@ -156,6 +159,24 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr, long long bytes, in
   }
 }
 
+// position of K_j (kv = 0) / V_j (kv = 1) in a task's load sequence K0 K1 V0 K2 V1 ... K_{n-1}
+// V_{n-2} V_{n-1}: K runs one tile ahead so slots refill two MMA steps before use
+__device__ __forceinline__ int ring_index(int j, int kv, int n) {
+  if (!kv) return j == 0 ? 0 : 2 * j - 1;
+  return j <= n - 2 ? 2 * j + 2 : 2 * n - 1;
+}
+__device__ __forceinline__ void ring_decode(int c, int n, int& j, int& kv) {
+  if (c == 0) { j = 0; kv = 0; return; }
+  if (c == 2 * n - 1) { j = n - 1; kv = 1; return; }
+  if (c & 1) { j = (c + 1) / 2; kv = 0; } else { j = (c - 2) / 2; kv = 1; }
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ unsigned long long* trace_at(const LayerParams& p, int idx) {
   return p.trace + (static_cast<long long>(blockIdx.x) * p.slots + idx) * 4;
 }
@@ -244,8 +265,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
   uint64_t* tempty = bars + 10;         // [2]
   uint64_t* q_full = bars + 12;
   uint64_t* q_empty = bars + 13;
-  uint64_t* kv_full = bars + 14;        // [2]
-  uint64_t* kv_empty = bars + 16;       // [2]
+  uint64_t* kv_full = bars + 28;        // [4] ring slots
+  uint64_t* kv_empty = bars + 32;       // [4]
   uint64_t* s_full = bars + 18;         // [2]
   uint64_t* s_empty = bars + 20;        // [2]
   uint64_t* p_full = bars + 22;
@@ -267,10 +288,12 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
+    }
+    for (int i = 0; i < kKVSlots; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
     }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
@@ -291,7 +314,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     // =========================================================== TMA producer
     int stage = 0;
     uint32_t phase = 0;
-    int kv_it = 0, att_it = 0;
+    int kv_it = 0, att_it = 0, ring_base = 0;
     for (int idx = 0; idx < n_tasks; ++idx) {
       Rec r;
       load_rec(p, idx, sm, r);
@@ -338,20 +361,22 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           mbar_arrive_expect_tx(q_full, 2 * kHalfBox);
           tma_load_3d_l(smem + kQOff, mq, q_full, 0, a.h, a.q_row0);
           tma_load_3d_l(smem + kQOff + kHalfBox, mq, q_full, 64, a.h, a.q_row0);
-          for (int j = 0; j < a.n_kv; ++j) {
-            const int gi = kv_it + j, st = gi & 1;
-            mbar_wait(&kv_empty[st], ((gi >> 1) & 1) ^ 1);
-            uint8_t* kb = smem + kKVOff + st * kKVStage;
+          for (int c = 0; c < 2 * a.n_kv; ++c) {
+            int j, kv;
+            ring_decode(c, a.n_kv, j, kv);
+            const int gc = ring_base + c, sl = gc % kKVSlots;
+            mbar_wait(&kv_empty[sl], ((gc / kKVSlots) & 1) ^ 1);
+            uint8_t* dst = smem + kKVOff + sl * kKVSlot;
             const int row = (a.kv0 + j) * 128;
-            mbar_arrive_expect_tx(&kv_full[st], kKVStage);
-            tma_load_3d_l(kb, mq, &kv_full[st], 0, a.hq + a.g, row);
-            tma_load_3d_l(kb + kHalfBox, mq, &kv_full[st], 64, a.hq + a.g, row);
-            tma_load_3d_l(kb + 2 * kHalfBox, mq, &kv_full[st], 0, a.hq + a.hkv + a.g, row);
-            tma_load_3d_l(kb + 3 * kHalfBox, mq, &kv_full[st], 64, a.hq + a.hkv + a.g, row);
+            const int head = a.hq + kv * a.hkv + a.g;
+            mbar_arrive_expect_tx(&kv_full[sl], kKVSlot);
+            tma_load_3d_l(dst, mq, &kv_full[sl], 0, head, row);
+            tma_load_3d_l(dst + kHalfBox, mq, &kv_full[sl], 64, head, row);
           }
         }
         __syncwarp();
         kv_it += a.n_kv;
+        ring_base += 2 * a.n_kv;
         ++att_it;
       }
     }
@@ -359,7 +384,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     // =========================================================== MMA issuer
     int stage = 0;
     uint32_t phase = 0;
-    int lin_it = 0, kv_it = 0, att_it = 0;
+    int lin_it = 0, kv_it = 0, att_it = 0, ring_base = 0;
     constexpr uint32_t idesc_lin = umma_idesc_bf16(128, 256);
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);  // B (V) MN-major
@@ -438,12 +463,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         mbar_wait(o_empty, (att_it & 1) ^ 1);
         tc_fence_after();
         auto issue_pv = [&](int gi, int jl) {
-          const int st = gi & 1;
+          const int gc = ring_base + ring_index(jl, 1, n), st = gc % kKVSlots;
+          mbar_wait(&kv_full[st], (gc / kKVSlots) & 1);
           mbar_wait(p_full, gi & 1);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = smem_u32(smem + kPOff);
-            const uint32_t vb = smem_u32(smem + kKVOff + st * kKVStage + 2 * kHalfBox);
+            const uint32_t vb = smem_u32(smem + kKVOff + st * kKVSlot);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
               umma_bf16(t_o, umma_desc_k_sw128(pa + (kk >> 2) * kHalfBox + (kk & 3) * 32),
@@ -455,12 +481,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         };
         for (int j = 0; j < n; ++j) {
           const int gi = kv_it + j, st = gi & 1;
-          mbar_wait(&kv_full[st], (gi >> 1) & 1);
+          const int gc = ring_base + ring_index(j, 0, n), ks = gc % kKVSlots;
+          mbar_wait(&kv_full[ks], (gc / kKVSlots) & 1);
           mbar_wait(&s_empty[st], ((gi >> 1) & 1) ^ 1);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t qa = smem_u32(smem + kQOff);
-            const uint32_t kb = smem_u32(smem + kKVOff + st * kKVStage);
+            const uint32_t kb = smem_u32(smem + kKVOff + ks * kKVSlot);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t off = (kk >> 2) * kHalfBox + (kk & 3) * 32;
@@ -468,6 +495,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
                         idesc_s, kk != 0);
             }
             umma_commit(&s_full[st]);
+            umma_commit(&kv_empty[ks]);
             if (j == n - 1) umma_commit(q_empty);
           }
           __syncwarp();
@@ -475,6 +503,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         }
         issue_pv(kv_it + n - 1, n - 1);
         kv_it += n;
+        ring_base += 2 * n;
         ++att_it;
       }
     }
@@ -597,34 +626,40 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_empty[st]);
           const bool diag = causal && j == n - 1;
-          float mx = mrow;
+          float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              float s = __uint_as_float(sv[c][i]) * scale_log2;
-              if (diag && c * 32 + i > row) s = -INFINITY;
-              sv[c][i] = __float_as_uint(s);
-              mx = fmaxf(mx, s);
+            for (int i = 0; i < 32; i += 2) {
+              if (diag && c * 32 + i > row) sv[c][i] = __float_as_uint(-INFINITY);
+              if (diag && c * 32 + i + 1 > row) sv[c][i + 1] = __float_as_uint(-INFINITY);
+              mx0 = fmaxf(mx0, __uint_as_float(sv[c][i]));
+              mx1 = fmaxf(mx1, __uint_as_float(sv[c][i + 1]));
             }
-          const float alpha = exp2f(mrow - mx);
-          float sum = 0.f;
+          const float mt = fmaxf(mx0, mx1) * scale_log2;
+          // lazy rescale: the running max may lag the true max by up to 2^8
+          float alpha = 1.f;
+          if (mt > mrow + kLazyRescale) {
+            alpha = ex2(mrow - mt);
+            mrow = mt;
+          }
+          float s0 = 0.f, s1 = 0.f;
           uint32_t pk[4][16];
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float p0 = exp2f(__uint_as_float(sv[c][2 * i]) - mx);
-              const float p1 = exp2f(__uint_as_float(sv[c][2 * i + 1]) - mx);
-              sum += p0 + p1;
+              const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -mrow));
+              const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -mrow));
+              s0 += p0;
+              s1 += p1;
               pk[c][i] = pack_bf16x2(p0, p1);
             }
-          l = l * alpha + sum;
-          mrow = mx;
+          l = l * alpha + (s0 + s1);
           if (j > 0) {
             mbar_wait(pv_done, (gi - 1) & 1);
             tc_fence_after();
-            if (__any_sync(0xffffffffu, alpha < 1.f)) {
+            if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
               for (int c = 0; c < 4; ++c) {
                 uint32_t ov[32];
@@ -738,9 +773,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
                 }
             }
           }
-        } else if (op == OP_ALLREDUCE_RES) {
+        } else if (op == OP_ALLREDUCE_RES && __ldg(cfg + 15) == 0) {
           // y = (x_0 + x_1 + ... + x_{w-1}) + res, fp32 in ascending PE order, bf16 out;
-          // 4 chunks of 8 elements per thread per round (loads of all PEs in flight)
+          // 8 chunks of 8 elements per thread per round (loads of all PEs in flight)
           const int rows = r.d0[0], cols = r.d1[0];
           const int r0 = r.tile * br, r1 = min(r0 + br, rows);
           const long long lo = static_cast<long long>(r0) * cols / 8, hi = static_cast<long long>(r1) * cols / 8;
@@ -783,6 +818,89 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
                   o[e] = pack_bf16x2(acc[u][2 * e] + bf16lo(w[e]), acc[u][2 * e + 1] + bf16hi(w[e]));
                 y[i] = make_uint4(o[0], o[1], o[2], o[3]);
               }
+            }
+          }
+        } else if (op == OP_ALLREDUCE_RES) {
+          // fused with the following RMSNorm: one warp per row, y = sum_pe x_pe + res
+          // (fp32, ascending PE, bf16), then yn = y * rsqrt(mean(y^2) + eps) * g
+          const int rows = r.d0[0], cols = r.d1[0];
+          const int r0 = r.tile * br, r1 = min(r0 + br, rows);
+          const float eps = __int_as_float(__ldg(cfg + 11));
+          const uint16_t* g = reinterpret_cast<const uint16_t*>(
+              my_base + (static_cast<long long>(__ldg(cfg + 15) - 1) << 4));
+          const long long lo = static_cast<long long>(r0) * cols, n_el = static_cast<long long>(r1 - r0) * cols;
+          for (int pe = 0; pe < p.world; ++pe)
+            prefetch_l2(reinterpret_cast<const uint16_t*>(p.base[pe] + r.off[0]) + lo, n_el * 2, et, 128);
+          prefetch_l2(reinterpret_cast<const uint16_t*>(my_base + r.off[1]) + lo, n_el * 2, et, 128);
+          constexpr int U = 4;
+          for (int rr = r0 + ew; rr < r1; rr += 4) {
+            const long long rb = static_cast<long long>(rr) * cols;
+            const uint16_t* res = reinterpret_cast<const uint16_t*>(my_base + r.off[1]) + rb;
+            uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]) + rb;
+            uint16_t* yn = reinterpret_cast<uint16_t*>(my_base + r.off[3]) + rb;
+            float ss = 0.f;
+            for (int c0 = lane * 8; c0 < cols; c0 += 256 * U) {
+              float acc[U][8];
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+              for (int pe = 0; pe < p.world; ++pe) {
+                const uint16_t* src = reinterpret_cast<const uint16_t*>(p.base[pe] + r.off[0]) + rb;
+                uint4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                  v[u] = c0 + u * 256 < cols ? *reinterpret_cast<const uint4*>(src + c0 + u * 256)
+                                             : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                  const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    acc[u][2 * e] += bf16lo(w[e]);
+                    acc[u][2 * e + 1] += bf16hi(w[e]);
+                  }
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int c = c0 + u * 256;
+                if (c < cols) {
+                  const uint4 rv = *reinterpret_cast<const uint4*>(res + c);
+                  const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+                  uint32_t o[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    o[e] = pack_bf16x2(acc[u][2 * e] + bf16lo(w[e]), acc[u][2 * e + 1] + bf16hi(w[e]));
+                    const float a0 = bf16lo(o[e]), a1 = bf16hi(o[e]);
+                    ss += a0 * a0 + a1 * a1;
+                  }
+                  *reinterpret_cast<uint4*>(y + c) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
+              }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            const float rstd = rsqrtf(ss / static_cast<float>(cols) + eps);
+            for (int c0 = lane * 8; c0 < cols; c0 += 256 * U) {
+              uint4 v[U], gv[U];
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (c0 + u * 256 < cols) {
+                  v[u] = *reinterpret_cast<const uint4*>(y + c0 + u * 256);  // this lane's own stores
+                  gv[u] = __ldg(reinterpret_cast<const uint4*>(g + c0 + u * 256));
+                }
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (c0 + u * 256 < cols) {
+                  const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                  const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+                  uint32_t o[4];
+#pragma unroll
+                  for (int i = 0; i < 4; ++i)
+                    o[i] = pack_bf16x2(bf16lo(w[i]) * rstd * bf16lo(gw[i]), bf16hi(w[i]) * rstd * bf16hi(gw[i]));
+                  *reinterpret_cast<uint4*>(yn + c0 + u * 256) = make_uint4(o[0], o[1], o[2], o[3]);
+                }
             }
           }
         }

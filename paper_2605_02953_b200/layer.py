@@ -17,8 +17,7 @@ the TP-sharded Llama-3 layer graph:
     qkv = linear(xn, Wqkv) + RoPE(q, k)          128 x 256 tiles
     att = attention(qkv)  (causal, GQA)          (128-query tile, head)
     op  = linear(att, Wo)                        partial sums (K sharded over TP)
-    h   = allreduce_residual(op, x)              h = sum_rank op + x
-    hn  = rmsnorm(h, g_mlp)
+    h, hn = allreduce_residual(op, x)            h = sum_rank op + x, hn = rmsnorm(h) fused
     act = linear(hn, W13) -> silu(gate) * up     gate/up rows interleaved per 128
     dp  = linear(act, W2)                        partial sums
     out = allreduce_residual(dp, h)
@@ -95,7 +94,7 @@ def plan_linear_bf16(io, config) -> MK.LayerPlan:
     # emission order = grouped raster (swizzle_2d, ovs/swizzle.py:76-88) so the tiles one
     # wave of round-robin queues runs share group_m A panels and ~grid/group_m B panels in
     # L2; tile ids stay row-major (the dependency contract)
-    gm = max(1, int(cfg.get("group_m", 16)))
+    gm = max(1, int(cfg.get("group_m", 8)))
     for step in range(tm_n * tn_n):
         grp, r = divmod(step, gm * tn_n)
         rows = min(tm_n - grp * gm, gm)
@@ -127,12 +126,19 @@ def plan_rmsnorm(io, config) -> MK.LayerPlan:
 
 def plan_allreduce_residual(io, config) -> MK.LayerPlan:
     """y = (x_0 + ... + x_{w-1}) + res over the team (fp32, ascending rank), bf16.
+    With `norm_gain=<[1, cols] tensor>` the following RMSNorm is fused in: a second
+    output yn = y * rsqrt(mean(y^2) + eps) * gain (one pass over the rows).
     Tiles are row blocks; each tile waits on the producer tiles of its rows on
     every rank (the reference's allreduce waits on the whole input, builders.py:222)."""
-    (x, res), (y,) = io[0], io[1]
+    (x, res), outs = io[0], io[1]
+    y = outs[0]
     if not (x.shape == res.shape == y.shape) or x.shape[1] % 8:
         raise BuildError(f"allreduce_residual shapes must match (cols % 8 == 0): {x.shape} {res.shape} {y.shape}")
-    cfg = {"block_rows": 32, **config}
+    cfg = {"block_rows": 32, "eps": 1e-5, "norm_gain": None, **config}
+    if (cfg["norm_gain"] is None) != (len(outs) == 1):
+        raise BuildError("allreduce_residual: a second output needs norm_gain (and vice versa)")
+    if cfg["norm_gain"] is not None and (cfg["norm_gain"].shape != (1, x.shape[1]) or outs[1].shape != y.shape):
+        raise BuildError("allreduce_residual norm: gain [1, cols] and yn shaped like y")
     rows, cols = x.shape
     br = cfg["block_rows"]
     n = -(-rows // br)
@@ -140,7 +146,8 @@ def plan_allreduce_residual(io, config) -> MK.LayerPlan:
     for t in range(n):
         reg = dict(start_indices=(t * br, 0), data_sizes=(min(br, rows - t * br), cols))
         tiles.append(MK.TileSpec(t, (MK.InputDependencyDesc(x, **reg), MK.InputDependencyDesc(res, **reg))))
-    return MK.LayerPlan("allreduce_residual", io, cfg, n, tiles, {y.name: MK.OutputTilingDesc((br, cols))})
+    return MK.LayerPlan("allreduce_residual", io, cfg, n, tiles,
+                        {o.name: MK.OutputTilingDesc((br, cols)) for o in outs})
 
 
 def plan_attention(io, config) -> MK.LayerPlan:
@@ -241,6 +248,9 @@ def layer_tables(program: MK.MegaProgram, built: MK.BuiltGraph):
             row[12] = 1 if c["causal"] else 0
         elif op == "rmsnorm":
             row[11] = _f32_bits(c["eps"])
+        elif op == "allreduce_residual" and c.get("norm_gain") is not None:
+            row[11] = _f32_bits(c["eps"])
+            row[15] = 1 + (c["norm_gain"].offset >> 4)
     for t in program.tensors:
         if t.offset % 16:
             raise BuildError(f"tensor {t.name} offset {t.offset} is not 16-byte aligned")
@@ -416,8 +426,7 @@ def llama_layer_program(topology, tokens: int, hidden: int, heads_q: int, heads_
     p.layer("linear", [xn, wqkv, rope], [qkv], epilogue="rope", rope_cols=(hq + hkv) * HEAD_DIM)
     p.layer("attention", [qkv], [att], heads_q=hq, heads_kv=hkv, seq_len=seq, causal=True)
     p.layer("linear", [att, wo], [op])
-    p.layer("allreduce_residual", [op, x], [h], block_rows=norm_rows)
-    p.layer("rmsnorm", [h, g2], [hn], eps=eps, block_rows=norm_rows)
+    p.layer("allreduce_residual", [op, x], [h, hn], block_rows=norm_rows, norm_gain=g2, eps=eps)
     p.layer("linear", [hn, w13], [act], epilogue="silu_mul")
     p.layer("linear", [act, w2], [dp])
     p.layer("allreduce_residual", [dp, h], [out], block_rows=norm_rows)

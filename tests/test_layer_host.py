@@ -45,16 +45,20 @@ def test_llama_graph_dependencies():
         prods = {int(r[0]) for r in built.dep_table[t.dep_start:t.dep_end]}
         assert prods == {3}
     # silu_mul output tiles are 128 wide
-    assert built.layer_configs[6]["epilogue"] == "silu_mul"
+    assert built.layer_configs[5]["epilogue"] == "silu_mul"
+    # the MLP rmsnorm is fused into the first allreduce_residual (two outputs)
+    assert built.layer_ops[4] == "allreduce_residual" and built.layer_configs[4]["norm_gain"] is not None
 
 
 def test_tables_and_specs():
     prog = L.llama_layer_program(build_topology(1, 1), 256, 512, 4, 2, 1024)
     built = prog.build()
     cfg, specs = L.layer_tables(prog, built)
-    assert cfg.shape == (9, 16) and list(cfg[:, 0]) == [1, 2, 3, 2, 4, 1, 2, 2, 4]
+    assert cfg.shape == (8, 16) and list(cfg[:, 0]) == [1, 2, 3, 2, 4, 2, 2, 4]
     assert cfg[1, 4] == 1 and cfg[1, 14] == 3 and cfg[1, 13] == 6 * 128
-    assert cfg[6, 4] == 2 and cfg[2, 12] == 1
+    assert cfg[5, 4] == 2 and cfg[2, 12] == 1
+    g2 = next(t for t in prog.tensors if t.name == "g_mlp")
+    assert cfg[4, 15] == 1 + g2.offset // 16 and cfg[7, 15] == 0
     assert specs.shape[1] == 8 and all(s[1] in (2, 3) for s in specs)
     assert all(s[0] % 16 == 0 for s in specs)
 
