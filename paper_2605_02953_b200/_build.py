@@ -34,6 +34,7 @@ def nvcc_path() -> str:
 
 def _digest() -> str:
     h = hashlib.sha256()
+    h.update(os.environ.get("TF_NVCC_EXTRA", "").encode())
     for p in sorted(list(CSRC.glob("*")) + [ROOT / "include" / "tilefuse.h", pathlib.Path(__file__)]):
         if p.is_file():
             h.update(p.name.encode())
@@ -50,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
            "-I", str(ROOT / "include"), "-I", str(CSRC),
-           "-DTF_BUILD_SO=1", "-o", str(LIB) + ".tmp", *srcs]
+           "-DTF_BUILD_SO=1", *os.environ.get("TF_NVCC_EXTRA", "").split(),
+           "-o", str(LIB) + ".tmp", *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
