@@ -31,3 +31,14 @@ def test_torchrun_ipc_team_parity(nproc):
            os.path.join(ROOT, "tests", "dist", "ipc_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "IPC_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_torchrun_layer_megakernel_ipc():
+    """Config-5 layer, one process per rank (IPC team), allreduce over P2P."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "tests", "dist", "layer_ipc_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "LAYER_IPC_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
