@@ -146,10 +146,17 @@ __global__ void __launch_bounds__(1024) scan_kernel(int32_t* __restrict__ chunk_
   extern __shared__ int32_t tot[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const int32_t v = chunk_hist[static_cast<int64_t>(c) * E + e];
-      chunk_hist[static_cast<int64_t>(c) * E + e] = run;
-      run += v;
+    for (int c0 = 0; c0 < nchunks; c0 += 16) {  // 16 independent loads in flight
+      int32_t v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        v[u] = c0 + u < nchunks ? chunk_hist[static_cast<int64_t>(c0 + u) * E + e] : 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (c0 + u < nchunks) {
+          chunk_hist[static_cast<int64_t>(c0 + u) * E + e] = run;
+          run += v[u];
+        }
     }
     tot[e] = run;
     counts[e] = run;
@@ -229,12 +236,11 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
   }
   for (int i = threadIdx.x; i < world * E; i += blockDim.x) counts_out[i] = mat[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t mine = 0;
-    for (int e = rank * epr; e < (rank + 1) * epr; ++e) mine += tot[e];
-    *recv_rows = mine;
-  }
+  __shared__ int32_t last_tot;
+  if (threadIdx.x == 0) last_tot = tot[(rank + 1) * epr - 1];
   block_exclusive_scan(tot, E);  // global exclusive prefix over experts
+  if (threadIdx.x == 0) *recv_rows = static_cast<int64_t>(tot[(rank + 1) * epr - 1]) + last_tot -
+                                     tot[rank * epr];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     const int owner_first = (e / epr) * epr;
     int32_t base = tot[e] - tot[owner_first];  // rows of lower experts on the same owner
@@ -243,38 +249,73 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
   }
 }
 
-// warp per (token, slot): 16-byte vector copy of x[t] into the owner's receive row
-__global__ void __launch_bounds__(256) scatter_kernel(
+// warp per (token, piece of <= 8 KB of the row), all data movement on the TMA
+// engine: one bulk copy brings the piece of x[t] into this warp's smem buffer, then
+// k bulk stores
+// write it into the k destination rows (the owners' receive buffers; peer-mapped
+// addresses for remote owners).  Lane j < k resolves slot j's destination row.
+constexpr int kScatterWarps = 8;
+constexpr int kScatterBuf = 8192;  // bytes per warp (>= half a row, 16-byte multiple)
+
+__global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
     const uint4* __restrict__ x, int64_t tokens, int64_t vec_per_row, int k, int E, int world,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ sorted_pos,
     const int32_t* __restrict__ expert_base, const int32_t* __restrict__ seg_base,
     int32_t* __restrict__ dest_row, PeerPtrs recv, int64_t max_recv, unsigned long long* err) {
-  const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(128) uint8_t sbuf[];
+  __shared__ uint64_t bar[kScatterWarps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* buf = sbuf + wib * kScatterBuf;
+  if (lane == 0) {
+    mbar_init(&bar[wib], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  uint32_t phase = 0;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int epr = E / world;
+  constexpr int64_t kPiece = kScatterBuf / 16;  // uint4 per piece
+  const int64_t npieces = (vec_per_row + kPiece - 1) / kPiece;
   for (int64_t wi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-       wi < tokens * k; wi += nwarps) {
-    const int64_t t = wi / k;
-    const int e = idx[wi];
-    const int owner = e / epr;
-    const int64_t row = static_cast<int64_t>(seg_base[e]) + (sorted_pos[wi] - expert_base[e]);
-    if (lane == 0) dest_row[wi] = static_cast<int32_t>(row);
-    if (row >= max_recv) {
-      if (lane == 0 && err) atomicCAS(err, 0ull, 0x5000000ull | 0xFFFFFFull);
-      continue;
+       wi < tokens * npieces; wi += nwarps) {
+    const int64_t t = wi / npieces, piece = wi % npieces;
+    const int64_t v0 = piece * kPiece, v1 = min(v0 + kPiece, vec_per_row);
+    const uint32_t bytes = static_cast<uint32_t>((v1 - v0) * 16);
+    uint4* my_dst = nullptr;
+    if (lane < k) {
+      const int64_t slot = t * k + lane;
+      const int e = idx[slot];
+      const int64_t row = static_cast<int64_t>(seg_base[e]) + (sorted_pos[slot] - expert_base[e]);
+      if (piece == 0) dest_row[slot] = static_cast<int32_t>(row);
+      if (row < max_recv) my_dst = static_cast<uint4*>(recv.p[e / epr]) + row * vec_per_row + v0;
+      else if (err) atomicCAS(err, 0ull, 0x5000000ull | 0xFFFFFFull);
     }
-    const uint4* src = x + t * vec_per_row;
-    uint4* dst = static_cast<uint4*>(recv.p[owner]) + row * vec_per_row;
-    int64_t v = lane;
-    for (; v + 7 * 32 < vec_per_row; v += 8 * 32) {  // 8 independent 16-byte loads per lane
-      uint4 r[8];
+    uint4* dsts[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] = __ldg(src + v + 32 * u);
+    for (int j = 0; j < 16; ++j)
+      dsts[j] = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), j));
+    if (lane == 0) {
+      // the previous half row's stores must have finished reading the buffer
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive_expect_tx(&bar[wib], bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(buf)),
+          "l"(x + t * vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bar[wib]))
+          : "memory");
+      mbar_wait(&bar[wib], phase);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) __stcs(dst + v + 32 * u, r[u]);  // streaming: no L2 reuse
+      for (int j = 0; j < 16; ++j)
+        if (j < k && dsts[j] != nullptr)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[j]),
+                       "r"(smem_u32(buf)), "r"(bytes)
+                       : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    for (; v < vec_per_row; v += 32) __stcs(dst + v, __ldg(src + v));
+    phase ^= 1;
+    __syncwarp();
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores globally done
 }
 
 // after the scatter kernel (stream order): release "source `rank` delivered" on every owner
@@ -492,8 +533,15 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
       recv.p[p] = t->pes[p].base + m.recv_off;
       flags.p[p] = t->pes[p].sig + sig + w;
     }
+    static uint64_t attr_done = 0;
+    if (!(attr_done & (1ull << dev))) {
+      TF_CUDA_TRY(cudaFuncSetAttribute(tf::scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tf::kScatterWarps * tf::kScatterBuf));
+      attr_done |= 1ull << dev;
+    }
     if (entries > 0)
-      tf::scatter_kernel<<<tf::grid_for(entries), 256, 0, s>>>(
+      tf::scatter_kernel<<<tf::grid_for(a->tokens * ((a->hidden / 8 + 511) / 512)), 32 * tf::kScatterWarps,
+                           tf::kScatterWarps * tf::kScatterBuf, s>>>(
           static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
           a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank));
     if (w > 1) tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
