@@ -625,14 +625,18 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_empty[st]);
-          const bool diag = causal && j == n - 1;
+          if (causal && j == n - 1) {  // diagonal tile only (warp-uniform branch)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i > row) sv[c][i] = __float_as_uint(-INFINITY);
+          }
           float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              if (diag && c * 32 + i > row) sv[c][i] = __float_as_uint(-INFINITY);
-              if (diag && c * 32 + i + 1 > row) sv[c][i + 1] = __float_as_uint(-INFINITY);
               mx0 = fmaxf(mx0, __uint_as_float(sv[c][i]));
               mx1 = fmaxf(mx1, __uint_as_float(sv[c][i + 1]));
             }
