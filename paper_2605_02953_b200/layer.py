@@ -258,6 +258,99 @@ def layer_tables(program: MK.MegaProgram, built: MK.BuiltGraph):
     return cfg, spec_arr
 
 
+ELEMENTWISE_OPS = ("rmsnorm", "allreduce_residual")
+
+
+def dataflow_order(built: MK.BuiltGraph, lag: int = 0) -> list:
+    """Task order for the static queues: tensor tasks keep the builder's order;
+    an elementwise task moves up to `lag` positions after the last producer tile it
+    waits on (about two waves of round-robin queues, so its inputs are usually
+    complete when its CTA reaches it), but never past its own builder position.
+    Each CTA drains its queue in order, so an elementwise task queued behind the
+    CTA's remaining GEMM tiles would wait for all of them (the final allreduce
+    would trail the whole down-projection), while one queued too early blocks the
+    CTA's epilogue warps.  An elementwise task only moves earlier and never ahead
+    of its producers, so the result is a topological order and round-robin queues
+    stay deadlock-free."""
+    slot = {}
+    keyed = []
+    for i, t in enumerate(built.tasks):
+        key = float(i)
+        if built.layer_ops[t.layer_id] in ELEMENTWISE_OPS:
+            deps = [slot.get((int(p), tile)) for p, lo, hi in built.dep_table[t.dep_start:t.dep_end]
+                    for tile in range(int(lo), int(hi))]
+            deps = [d for d in deps if d is not None]
+            if deps:
+                key = min(max(deps) + 0.5 + lag, float(i))
+        slot[(t.task_id, t.tile_id)] = key
+        keyed.append((key, i, t))
+    keyed.sort(key=lambda x: (x[0], x[1]))
+    return [t for _, _, t in keyed]
+
+
+# per-SM rates for the static schedule's cost model (measured on B200, round 1):
+# linear tiles ~9 TFLOP/s per SM (1.34 PFLOP/s sustained / 148), attention ~5.5,
+# elementwise tasks are latency-bound at ~25 GB/s per CTA
+_RATE_LINEAR, _RATE_ATTN, _RATE_ELEM = 9.0e12, 5.5e12, 25.0e9
+
+
+def task_cost_us(built: MK.BuiltGraph, program: MK.MegaProgram, t) -> float:
+    """Estimated duration of one task on one CTA (microseconds)."""
+    op = built.layer_ops[t.layer_id]
+    ins, outs = program.layers[t.layer_id][1]
+    c = built.layer_configs[t.layer_id]
+    if op == "linear":
+        return 2.0 * BLOCK_M * BLOCK_N * ins[0].shape[1] / _RATE_LINEAR * 1e6
+    if op == "attention":
+        i = t.tile_id // c["heads_q"]
+        tps = c["seq_len"] // 128
+        n_kv = (i % tps) + 1 if c["causal"] else tps
+        return 4.0 * 128 * 128 * HEAD_DIM * n_kv / _RATE_ATTN * 1e6 + 2.0
+    rows = min(c["block_rows"], ins[0].shape[0] - t.tile_id * c["block_rows"])
+    nbytes = rows * ins[0].shape[1] * 2 * (len(ins) + len(outs))
+    return nbytes / _RATE_ELEM * 1e6 + 2.0
+
+
+def list_schedule(program: MK.MegaProgram, built: MK.BuiltGraph, num_sms: int, order=None):
+    """Static queues by simulated list scheduling: walk a topological task order and
+    give each task to the CTA that can start it earliest (max of the CTA's free time
+    and the task's inputs' estimated finish), appending it to that CTA's queue.
+    Every queue is a subsequence of one topological order, so the in-order
+    persistent executor cannot deadlock (the globally earliest unfinished task
+    always has its inputs done and nothing ahead of it in its queue).  Balances the
+    causal attention tiles (longest first), the GEMM waves and the elementwise
+    tasks, which land on CTAs that run out of tensor work first."""
+    import heapq
+    order = list(built.tasks if order is None else order)
+    finish = {}
+    free = [(0.0, c) for c in range(num_sms)]
+    heapq.heapify(free)
+    queues = [[] for _ in range(num_sms)]
+    for t in order:
+        ready = 0.0
+        for p, lo, hi in built.dep_table[t.dep_start:t.dep_end]:
+            for tile in range(int(lo), int(hi)):
+                f = finish.get((int(p), tile))
+                if f is not None and f > ready:
+                    ready = f
+        # earliest-start CTA: the least-loaded one unless several are free before `ready`
+        ft, cta = heapq.heappop(free)
+        start = max(ft, ready)
+        end = start + task_cost_us(built, program, t)
+        finish[(t.task_id, t.tile_id)] = end
+        queues[cta].append(t)
+        heapq.heappush(free, (end, cta))
+    slots = max(1, max(len(q) for q in queues))
+    q = np.zeros((slots, num_sms, MK.INT_PER_TASK), dtype=np.int32)
+    q[:, :, MK.IO_TENSORS_OFFSET::MK.INTS_PER_IO_SLOT] = -1
+    counts = np.zeros(num_sms, dtype=np.int32)
+    for c, tasks in enumerate(queues):
+        for i, t in enumerate(tasks):
+            q[i, c] = MK.encode_task(t)
+        counts[c] = len(tasks)
+    return q, counts
+
+
 class LayerArgs(C.Structure):
     _fields_ = [("queues", C.c_void_p), ("counts", C.c_void_p), ("deps", C.c_void_p),
                 ("layer_cfg", C.c_void_p), ("map_specs", C.c_void_p), ("num_maps", C.c_int32),
@@ -277,7 +370,8 @@ class LayerRunner:
     process runs its own rank with num_sms CTAs; peers' heaps are IPC-mapped."""
 
     def __init__(self, program: MK.MegaProgram, built: MK.BuiltGraph | None = None, num_sms: int | None = None,
-                 *, team=None, device: int = 0, queues=None, counts=None, timeout_s: float = 20.0):
+                 *, team=None, device: int = 0, queues=None, counts=None, timeout_s: float = 20.0,
+                 schedule: str = "rr"):
         import torch
 
         from .shmem import SymmetricHeap, Team
@@ -311,7 +405,18 @@ class LayerRunner:
         nslots = (self.built.max_task_id + 1) * self.built.max_tiles_per_op
         self.flags = self.heap.alloc_signals(nslots)
         if queues is None:
-            queues, counts = MK.encode_work_queues(self.built.tasks, self.num_sms)
+            # "rr": the reference's round-robin over the builder order (fastest measured
+            # at config 5: it keeps the GEMM waves' grouped raster); "dataflow" /
+            # "list" are the alternatives measured in DESIGN.md §3.9
+            if schedule == "rr":
+                queues, counts = MK.encode_work_queues(self.built.tasks, self.num_sms)
+            elif schedule == "dataflow":
+                queues, counts = MK.encode_work_queues(dataflow_order(self.built, 2 * self.num_sms),
+                                                       self.num_sms)
+            elif schedule == "list":
+                queues, counts = list_schedule(program, self.built, self.num_sms)
+            else:
+                raise ValueError(f"unknown schedule {schedule!r}")
         self.queues = np.ascontiguousarray(queues, dtype=np.int32)
         self.counts = np.ascontiguousarray(counts, dtype=np.int32)
         if self.queues.shape[1] != self.num_sms:
@@ -399,7 +504,7 @@ def interleave_gate_up(w_gate: np.ndarray, w_up: np.ndarray, block: int = 128) -
 
 
 def llama_layer_program(topology, tokens: int, hidden: int, heads_q: int, heads_kv: int, ffn: int,
-                        seq_len: int | None = None, eps: float = 1e-5, norm_rows: int = 32):
+                        seq_len: int | None = None, eps: float = 1e-5, norm_rows: int = 8):
     """The TP-sharded Llama layer as a MegaProgram (per-rank shard shapes; TP =
     topology.world_size).  Returns (program, names)."""
     tp = topology.world_size

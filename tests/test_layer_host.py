@@ -120,3 +120,36 @@ def test_oracle_attention_against_float64():
                 p /= p.sum()
                 ref = p @ v[s0:s0 + i + 1]
                 assert np.allclose(got[s0 + i, h * 128:(h + 1) * 128], ref, rtol=1e-2, atol=1e-2)
+
+
+def test_dataflow_order_is_topological():
+    prog = L.llama_layer_program(build_topology(2, 1), 512, 512, 8, 2, 1024, seq_len=256)
+    built = prog.build()
+    order = L.dataflow_order(built)
+    assert sorted((t.task_id, t.tile_id) for t in order) == sorted((t.task_id, t.tile_id) for t in built.tasks)
+    pos = {(t.task_id, t.tile_id): i for i, t in enumerate(order)}
+    for t in order:
+        for p, lo, hi in built.dep_table[t.dep_start:t.dep_end]:
+            for tile in range(int(lo), int(hi)):
+                assert pos[(int(p), tile)] < pos[(t.task_id, t.tile_id)]
+    # the final allreduce tasks are spread through the down projection, not appended
+    last = [i for i, t in enumerate(order) if t.task_id == 7]
+    first_down = min(i for i, t in enumerate(order) if t.task_id == 6)
+    assert min(last) < max(i for i, t in enumerate(order) if t.task_id == 6)
+    assert min(last) > first_down
+
+
+def test_list_schedule_queues_are_topological_subsequences():
+    prog = L.llama_layer_program(build_topology(2, 1), 512, 512, 8, 2, 1024, seq_len=256)
+    built = prog.build()
+    q, c = L.list_schedule(prog, built, 7)
+    seen = []
+    for cta in range(7):
+        for i in range(int(c[cta])):
+            seen.append((cta, i, MK.decode_task(q[i, cta])))
+    assert sorted((t.task_id, t.tile_id) for _, _, t in seen) == sorted((t.task_id, t.tile_id) for t in built.tasks)
+    # each queue follows the builder's topological order
+    pos = {(t.task_id, t.tile_id): k for k, t in enumerate(built.tasks)}
+    for cta in range(7):
+        ks = [pos[(t.task_id, t.tile_id)] for cc, _, t in seen if cc == cta]
+        assert ks == sorted(ks)
