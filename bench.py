@@ -51,6 +51,19 @@ def parse():
     return p.parse_args()
 
 
+def _committed_traffic():
+    """DRAM bytes per launch of the GEMM kernel from the committed ncu --set full
+    capture (profiles/gemm_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"dram_bytes_per_launch": d["dram_bytes_per_launch"],
+                "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"], "source": d["source"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -628,7 +641,7 @@ def main_ours(args):
     roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "frac_of_sustained": round(achieved / peak_sus, 4),
             "peak_kind": f"{peaks_kind} burst bf16 (MEASURED_PEAKS.json bf16_tflops)",
-            "traffic": None, "kernel": "gemm_sm100_kernel<CG=2,BN=256,bf16> (256x256 tile per CTA pair)",
+            "traffic": _committed_traffic(), "kernel": "gemm_sm100_kernel<CG=2,MH=2,BN=256,bf16> (512x256 tile per CTA pair)",
             "group_m": args.group_m,
             "flops_per_launch": gemm_flops, "nvlink_bytes_per_ag": nv_bytes,
             "per_op_ms": {"ag_gemm": round(ag_avg, 4), "gemm_rs": round(rs_avg, 4)}}
