@@ -140,9 +140,11 @@ __device__ __forceinline__ bool wait_deps(const LayerParams& p, const Rec& r, in
   return any;
 }
 
-__device__ __forceinline__ void release_flag(const LayerParams& p, int rank, const Rec& r) {
-  uint64_t* f = p.sig[rank] + p.flag_base + static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile;
-  if (ld_acquire_sys(f) >= p.epoch)  // double release (scoreboard.py:50-56)
+// release (task, tile) on PE `pe`'s scoreboard; a flag already at this epoch is a
+// double release (scoreboard.py:50-56), reported on the releasing rank's error word
+__device__ __forceinline__ void release_flag(const LayerParams& p, int rank, const Rec& r, int pe) {
+  uint64_t* f = p.sig[pe] + p.flag_base + static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile;
+  if (ld_acquire_sys(f) >= p.epoch)
     atomicCAS(p.err[rank], 0ull,
               0x9000000ull | (static_cast<uint64_t>(r.task_id) * p.max_tiles + r.tile));
   fence_sys();
@@ -713,7 +715,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         kv_it += n;
       } else {
         // ------------------------------------------------ elementwise tasks (128 threads)
+        // two-shot allreduce: row block b is reduced once, by rank b % world, which
+        // P2P-stores the result into every PE and releases the tile on every PE's
+        // scoreboard; the other ranks skip the task (no release of their own)
+        const bool two_shot = op == OP_ALLREDUCE_RES && p.world > 1 && __ldg(cfg + 13) != 0;
+        if (two_shot && r.tile % p.world != rank) continue;
         const int npe = op == OP_ALLREDUCE_RES ? p.world : 1;
+        const int nout = two_shot ? p.world : 1;  // destinations of the outputs
         const unsigned long long t_fetch = p.trace ? globaltimer_ns() : 0;
         wait_deps(p, r, rank, npe, et, 128);
         named_bar(2, 128);
@@ -820,7 +828,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
                   o[e] = pack_bf16x2(acc[u][2 * e] + bf16lo(w[e]), acc[u][2 * e + 1] + bf16hi(w[e]));
-                y[i] = make_uint4(o[0], o[1], o[2], o[3]);
+                const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+                if (nout == 1) {
+                  y[i] = ov;
+                } else {
+                  for (int q = 0; q < nout; ++q)
+                    reinterpret_cast<uint4*>(p.base[(rank + q) % nout] + r.off[2])[i] = ov;
+                }
               }
             }
           }
@@ -879,7 +893,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
                     const float a0 = bf16lo(o[e]), a1 = bf16hi(o[e]);
                     ss += a0 * a0 + a1 * a1;
                   }
-                  *reinterpret_cast<uint4*>(y + c) = make_uint4(o[0], o[1], o[2], o[3]);
+                  const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+                  *reinterpret_cast<uint4*>(y + c) = ov;
+                  for (int q = 1; q < nout; ++q)
+                    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.base[(rank + q) % nout] + r.off[2]) +
+                                              rb + c) = ov;
                 }
               }
             }
@@ -903,7 +921,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
 #pragma unroll
                   for (int i = 0; i < 4; ++i)
                     o[i] = pack_bf16x2(bf16lo(w[i]) * rstd * bf16lo(gw[i]), bf16hi(w[i]) * rstd * bf16hi(gw[i]));
-                  *reinterpret_cast<uint4*>(yn + c0 + u * 256) = make_uint4(o[0], o[1], o[2], o[3]);
+                  const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+                  *reinterpret_cast<uint4*>(yn + c0 + u * 256) = ov;
+                  for (int q = 1; q < nout; ++q)
+                    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.base[(rank + q) % nout] + r.off[3]) +
+                                              rb + c0 + u * 256) = ov;
                 }
             }
           }
@@ -912,7 +934,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       // every task of warps 2-5 ends with its scoreboard release
       named_bar(2, 128);
       if (et == 0) {
-        release_flag(p, rank, r);
+        if (op == OP_ALLREDUCE_RES && p.world > 1 && __ldg(cfg + 13) != 0)
+          for (int q = 0; q < p.world; ++q) release_flag(p, rank, r, (rank + q) % p.world);
+        else
+          release_flag(p, rank, r, rank);
         if (p.trace) {
           unsigned long long* tr = trace_at(p, idx);
           tr[2] = globaltimer_ns();

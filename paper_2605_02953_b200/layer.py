@@ -128,13 +128,17 @@ def plan_allreduce_residual(io, config) -> MK.LayerPlan:
     """y = (x_0 + ... + x_{w-1}) + res over the team (fp32, ascending rank), bf16.
     With `norm_gain=<[1, cols] tensor>` the following RMSNorm is fused in: a second
     output yn = y * rsqrt(mean(y^2) + eps) * gain (one pass over the rows).
+    two_shot (default): row block b is reduced only by rank b % world, which stores
+    the result into every rank's copy over P2P and releases the tile on every
+    rank's scoreboard (reduce-scatter + all-gather traffic, 2 (w-1)/w of the data
+    per rank, instead of every rank reading all w partials).
     Tiles are row blocks; each tile waits on the producer tiles of its rows on
     every rank (the reference's allreduce waits on the whole input, builders.py:222)."""
     (x, res), outs = io[0], io[1]
     y = outs[0]
     if not (x.shape == res.shape == y.shape) or x.shape[1] % 8:
         raise BuildError(f"allreduce_residual shapes must match (cols % 8 == 0): {x.shape} {res.shape} {y.shape}")
-    cfg = {"block_rows": 32, "eps": 1e-5, "norm_gain": None, **config}
+    cfg = {"block_rows": 32, "eps": 1e-5, "norm_gain": None, "two_shot": True, **config}
     if (cfg["norm_gain"] is None) != (len(outs) == 1):
         raise BuildError("allreduce_residual: a second output needs norm_gain (and vice versa)")
     if cfg["norm_gain"] is not None and (cfg["norm_gain"].shape != (1, x.shape[1]) or outs[1].shape != y.shape):
@@ -248,9 +252,11 @@ def layer_tables(program: MK.MegaProgram, built: MK.BuiltGraph):
             row[12] = 1 if c["causal"] else 0
         elif op == "rmsnorm":
             row[11] = _f32_bits(c["eps"])
-        elif op == "allreduce_residual" and c.get("norm_gain") is not None:
-            row[11] = _f32_bits(c["eps"])
-            row[15] = 1 + (c["norm_gain"].offset >> 4)
+        elif op == "allreduce_residual":
+            row[13] = 1 if c.get("two_shot", True) else 0
+            if c.get("norm_gain") is not None:
+                row[11] = _f32_bits(c["eps"])
+                row[15] = 1 + (c["norm_gain"].offset >> 4)
     for t in program.tensors:
         if t.offset % 16:
             raise BuildError(f"tensor {t.name} offset {t.offset} is not 16-byte aligned")
@@ -453,7 +459,8 @@ class LayerRunner:
         for cta in range(t.shape[0]):
             for idx in range(int(self.counts[cta % self.num_sms])):
                 f, d, e, tt = (int(v) for v in t[cta, idx])
-                out.append((cta, tt >> 32, tt & 0xFFFFFFFF, f, d, e))
+                if e:  # tasks a rank skips (two-shot allreduce tiles it does not own) leave no record
+                    out.append((cta, tt >> 32, tt & 0xFFFFFFFF, f, d, e))
         return out
 
     def run(self, stream=None) -> None:
@@ -471,6 +478,11 @@ class LayerRunner:
                          self.queues.shape[0])
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.device(self.device):
+            if self.rank >= 0 and self.world > 1:
+                # one launch per process: no rank may start writing peers' buffers (two-shot
+                # allreduce) or its own partials (read by peers) while a peer still runs
+                # the previous epoch -- stream-ordered team barrier first
+                _lib.call("tf_barrier_all", self.team.handle, int(self.rank), s.cuda_stream)
             _lib.call("tf_layer_megakernel_run", self.team.handle, int(self.rank), C.byref(args),
                       s.cuda_stream)
 

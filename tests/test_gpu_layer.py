@@ -82,3 +82,26 @@ def test_runner_repeats_with_epochs_and_scoreboard():
         assert all(flags[s] == 3 for s in used)
         assert all(flags[s] == 0 for s in range(nflag) if s not in used)
     runner.close()
+
+
+@pytest.mark.parametrize("two_shot", [False, True])
+def test_allreduce_one_and_two_shot_agree(two_shot):
+    """One-shot (every rank reduces every row) and two-shot (owner reduces, P2P
+    broadcast) give bit-identical layers (TP=4)."""
+    from paper_2605_02953_b200 import build_topology
+    prog, inputs, want, _ = make_case(4, seq=128, heads_kv=4, seed=13)
+    for lid, (op, io, cfg) in enumerate(prog.layers):
+        if op == "allreduce_residual":
+            cfg["two_shot"] = two_shot
+    run = MK.run_megakernel(prog, prog.build(), 12, inputs=inputs)
+    for r in range(4):
+        assert compare(run.outputs["out"][r], want) <= TOL
+        assert np.array_equal(run.outputs["out"][r], run.outputs["out"][0])
+        assert np.array_equal(run.outputs["h"][r], run.outputs["h"][0])
+    key = "two" if two_shot else "one"
+    _RESULTS[key] = run.outputs["out"][0]
+    if len(_RESULTS) == 2:
+        assert np.array_equal(_RESULTS["one"], _RESULTS["two"])
+
+
+_RESULTS = {}
