@@ -420,17 +420,56 @@ def bench_layer(dev, steps, warmup, peaks, flush, tp_emulated=1):
     torch.cuda.synchronize(dev)
     cms = sum(a.elapsed_time(b) for a, b in cevs) / steps
     rel = float((out_fused.float() - ref.float()).abs().max() / ref.float().abs().max())
+    n_tasks = len(runner.built.tasks)
     runner.close()
+    del runner
+    torch.cuda.empty_cache()
+
+    # ---- the TP=8 graph of the same layer, all 8 ranks co-scheduled on this GPU
+    # (8 x 18 CTAs in one launch; peers' partials are HBM-local here, so this checks
+    # the TP8 protocol -- two-shot allreduce, per-rank scoreboards -- at full size,
+    # not NVLink scaling)
+    tp = 8
+    prog8 = L.llama_layer_program(build_topology(tp, 1), T, H, HQ, HKV, FF, seq_len=T)
+    r8 = L.LayerRunner(prog8, device=dev)
+    for pe in range(tp):
+        for t in prog8.tensors:
+            v = r8.view(t.name, pe)
+            if t.name == "rope":
+                v.copy_(rope)
+            elif t.name in ("g_attn", "g_mlp"):
+                v.copy_(g1)
+            else:
+                sc = (t.shape[1] ** -0.5) if t.name.startswith("w_") else 1.0
+                v.copy_((torch.randn(v.shape, generator=g) * sc).to(v.dtype))
+    for _ in range(2):
+        r8.run(stream)
+    torch.cuda.synchronize(dev)
+    r8.check()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        r8.run(stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    r8.check()
+    ms8 = e0.elapsed_time(e1) / 3
+    flops8 = tp * layer_flops(T, H, HQ, HKV, FF, tp)
+    tp8 = {"ms_all_8_ranks": round(ms8, 4), "tflops": round(flops8 / (ms8 * 1e-3) / 1e12, 2),
+           "tasks_per_rank": len(r8.built.tasks), "ctas_per_rank": r8.num_sms,
+           "note": "TP=8 graph, 8 ranks co-resident on one GPU (18 CTAs each); protocol at full "
+                   "size, not NVLink scaling"}
+    r8.close()
     peak = peaks.get("bf16_tflops", 1622.7)
     return {"workload": f"config 5: Llama-3-70B layer, {T} tokens (one causal sequence), hidden {H}, "
                         f"{HQ}/{HKV} heads, ffn {FF}, TP=1, bf16, one persistent megakernel launch",
             "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2),
-            "flops": flops, "tasks": len(runner.built.tasks),
+            "flops": flops, "tasks": n_tasks,
             "roofline": {"bound": "tensor", "frac": round(flops / (ms * 1e-3) / 1e12 / peak, 4),
                          "peak": peak, "unit": "TFLOP/s"},
             "comparator": {"impl": "unfused cuBLAS GEMMs + torch SDPA (causal, GQA) + torch elementwise",
                            "ms": round(cms, 4), "speedup": round(cms / ms, 4)},
-            "max_rel_err_vs_unfused": round(rel, 5)}
+            "max_rel_err_vs_unfused": round(rel, 5), "tp8_emulated": tp8}
 
 
 # ------------------------------------------------------------------ GPU arm
