@@ -70,6 +70,7 @@ struct KParams {
   unsigned long long* trace;
   int trace_cap;
   int trace_rank;
+  int hint_a, hint_b;                 // L2 policy of the A / B TMA loads (l2_policy kinds)
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t ready_mask = 0;  // AllGather chunks already observed as arrived
+      const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
       for (int work = cluster_id; work < p.total_work; work += num_clusters) {
         int step, kb0, kb1, slot;
         decode_work(p, work, step, kb0, kb1, slot);
@@ -262,10 +264,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
 #pragma unroll
-            for (int h = 0; h < MH; ++h)
-              tma_load_2d_pair(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
-                               tile_m0 + block_row<CG>(h, cta_rank));
-            tma_load_2d_pair(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
+            for (int h = 0; h < MH; ++h) {
+              if (p.hint_a)
+                tma_load_2d_pair_hint(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
+                                      tile_m0 + block_row<CG>(h, cta_rank), pol_a);
+              else
+                tma_load_2d_pair(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
+                                 tile_m0 + block_row<CG>(h, cta_rank));
+            }
+            if (p.hint_b) tma_load_2d_pair_hint(sb, &tmap_b, &full_bar[stage], kb * BK, n0, pol_b);
+            else tma_load_2d_pair(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           } else {
             mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
 #pragma unroll
@@ -858,6 +866,17 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   kp.trace = nullptr;
   kp.trace_cap = 0;
   kp.trace_rank = g.trace_rank;
+  {
+    static int ha = -1, hb = -1;  // L2 policies of the operand loads (TF_L2_HINT_A/B experiments)
+    if (ha < 0) {
+      const char* ea = getenv("TF_L2_HINT_A");
+      const char* eb = getenv("TF_L2_HINT_B");
+      ha = ea ? atoi(ea) : 0;
+      hb = eb ? atoi(eb) : 0;
+    }
+    kp.hint_a = ha;
+    kp.hint_b = hb;
+  }
   {
     std::lock_guard<std::mutex> lock(g_trace_mu);
     int dev = 0;
