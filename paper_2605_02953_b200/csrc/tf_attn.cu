@@ -59,10 +59,9 @@ struct AttnParams {
 struct AttnSmem {
   static constexpr int kQ = 2 * kHalf;        // one Q tile, 32 KB
   static constexpr int kSlot = 2 * kHalf;     // one K or V tile (128 keys x 128 dims), 32 KB
-  static constexpr int kSlots = 3;            // ring K0 V0 K1 V1 ...
-  static constexpr int kP = 2 * kHalf;        // one P tile, 32 KB
+  static constexpr int kSlots = 5;            // ring K0 V0 K1 V1 ...
   static constexpr int kBars = 256;
-  static constexpr int kTotal = 1024 + 2 * kQ + kSlots * kSlot + 2 * kP + kBars;
+  static constexpr int kTotal = 1024 + 2 * kQ + kSlots * kSlot + kBars;
 };
 constexpr int kAttnThreads2 = 320;            // TMA, MMA, 2 x 4 softmax warps
 constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag (FA4)
@@ -154,6 +153,18 @@ __device__ __forceinline__ float ex2_fma(float x) {
   return __int_as_float(__float_as_int(pl) + (__float_as_int(t) << 23));
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]^T: the A operand (P, bf16 pairs packed per 32-bit
+// column, rows = lanes) is read from tensor memory, so P never touches shared memory
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __global__ void __maxnreg__(168)
     ag_attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ AttnParams p) {
@@ -162,17 +173,15 @@ __global__ void __maxnreg__(168)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sq = smem;                               // Q_A, Q_B
-  uint8_t* sring = sq + 2 * S::kQ;                  // 3 slots
-  uint8_t* sp = sring + S::kSlots * S::kSlot;       // P_A, P_B
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * S::kP);
+  uint8_t* sring = sq + 2 * S::kQ;                  // 5 slots: K0 V0 K1 V1 ...
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sring + S::kSlots * S::kSlot);
   uint64_t* q_full = bars;
-  uint64_t* r_full = bars + 1;     // [3]
-  uint64_t* r_empty = bars + 4;    // [3]
-  uint64_t* s_full = bars + 7;     // [2] per Q tile
-  uint64_t* s_empty = bars + 9;    // [2]
-  uint64_t* p_full = bars + 11;    // [2]
-  uint64_t* p_free = bars + 13;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* r_full = bars + 1;     // [5]
+  uint64_t* r_empty = bars + 6;    // [5]
+  uint64_t* s_full = bars + 11;    // [2] per Q tile
+  uint64_t* p_full = bars + 13;    // [2]
+  uint64_t* o_ready = bars + 15;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 2 * kQT;
@@ -184,15 +193,14 @@ __global__ void __maxnreg__(168)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < S::kSlots; ++i) {
       mbar_init(&r_full[i], 1);
       mbar_init(&r_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_free[i], 1);
+      mbar_init(&o_ready[i], 1);
     }
     fence_barrier_init();
   }
@@ -200,7 +208,9 @@ __global__ void __maxnreg__(168)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+  // TMEM: S_A [0,128) S_B [128,256) (P_t packed bf16 in the first 64 columns of S_t),
+  //       O_A [256,384) O_B [384,512)
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -209,12 +219,9 @@ __global__ void __maxnreg__(168)
         tma_load_3d(sq + t * S::kQ, &tq, q_full, 0, h, q0 + t * kQT);
         tma_load_3d(sq + t * S::kQ + kHalf, &tq, q_full, 64, h, q0 + t * kQT);
       }
-      // load order K0 K1 V0 K2 V1 ... K_{n-1} V_{n-2} V_{n-1}: K runs one tile ahead, so a
-      // slot is refilled two MMA steps before it is consumed (hides the TMA latency)
       uint32_t ready = 0;
-      for (int c = 0; c < 2 * n; ++c) {
-        int j, kv;
-        ring_decode(c, n, j, kv);
+      for (int c = 0; c < 2 * n; ++c) {  // K_j = 2j, V_j = 2j + 1
+        const int j = c >> 1, kv = c & 1;
         const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
         const int chunk = kt / p.tiles_per_chunk;
         if (!kv && p.chunk_flags && !(ready & (1u << chunk))) {
@@ -223,8 +230,8 @@ __global__ void __maxnreg__(168)
           fence_proxy_async_global();
           ready |= 1u << chunk;
         }
-        const int sl = c % 3;
-        mbar_wait_spin(&r_empty[sl], ((c / 3) & 1) ^ 1);
+        const int sl = c % S::kSlots;
+        mbar_wait(&r_empty[sl], ((c / S::kSlots) & 1) ^ 1);
         uint8_t* dst = sring + sl * S::kSlot;
         const CUtensorMap* m = kv ? &tv : &tk;
         mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
@@ -233,54 +240,51 @@ __global__ void __maxnreg__(168)
       }
     }
   } else if (warp == 1) {
+    // per Q tile t: S_t(0); then for each j: PV_t(j) (A = P_t from TMEM), S_t(j+1) into the
+    // same columns -- issued in that order, the tensor pipe reads P_t(j) before S_t(j+1)
+    // overwrites it, and S_t(j+1) completing implies PV_t(j) completed (O_t is stable for
+    // the softmax's rescale)
     constexpr uint32_t idesc_s = umma_idesc_bf16(kQT, kKT);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(kQT, kD) | (1u << 16);  // B (V) MN-major
-    mbar_wait_spin(q_full, 0);
-    tc_fence_after();
-    auto issue_pv = [&](int jj) {
-      const int c = ring_index(jj, 1, n), sl = c % 3;
-      mbar_wait_spin(&r_full[sl], (c / 3) & 1);
-      for (int t = 0; t < nq; ++t) {
-        mbar_wait_spin(&p_full[t], jj & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t pa = smem_u32(sp + t * S::kP);
-          const uint32_t vb = smem_u32(sring + sl * S::kSlot);
+    if (lane == 0) {
+      mbar_wait_spin(q_full, 0);
+      tc_fence_after();
+      auto issue_s = [&](int t, int sl) {
+        const uint32_t qa = smem_u32(sq + t * S::kQ);
+        const uint32_t kb = smem_u32(sring + sl * S::kSlot);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
+          umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off), idesc_s,
+                    kk != 0);
+        }
+        umma_commit(&s_full[t]);
+      };
+      mbar_wait_spin(&r_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < nq; ++t) issue_s(t, 0);
+      umma_commit(&r_empty[0]);
+      for (int j = 0; j < n; ++j) {
+        const int cv = 2 * j + 1, vs = cv % S::kSlots;
+        const int ck = 2 * j + 2, ks = ck % S::kSlots;
+        mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
+        if (j + 1 < n) mbar_wait_spin(&r_full[ks], (ck / S::kSlots) & 1);
+        for (int t = 0; t < nq; ++t) {
+          mbar_wait_spin(&p_full[t], j & 1);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sring + vs * S::kSlot);
 #pragma unroll
           for (int kk = 0; kk < kKT / 16; ++kk)
-            umma_bf16(tmem + 256 + t * 128, umma_desc_k_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32),
-                      umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (jj | kk) != 0);
-          umma_commit(&p_free[t]);
+            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                         umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (j | kk) != 0);
+          if (j + 1 < n) issue_s(t, ks);
+          else umma_commit(&o_ready[t]);
         }
-        __syncwarp();
+        umma_commit(&r_empty[vs]);
+        if (j + 1 < n) umma_commit(&r_empty[ks]);
       }
-      if (lane == 0) umma_commit(&r_empty[sl]);
-      __syncwarp();
-    };
-    for (int j = 0; j < n; ++j) {
-      const int c = ring_index(j, 0, n), sl = c % 3;
-      mbar_wait_spin(&r_full[sl], (c / 3) & 1);
-      for (int t = 0; t < nq; ++t) {
-        mbar_wait_spin(&s_empty[t], (j & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t qa = smem_u32(sq + t * S::kQ);
-          const uint32_t kb = smem_u32(sring + sl * S::kSlot);
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-            umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off), idesc_s,
-                      kk != 0);
-          }
-          umma_commit(&s_full[t]);
-        }
-        __syncwarp();
-      }
-      if (lane == 0) umma_commit(&r_empty[sl]);
-      __syncwarp();
-      if (j > 0) issue_pv(j - 1);
     }
-    issue_pv(n - 1);
+    __syncwarp();
   } else {
     const int t = (warp - 2) >> 2;                 // Q tile of this warpgroup
     if (t < nq) {
@@ -290,7 +294,6 @@ __global__ void __maxnreg__(168)
       const uint32_t t_s = tmem + lane_off + t * 128;
       const uint32_t t_o = tmem + lane_off + 256 + t * 128;
       float m = -INFINITY, l = 0.f;
-      uint8_t* prow = sp + t * S::kP + row * 128;
       for (int j = 0; j < n; ++j) {
         mbar_wait_spin(&s_full[t], j & 1);
         tc_fence_after();
@@ -298,9 +301,6 @@ __global__ void __maxnreg__(168)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[t]);
         float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -316,55 +316,48 @@ __global__ void __maxnreg__(168)
           alpha = ex2(m - mt);
           m = mt;
         }
-        // exponentials into registers first: they overlap P_{j-1} V_{j-1} on the tensor pipe
         float s0 = 0.f, s1 = 0.f;
-        uint32_t pk[4][16];
+        // P row packed in place of the first 64 S columns (the whole row is in registers)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float a0 = fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m);
             const float a1 = fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m);
             const bool emu = TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0;
+#ifdef TF_ATTN_EXP_CHEAP  // bottleneck experiment: no SFU work
+            const float p0 = a0 * 0.001f, p1 = a1 * 0.001f;
+            (void)emu;
+#else
             const float p0 = emu ? ex2_fma(a0) : ex2(a0);
             const float p1 = emu ? ex2_fma(a1) : ex2(a1);
+#endif
             s0 += p0;
             s1 += p1;
-            pk[c][i] = pack_bf16x2(p0, p1);
-          }
-        l = l * alpha + (s0 + s1);
-        if (j > 0) {
-          // P buffer and O_t are free once P_{j-1} V_{j-1} has completed
-          mbar_wait_spin(&p_free[t], (j - 1) & 1);
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
-              uint32_t ov[16];
-              tmem_ld_32x32b_x16(t_o + c * 16, ov);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-              tmem_st_32x32b_x16(t_o + c * 16, ov);
-            }
-            tmem_st_wait();
+            sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
           }
         }
+        l = l * alpha + (s0 + s1);
+        // O_t is stable: S_t(j) completing implies PV_t(j-1) completed
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld_32x32b_x16(t_o + c * 16, ov);
+            tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int chunk = c * 4 + q;
-            const int half = chunk >> 3, jj = chunk & 7;
-            *reinterpret_cast<uint4*>(prow + half * kHalf + ((jj ^ (row & 7)) << 4)) =
-                make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
+            for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st_32x32b_x16(t_o + c * 16, ov);
           }
-        fence_proxy_async_shared();
+        }
+        tmem_st_32x32b_x32(t_s, sv[0]);
+        tmem_st_32x32b_x32(t_s + 32, sv[1]);
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      mbar_wait_spin(&p_free[t], (n - 1) & 1);
+      mbar_wait_spin(&o_ready[t], 0);
       tc_fence_after();
       const float inv = 1.f / l;
       const int q = q0 + t * kQT + row;
