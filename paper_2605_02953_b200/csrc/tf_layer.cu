@@ -15,13 +15,13 @@
 //                                         lags 2 k-blocks at tile    tile flag
 //                                         edges (drain overlaps)
 //   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
-//                 tiles through a 4-slot  (V MN-major)               mask, lazy rescale),
-//                 ring, K one tile ahead                             O / l -> bf16
+//                 tiles through a 5-slot  (P from TMEM, V MN-major)  mask, lazy rescale),
+//                 ring, K one tile ahead                             P -> TMEM, O / l -> bf16
 //   rmsnorm       -                       -                          wait deps, y = x*rstd*g
 //   allreduce_    -                       -                          wait deps on every PE,
 //   residual                                                         y = sum_pe x_pe + res (P2P)
 //
-// The linear ring (3 x 64 KB) and the attention buffers (Q, 2 x K/V, P) alias the
+// The linear ring (3 x 64 KB) and the attention buffers (Q, 5 K/V slots) alias the
 // same 192 KB of shared memory and TMEM columns [0, 512); when consecutive tensor
 // tasks of a CTA change class, all six warps meet at a named barrier first, by
 // which point every TMA load has been consumed and every MMA has retired.
@@ -55,8 +55,7 @@ constexpr int kLag = 2;                       // k-blocks the second M-half trai
 constexpr int kQOff = 0;                      // attention aliases
 constexpr int kKVOff = 2 * kHalfBox;          // ring of 4 K-or-V slots (32 KB each)
 constexpr int kKVSlot = 2 * kHalfBox;
-constexpr int kKVSlots = 4;
-constexpr int kPOff = kKVOff + kKVSlots * kKVSlot;  // 160 KB
+constexpr int kKVSlots = 5;                   // P lives in TMEM (over its S buffer), not smem
 constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag before O is rescaled
 constexpr int kLayerSmem = 1024 + kRegion + 512;
 constexpr int kCfgInts = 16;
@@ -202,6 +201,17 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t l
   return d;
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]^T (A = P, bf16 pairs packed per 32-bit column)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -267,8 +277,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
   uint64_t* tempty = bars + 10;         // [2]
   uint64_t* q_full = bars + 12;
   uint64_t* q_empty = bars + 13;
-  uint64_t* kv_full = bars + 28;        // [4] ring slots
-  uint64_t* kv_empty = bars + 32;       // [4]
+  uint64_t* kv_full = bars + 28;        // [5] ring slots
+  uint64_t* kv_empty = bars + 34;       // [5]
   uint64_t* s_full = bars + 18;         // [2]
   uint64_t* s_empty = bars + 20;        // [2]
   uint64_t* p_full = bars + 22;
@@ -470,12 +480,12 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           mbar_wait(p_full, gi & 1);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t pa = smem_u32(smem + kPOff);
+            // A = P from tensor memory (packed bf16 over the first 64 columns of S[gi & 1])
+            const uint32_t pa = tmem + (gi & 1) * 128;
             const uint32_t vb = smem_u32(smem + kKVOff + st * kKVSlot);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              umma_bf16(t_o, umma_desc_k_sw128(pa + (kk >> 2) * kHalfBox + (kk & 3) * 32),
-                        desc_mn_sw128(vb + kk * 2048, kHalfBox), idesc_pv, (jl | kk) != 0);
+              umma_bf16_ts(t_o, pa + kk * 8, desc_mn_sw128(vb + kk * 2048, kHalfBox), idesc_pv, (jl | kk) != 0);
             umma_commit(&kv_empty[st]);
             umma_commit(pv_done);
           }
@@ -615,7 +625,6 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const float scale_log2 = __int_as_float(__ldg(cfg + 10)) * 1.4426950408889634f;
         const uint32_t t_o = tmem + 256;
         float mrow = -INFINITY, l = 0.f;
-        uint8_t* prow = smem + kPOff + row * 128;
         for (int j = 0; j < n; ++j) {
           const int gi = kv_it + j, st = gi & 1;
           mbar_wait(&s_full[st], (gi >> 1) & 1);
@@ -650,7 +659,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
             mrow = mt;
           }
           float s0 = 0.f, s1 = 0.f;
-          uint32_t pk[4][16];
+          // P packed in place: pair (2i, 2i+1) of chunk c -> sv[c / 2][(c % 2) * 16 + i]
 #pragma unroll
           for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -659,7 +668,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
               const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -mrow));
               s0 += p0;
               s1 += p1;
-              pk[c][i] = pack_bf16x2(p0, p1);
+              sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
             }
           l = l * alpha + (s0 + s1);
           if (j > 0) {
@@ -678,16 +687,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
               asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
           }
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int chunk = c * 4 + q;
-              const int half = chunk >> 3, jj = chunk & 7;
-              *reinterpret_cast<uint4*>(prow + half * kHalfBox + ((jj ^ (row & 7)) << 4)) =
-                  make_uint4(pk[c][4 * q], pk[c][4 * q + 1], pk[c][4 * q + 2], pk[c][4 * q + 3]);
-            }
-          fence_proxy_async_shared();
+          // P(j) over the first 64 columns of its own S buffer (S(j) is in registers; the
+          // next write of this buffer, S(j+2), is issued after PV(j) on the in-order pipe)
+          tmem_st_x32(tmem + lane_off + st * 128, sv[0]);
+          tmem_st_x32(tmem + lane_off + st * 128 + 32, sv[1]);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_full);
