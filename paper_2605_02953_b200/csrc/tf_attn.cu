@@ -142,6 +142,9 @@ __device__ __forceinline__ float ex2(float x) {
 // 2^x on the FMA pipe (FA4's trick to offload the SFU): k = round(x) through the
 // 1.5 * 2^23 magic add, 2^(x-k) by a degree-3 polynomial on [-0.5, 0.5] (rel. error
 // < 1e-4, below bf16's 2^-8), and k added straight into the exponent bits.
+#ifndef TF_ATTN_SPLIT_P
+#define TF_ATTN_SPLIT_P 1  // release P's first 64 keys to the MMA before the rest
+#endif
 #ifndef TF_EXP2_EMU_MASK
 #define TF_EXP2_EMU_MASK -1  // off: measured slower on B200 (4.43 -> 4.83 ms at 25%); 3 -> 25%, 1 -> 50%
 #endif
@@ -182,6 +185,7 @@ __global__ void __maxnreg__(168)
   uint64_t* p_full = bars + 13;    // [2]
   uint64_t* o_ready = bars + 15;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* p_half = bars + 18;    // [2] first 64 keys of P_t written
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 2 * kQT;
@@ -200,6 +204,7 @@ __global__ void __maxnreg__(168)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
+      mbar_init(&p_half[i], 4);
       mbar_init(&o_ready[i], 1);
     }
     fence_barrier_init();
@@ -270,13 +275,20 @@ __global__ void __maxnreg__(168)
         mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
         if (j + 1 < n) mbar_wait_spin(&r_full[ks], (ck / S::kSlots) & 1);
         for (int t = 0; t < nq; ++t) {
-          mbar_wait_spin(&p_full[t], j & 1);
-          tc_fence_after();
           const uint32_t vb = smem_u32(sring + vs * S::kSlot);
+          // keys 0-63 of P_t(j) as soon as the softmax has them, keys 64-127 after
+          mbar_wait_spin(&p_half[t], j & 1);
+          tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < kKT / 16; ++kk)
+          for (int kk = 0; kk < kKT / 32; ++kk)
             umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                          umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (j | kk) != 0);
+          mbar_wait_spin(&p_full[t], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = kKT / 32; kk < kKT / 16; ++kk)
+            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                         umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, 1);
           if (j + 1 < n) issue_s(t, ks);
           else umma_commit(&o_ready[t]);
         }
@@ -316,29 +328,8 @@ __global__ void __maxnreg__(168)
           alpha = ex2(m - mt);
           m = mt;
         }
-        float s0 = 0.f, s1 = 0.f;
-        // P row packed in place of the first 64 S columns (the whole row is in registers)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float a0 = fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m);
-            const float a1 = fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m);
-            const bool emu = TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0;
-#ifdef TF_ATTN_EXP_CHEAP  // bottleneck experiment: no SFU work
-            const float p0 = a0 * 0.001f, p1 = a1 * 0.001f;
-            (void)emu;
-#else
-            const float p0 = emu ? ex2_fma(a0) : ex2(a0);
-            const float p1 = emu ? ex2_fma(a1) : ex2(a1);
-#endif
-            s0 += p0;
-            s1 += p1;
-            sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
-          }
-        }
-        l = l * alpha + (s0 + s1);
-        // O_t is stable: S_t(j) completing implies PV_t(j-1) completed
+        // O_t is stable: S_t(j) completing implies PV_t(j-1) completed; rescale before any
+        // part of P_t(j) is released to the MMA
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
           for (int c = 0; c < 8; ++c) {
@@ -350,12 +341,50 @@ __global__ void __maxnreg__(168)
             tmem_st_32x32b_x16(t_o + c * 16, ov);
           }
         }
-        tmem_st_32x32b_x32(t_s, sv[0]);
-        tmem_st_32x32b_x32(t_s + 32, sv[1]);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
+        float s0 = 0.f, s1 = 0.f;
+        // P row packed in place of the first 64 S columns (the whole row is in registers),
+        // in two halves of 64 keys: PV on the first half overlaps the second half's exps
+#pragma unroll
+        for (int hk = 0; hk < 2; ++hk) {
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hk + cc;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float a0 = fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m);
+              const float a1 = fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m);
+              const bool emu = TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0;
+#ifdef TF_ATTN_EXP_CHEAP  // bottleneck experiment: no SFU work
+              const float p0 = a0 * 0.001f, p1 = a1 * 0.001f;
+              (void)emu;
+#else
+              const float p0 = emu ? ex2_fma(a0) : ex2(a0);
+              const float p1 = emu ? ex2_fma(a1) : ex2(a1);
+#endif
+              s0 += p0;
+              s1 += p1;
+              sv[hk][cc * 16 + i] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st_32x32b_x32(t_s + hk * 32, sv[hk]);
+#if TF_ATTN_SPLIT_P
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(hk == 0 ? &p_half[t] : &p_full[t]);
+#else
+          if (hk == 1) {
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive(&p_half[t]);
+              mbar_arrive(&p_full[t]);
+            }
+          }
+#endif
+        }
+        l = l * alpha + (s0 + s1);
       }
       mbar_wait_spin(&o_ready[t], 0);
       tc_fence_after();
