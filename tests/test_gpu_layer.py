@@ -105,3 +105,16 @@ def test_allreduce_one_and_two_shot_agree(two_shot):
 
 
 _RESULTS = {}
+
+
+@pytest.mark.parametrize("tokens,seq,hidden,ffn", [(384, 384, 512, 1024), (640, 128, 384, 768)])
+def test_layer_ragged_tiles(tokens, seq, hidden, ffn):
+    """Token counts and widths that leave partial 256-row / 256-column tiles
+    (TMA zero-fill on loads, masked epilogue stores)."""
+    prog, inputs, want, inter = make_case(2, tokens=tokens, hidden=hidden, ffn=ffn, seq=seq,
+                                          seed=tokens + hidden)
+    run = MK.run_megakernel(prog, prog.build(), 20, inputs=inputs)
+    for name in ("qkv", "attn", "h", "act"):
+        assert compare(run.outputs[name][0], inter[name]) <= TOL, name
+    for r in range(2):
+        assert compare(run.outputs["out"][r], want) <= TOL
