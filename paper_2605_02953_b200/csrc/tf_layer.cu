@@ -5,7 +5,7 @@
 // (producer task, first tile, one-past-last tile), scoreboard slot
 // task * max_tiles + tile, release-stored with the call epoch.
 //
-// One persistent launch, one CTA per SM, 192 threads with fixed roles; every role
+// One persistent launch, one CTA per SM, 256 threads with fixed roles; every role
 // walks the CTA's queue in order and does its share of each task:
 //
 //   task          warp 0 (TMA)            warp 1 (MMA, one lane)     warps 2-5 (128 thr)
@@ -17,16 +17,17 @@
 //   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
 //                 tiles through a 5-slot  (P from TMEM, V MN-major)  mask, lazy rescale),
 //                 ring, K one tile ahead                             P -> TMEM, O / l -> bf16
-//   rmsnorm       -                       -                          wait deps, y = x*rstd*g
-//   allreduce_    -                       -                          wait deps on every PE,
-//   residual                                                         y = sum_pe x_pe + res (P2P)
+//   rmsnorm       -                       -                          - (warps 6-7: wait deps,
+//                                                                      y = x*rstd*g)
+//   allreduce_    -                       -                          - (warps 6-7: wait deps on
+//   residual                                                           every PE, y = sum x_pe + res)
 //
 // The linear ring (3 x 64 KB) and the attention buffers (Q, 5 K/V slots) alias the
 // same 192 KB of shared memory and TMEM columns [0, 512); when consecutive tensor
 // tasks of a CTA change class, all six warps meet at a named barrier first, by
 // which point every TMA load has been consumed and every MMA has retired.
-// Elementwise tasks only involve warps 2-5, so warps 0-1 keep prefetching the
-// next GEMM tile while they run.
+// Elementwise tasks run on two dedicated warps (6-7), so the tensor roles keep
+// streaming GEMM tiles while a norm or allreduce of the same CTA is in flight.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -44,7 +45,8 @@
 namespace tf {
 namespace {
 
-constexpr int kLThreads = 192;
+constexpr int kLThreads = 256;      // warps 0-5 tensor roles, warps 6-7 elementwise tasks
+constexpr int kTensorThreads = 192;
 constexpr int kRing = 3;
 constexpr int kHalfBox = 16384;               // 128 rows x 128 B
 constexpr int kAStage = 2 * 128 * 64 * 2;     // two 128-row A blocks, 32 KB
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       const int op = __ldg(cfg);
       const int cls = op_class(op);
       if (cls == CLS_ELEM) continue;
-      if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+      if (last_cls >= 0 && cls != last_cls) named_bar(1, kTensorThreads);
       last_cls = cls;
       const unsigned long long t_fetch = p.trace ? globaltimer_ns() : 0;
       const bool waited = __any_sync(0xffffffffu, wait_deps(p, r, rank, 1, lane, 32));
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       const int op = __ldg(cfg);
       const int cls = op_class(op);
       if (cls == CLS_ELEM) continue;
-      if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+      if (last_cls >= 0 && cls != last_cls) named_bar(1, kTensorThreads);
       last_cls = cls;
       if (cls == CLS_LINEAR) {
         // two M=128 halves per 256x256 tile share each B stage; half h accumulates in
@@ -524,8 +526,14 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;                 // TMEM lane = tile row
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const int et = threadIdx.x - 64;                     // 0..127
-    const int ew = warp - 2;                             // 0..3
+    // warps 2-5 drain the tensor tasks; warps 6-7 run the elementwise tasks, so a
+    // norm / allreduce never holds the accumulator drain (and with it the MMA) back
+    const bool elem_grp = warp >= 6;
+    const int gthreads = elem_grp ? 64 : 128;
+    const int gbar = elem_grp ? 3 : 2;
+    const int et = threadIdx.x - (elem_grp ? 192 : 64);  // thread index in the group
+    const int nw = gthreads / 32;
+    const int ew = warp - (elem_grp ? 6 : 2);            // warp index in the group
     int lin_it = 0, kv_it = 0;
     for (int idx = 0; idx < n_tasks; ++idx) {
       Rec r;
@@ -534,8 +542,11 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       const int op = __ldg(cfg);
       const int cls = op_class(op);
       if (cls != CLS_ELEM) {
-        if (last_cls >= 0 && cls != last_cls) named_bar(1, kLThreads);
+        if (elem_grp) continue;
+        if (last_cls >= 0 && cls != last_cls) named_bar(1, kTensorThreads);
         last_cls = cls;
+      } else if (!elem_grp) {
+        continue;
       }
       if (op == OP_LINEAR) {
         const int m = r.d0[0], n = r.d0[1];
@@ -718,7 +729,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         if (lane == 0) mbar_arrive(o_empty);
         kv_it += n;
       } else {
-        // ------------------------------------------------ elementwise tasks (128 threads)
+        // ------------------------------------------------ elementwise tasks (warps 6-7)
         // two-shot allreduce: row block b is reduced once, by rank b % world, which
         // P2P-stores the result into every PE and releases the tile on every PE's
         // scoreboard; the other ranks skip the task (no release of their own)
@@ -727,8 +738,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const int npe = op == OP_ALLREDUCE_RES ? p.world : 1;
         const int nout = two_shot ? p.world : 1;  // destinations of the outputs
         const unsigned long long t_fetch = p.trace ? globaltimer_ns() : 0;
-        wait_deps(p, r, rank, npe, et, 128);
-        named_bar(2, 128);
+        wait_deps(p, r, rank, npe, et, gthreads);
+        named_bar(gbar, gthreads);
         if (p.trace && et == 0) {
           unsigned long long* tr = trace_at(p, idx);
           tr[0] = t_fetch;
@@ -743,9 +754,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           const uint16_t* g = reinterpret_cast<const uint16_t*>(my_base + r.off[1]);
           uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]);
           const int r0 = r.tile * br, r1 = min(r0 + br, rows);
-          prefetch_l2(x + static_cast<long long>(r0) * cols, static_cast<long long>(r1 - r0) * cols * 2, et, 128);
+          prefetch_l2(x + static_cast<long long>(r0) * cols, static_cast<long long>(r1 - r0) * cols * 2, et, gthreads);
           constexpr int U = 8;
-          for (int rr = r0 + ew; rr < r1; rr += 4) {
+          for (int rr = r0 + ew; rr < r1; rr += nw) {
             const uint16_t* xr = x + static_cast<long long>(rr) * cols;
             float ss = 0.f;
             for (int c0 = lane * 8; c0 < cols; c0 += 256 * U) {
@@ -798,10 +809,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           const uint4* res = reinterpret_cast<const uint4*>(my_base + r.off[1]);
           uint4* y = reinterpret_cast<uint4*>(my_base + r.off[2]);
           for (int pe = 0; pe < p.world; ++pe)
-            prefetch_l2(reinterpret_cast<const uint4*>(p.base[pe] + r.off[0]) + lo, (hi - lo) * 16, et, 128);
-          prefetch_l2(res + lo, (hi - lo) * 16, et, 128);
+            prefetch_l2(reinterpret_cast<const uint4*>(p.base[pe] + r.off[0]) + lo, (hi - lo) * 16, et, gthreads);
+          prefetch_l2(res + lo, (hi - lo) * 16, et, gthreads);
           constexpr int U = 8;
-          for (long long i0 = lo + et; i0 < hi; i0 += 128 * U) {
+          for (long long i0 = lo + et; i0 < hi; i0 += gthreads * U) {
             float acc[U][8];
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -811,7 +822,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
               const uint4* src = reinterpret_cast<const uint4*>(p.base[pe] + r.off[0]);
               uint4 v[U];
 #pragma unroll
-              for (int u = 0; u < U; ++u) v[u] = i0 + u * 128 < hi ? src[i0 + u * 128] : make_uint4(0, 0, 0, 0);
+              for (int u = 0; u < U; ++u) v[u] = i0 + u * gthreads < hi ? src[i0 + u * gthreads] : make_uint4(0, 0, 0, 0);
 #pragma unroll
               for (int u = 0; u < U; ++u) {
                 const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
@@ -824,7 +835,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const long long i = i0 + u * 128;
+              const long long i = i0 + u * gthreads;
               if (i < hi) {
                 const uint4 rv = res[i];
                 const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
@@ -852,10 +863,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
               my_base + (static_cast<long long>(__ldg(cfg + 15) - 1) << 4));
           const long long lo = static_cast<long long>(r0) * cols, n_el = static_cast<long long>(r1 - r0) * cols;
           for (int pe = 0; pe < p.world; ++pe)
-            prefetch_l2(reinterpret_cast<const uint16_t*>(p.base[pe] + r.off[0]) + lo, n_el * 2, et, 128);
-          prefetch_l2(reinterpret_cast<const uint16_t*>(my_base + r.off[1]) + lo, n_el * 2, et, 128);
+            prefetch_l2(reinterpret_cast<const uint16_t*>(p.base[pe] + r.off[0]) + lo, n_el * 2, et, gthreads);
+          prefetch_l2(reinterpret_cast<const uint16_t*>(my_base + r.off[1]) + lo, n_el * 2, et, gthreads);
           constexpr int U = 4;
-          for (int rr = r0 + ew; rr < r1; rr += 4) {
+          for (int rr = r0 + ew; rr < r1; rr += nw) {
             const long long rb = static_cast<long long>(rr) * cols;
             const uint16_t* res = reinterpret_cast<const uint16_t*>(my_base + r.off[1]) + rb;
             uint16_t* y = reinterpret_cast<uint16_t*>(my_base + r.off[2]) + rb;
@@ -935,8 +946,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
           }
         }
       }
-      // every task of warps 2-5 ends with its scoreboard release
-      named_bar(2, 128);
+      // every task ends with its scoreboard release by its group
+      named_bar(gbar, gthreads);
       if (et == 0) {
         if (op == OP_ALLREDUCE_RES && p.world > 1 && __ldg(cfg + 13) != 0)
           for (int q = 0; q < p.world; ++q) release_flag(p, rank, r, (rank + q) % p.world);
