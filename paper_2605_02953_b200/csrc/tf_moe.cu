@@ -249,11 +249,10 @@ __global__ void __launch_bounds__(1024) layout_kernel(const int32_t* __restrict_
   }
 }
 
-// warp per (token, piece of <= 8 KB of the row), all data movement on the TMA
-// engine: one bulk copy brings the piece of x[t] into this warp's smem buffer, then
-// k bulk stores
-// write it into the k destination rows (the owners' receive buffers; peer-mapped
-// addresses for remote owners).  Lane j < k resolves slot j's destination row.
+// warp per (token, piece of <= 8 KB of the row): one bulk copy (TMA engine) brings the
+// piece of x[t] into this warp's smem buffer; destination rows on this rank are
+// written by bulk stores, rows owned by peers by the warp's 16-byte P2P stores over
+// NVLink.  Lane j < k resolves slot j's destination row.
 constexpr int kScatterWarps = 8;
 constexpr int kScatterBuf = 8192;  // bytes per warp (>= half a row, 16-byte multiple)
 
@@ -261,7 +260,7 @@ __global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
     const uint4* __restrict__ x, int64_t tokens, int64_t vec_per_row, int k, int E, int world,
     const int32_t* __restrict__ idx, const int32_t* __restrict__ sorted_pos,
     const int32_t* __restrict__ expert_base, const int32_t* __restrict__ seg_base,
-    int32_t* __restrict__ dest_row, PeerPtrs recv, int64_t max_recv, unsigned long long* err) {
+    int32_t* __restrict__ dest_row, PeerPtrs recv, int64_t max_recv, unsigned long long* err, int rank) {
   extern __shared__ __align__(128) uint8_t sbuf[];
   __shared__ uint64_t bar[kScatterWarps];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -282,6 +281,7 @@ __global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
     const int64_t v0 = piece * kPiece, v1 = min(v0 + kPiece, vec_per_row);
     const uint32_t bytes = static_cast<uint32_t>((v1 - v0) * 16);
     uint4* my_dst = nullptr;
+    int my_remote = 0;
     if (lane < k) {
       const int64_t slot = t * k + lane;
       const int e = idx[slot];
@@ -289,11 +289,13 @@ __global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
       if (piece == 0) dest_row[slot] = static_cast<int32_t>(row);
       if (row < max_recv) my_dst = static_cast<uint4*>(recv.p[e / epr]) + row * vec_per_row + v0;
       else if (err) atomicCAS(err, 0ull, 0x5000000ull | 0xFFFFFFull);
+      my_remote = (e / epr) != rank;
     }
     uint4* dsts[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       dsts[j] = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), j));
+    const unsigned remote = __ballot_sync(0xffffffffu, my_remote != 0 && my_dst != nullptr);
     if (lane == 0) {
       // the previous half row's stores must have finished reading the buffer
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -303,14 +305,23 @@ __global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
               smem_u32(buf)),
           "l"(x + t * vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bar[wib]))
           : "memory");
-      mbar_wait(&bar[wib], phase);
+    }
+    mbar_wait(&bar[wib], phase);  // every lane: the bulk load's bytes are visible
+    if (lane == 0) {
+      // local owner: bulk store straight from smem on the TMA engine
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (j < k && dsts[j] != nullptr)
+        if (j < k && dsts[j] != nullptr && !((remote >> j) & 1))
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[j]),
                        "r"(smem_u32(buf)), "r"(bytes)
                        : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    // remote owners: 16-byte P2P stores over NVLink from the staged row piece
+    for (int j = 0; j < k; ++j) {
+      if (!((remote >> j) & 1)) continue;
+      const uint4* sb = reinterpret_cast<const uint4*>(buf);
+      for (int v = lane; v < static_cast<int>(bytes / 16); v += 32) dsts[j][v] = sb[v];
     }
     phase ^= 1;
     __syncwarp();
@@ -543,7 +554,7 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
       tf::scatter_kernel<<<tf::grid_for(a->tokens * ((a->hidden / 8 + 511) / 512)), 32 * tf::kScatterWarps,
                            tf::kScatterWarps * tf::kScatterBuf, s>>>(
           static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
-          a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank));
+          a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank), rank);
     if (w > 1) tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
