@@ -614,9 +614,46 @@ def main_ours(args):
     value = total_flops / (step_ms * 1e-3) / 1e12
 
     cub_ms = None
+    overlap = None
     if not shared_gpus:  # NCCL cannot run with several ranks on one GPU
         cub_ms = 0.5 * (cub_before + time_cublas(args.steps)) if cub_before else time_cublas(args.steps)
         cub_ms = max_over_ranks([cub_ms], dev, distributed)[0]
+        if distributed:
+            # overlap efficiency, the reference's formula (simengine.py:346-352):
+            # hidden = 1 - (t_fused - t_gemm_alone) / t_comm_alone, with the GEMMs alone
+            # (cuBLAS, on the pre-gathered operand) and the collectives alone (NCCL)
+            def time_fn(fn, n):
+                with torch.cuda.stream(stream):
+                    for _ in range(2):
+                        fn()
+                    torch.cuda.synchronize()
+                    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                           for _ in range(n)]
+                    for e0, e1 in evs:
+                        flush.zero_()
+                        e0.record(stream)
+                        fn()
+                        e1.record(stream)
+                    torch.cuda.synchronize()
+                return sum(a.elapsed_time(b) for a, b in evs) / n
+
+            def gemms_only():
+                hh = torch.matmul(xg, w1.t())
+                torch.matmul(hh, w2.t(), out=hp)
+
+            def comm_only():
+                dist.all_gather_into_tensor(xg, x)
+                dist.reduce_scatter_tensor(y, hp)
+
+            t_gemm = max_over_ranks([time_fn(gemms_only, args.steps)], dev, distributed)[0]
+            t_comm = max_over_ranks([time_fn(comm_only, args.steps)], dev, distributed)[0]
+            hidden = 1.0 - (step_ms - t_gemm) / t_comm if t_comm > 0 else 0.0
+            overlap = {"t_fused_ms": round(step_ms, 4), "t_gemm_alone_ms": round(t_gemm, 4),
+                       "t_comm_alone_ms": round(t_comm, 4),
+                       "hidden_fraction": round(min(max(hidden, 0.0), 1.0), 4),
+                       "speedup_vs_serial": round((t_gemm + t_comm) / step_ms, 4),
+                       "formula": "1 - (t_fused - t_gemm_alone) / t_comm_alone (simengine.py:346-352); "
+                                  "gemm = cuBLAS, comm = NCCL all_gather + reduce_scatter"}
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -724,6 +761,7 @@ def main_ours(args):
                 "ms_per_step": round(cub_ms, 4),
                 "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
                 "speedup": round(cub_ms / step_ms, 4)},
+            "overlap": overlap,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "attention": attn, "layer": layer,
             "gpu_launches": launches_per_step * args.steps,
         }
