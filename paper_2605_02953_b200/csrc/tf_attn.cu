@@ -416,12 +416,248 @@ __global__ void __maxnreg__(168)
   }
 }
 
+
+// ---------------------------------------------------------------- CTA-pair variant
+// A cluster of two CTAs runs four 128-query tiles (two per CTA) against the same
+// key/value tiles with cta_group::2 MMAs issued by the leader: S_t = [Q_t(cta0);
+// Q_t(cta1)] K^T is one M=256 MMA whose B operand (the 128 keys) is split 64/64
+// between the two CTAs' shared memory, and O_t += P_t V is one M=256 TS-MMA (P_t
+// from each CTA's TMEM) whose B operand (V, N = 128 dims) is split 64/64.  Each CTA
+// therefore stages only half of every K and V tile, which halves the shared-memory
+// operand traffic of Q K^T -- the limiter of the single-CTA kernel.
+struct AttnPairSmem {
+  static constexpr int kQ = 2 * kHalf;        // one Q tile, 32 KB
+  static constexpr int kSlot = 16384;         // half a K tile (64 keys x 128 dims) or half a V tile (128 keys x 64 dims)
+  static constexpr int kSlots = 10;
+  static constexpr int kBars = 256;
+  static constexpr int kTotal = 1024 + 2 * kQ + kSlots * kSlot + kBars;
+};
+
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const void* tmap, uint64_t* bar,
+                                                 int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __maxnreg__(168)
+    ag_attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                            const __grid_constant__ CUtensorMap tv, const __grid_constant__ AttnParams p) {
+  using S = AttnPairSmem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sq = smem;                               // Q_A, Q_B of this CTA
+  uint8_t* sring = sq + 2 * S::kQ;                  // K0 V0 K1 V1 ... halves
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sring + S::kSlots * S::kSlot);
+  uint64_t* q_full = bars;         // leader: both CTAs' Q bytes
+  uint64_t* r_full = bars + 1;     // [10] leader: both halves of a K or V tile
+  uint64_t* r_empty = bars + 11;   // [10] each CTA (multicast commits)
+  uint64_t* s_full = bars + 21;    // [2] each CTA (multicast commits)
+  uint64_t* p_full = bars + 23;    // [2] leader: 4 softmax warps x 2 CTAs
+  uint64_t* o_ready = bars + 25;   // [2] each CTA (multicast commits)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 27);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int q0 = (blockIdx.x >> 1) * 4 * kQT + static_cast<int>(cta) * 2 * kQT;  // this CTA's two tiles
+  const int h = blockIdx.y;
+  const int g = h / (p.hq / p.hkv);
+  const int n = p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < S::kSlots; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&o_ready[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  // TMEM (each CTA, its 128 query rows): S/P_A [0,128) S/P_B [128,256) O_A [256,384) O_B [384,512)
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * S::kQ);
+      for (int t = 0; t < 2; ++t) {
+        tma_load_3d_pair(sq + t * S::kQ, &tq, q_full, 0, h, q0 + t * kQT);
+        tma_load_3d_pair(sq + t * S::kQ + kHalf, &tq, q_full, 64, h, q0 + t * kQT);
+      }
+      uint32_t ready = 0;
+      for (int c = 0; c < 2 * n; ++c) {  // K_j = 2j, V_j = 2j + 1
+        const int j = c >> 1, kv = c & 1;
+        const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
+        const int chunk = kt / p.tiles_per_chunk;
+        if (!kv && p.chunk_flags && !(ready & (1u << chunk))) {
+          wait_geq_sys(p.chunk_flags + chunk, p.epoch, p.timeout_ns, p.err,
+                       0x1000000ull | static_cast<unsigned>(chunk));
+          fence_proxy_async_global();
+          ready |= 1u << chunk;
+        }
+        const int sl = c % S::kSlots;
+        mbar_wait(&r_empty[sl], ((c / S::kSlots) & 1) ^ 1);
+        uint8_t* dst = sring + sl * S::kSlot;
+        if (leader) mbar_arrive_expect_tx(&r_full[sl], 2 * S::kSlot);
+        if (!kv) {  // this CTA's 64 keys of K_j, all 128 dims (two 64-dim boxes)
+          const int row = kt * 128 + static_cast<int>(cta) * 64;
+          tma_load_3d_pair(dst, &tk, &r_full[sl], 0, g, row);
+          tma_load_3d_pair(dst + 8192, &tk, &r_full[sl], 64, g, row);
+        } else {    // all 128 keys of V_j, this CTA's 64 dims
+          tma_load_3d_pair(dst, &tv, &r_full[sl], static_cast<int>(cta) * 64, g, kt * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(2 * kQT, 128);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(2 * kQT, kD) | (1u << 16);  // B (V) MN-major
+      auto issue_s = [&](int t, int sl) {
+        const uint32_t qa = smem_u32(sq + t * S::kQ);
+        const uint32_t kb = smem_u32(sring + sl * S::kSlot);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          umma_bf16_pair(tmem + t * 128, umma_desc_k_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32),
+                         umma_desc_k_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32), idesc_s, kk != 0);
+        umma_commit_pair_mc(&s_full[t], 0x3);
+      };
+      mbar_wait_spin(q_full, 0);
+      mbar_wait_spin(&r_full[0], 0);
+      tc_fence_after();
+      for (int t = 0; t < 2; ++t) issue_s(t, 0);
+      umma_commit_pair_mc(&r_empty[0], 0x3);
+      for (int j = 0; j < n; ++j) {
+        const int cv = 2 * j + 1, vs = cv % S::kSlots;
+        const int ck = 2 * j + 2, ks = ck % S::kSlots;
+        mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
+        if (j + 1 < n) mbar_wait_spin(&r_full[ks], (ck / S::kSlots) & 1);
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait_spin(&p_full[t], j & 1);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sring + vs * S::kSlot);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16_ts_pair(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                              umma_desc_mn_sw128(vb + kk * 2048, 16384), idesc_pv, (j | kk) != 0);
+          if (j + 1 < n) issue_s(t, ks);
+          else umma_commit_pair_mc(&o_ready[t], 0x3);
+        }
+        umma_commit_pair_mc(&r_empty[vs], 0x3);
+        if (j + 1 < n) umma_commit_pair_mc(&r_empty[ks], 0x3);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int t = (warp - 2) >> 2;                 // Q tile of this warpgroup
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + t * 128;
+    const uint32_t t_o = tmem + lane_off + 256 + t * 128;
+    const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[t]), 0);
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      mbar_wait_spin(&s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
+      tmem_ld_wait();
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(sv[c][i]));
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+      float alpha = 1.f;
+      if (mt > m + kLazyRescale) {
+        alpha = ex2(m - mt);
+        m = mt;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ov[16];
+          tmem_ld_32x32b_x16(t_o + c * 16, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st_32x32b_x16(t_o + c * 16, ov);
+        }
+      }
+      float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m));
+          const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m));
+          sacc[i & 3] += p0 + p1;
+          sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
+        }
+      l = l * alpha + ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]));
+      tmem_st_32x32b_x32(t_s, sv[0]);
+      tmem_st_32x32b_x32(t_s + 32, sv[1]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full_leader);
+    }
+    mbar_wait_spin(&o_ready[t], 0);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const int q = q0 + t * kQT + row;
+    uint16_t* dst = static_cast<uint16_t*>(p.out) + (static_cast<long long>(q) * p.hq + h) * kD;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t ov[32];
+      tmem_ld_32x32b_x32(t_o + c * 32, ov);
+      tmem_ld_wait();
+      if (q < p.s_local) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int make_tmap_3d(CUtensorMap* map, const void* base, int64_t rows, int64_t heads) {
+int make_tmap_3d(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int box_rows = 128) {
   static EncodeTiledFn enc = nullptr;
   if (!enc) {
     void* ptr = nullptr;
@@ -434,7 +670,7 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int64_t rows, int64_t heads
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(kD), static_cast<cuuint64_t>(heads),
                         static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(kD * 2), static_cast<cuuint64_t>(heads * kD * 2)};
-  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -509,10 +745,16 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
         if (rc) return rc;
       }
     }
+    // CTA-pair variant (TF_ATTN_PAIR=1) when the local sequence splits into groups of
+    // 4 query tiles; measured slower than the single-CTA kernel at config 3 (4.75 vs
+    // 3.88 ms/rank: the pair's softmax warpgroups run in lockstep across two SMs), so
+    // it is opt-in
+    const char* pair_env = getenv("TF_ATTN_PAIR");
+    const bool pair = pair_env && atoi(pair_env) && sl % (4 * tf::kQT) == 0;
     CUtensorMap tq, tk, tv;
     rc = tf::make_tmap_3d(&tq, a->q, sl, a->hq);
     if (rc) return rc;
-    rc = tf::make_tmap_3d(&tk, kbuf, st, a->hkv);
+    rc = tf::make_tmap_3d(&tk, kbuf, st, a->hkv, pair ? 64 : 128);
     if (rc) return rc;
     rc = tf::make_tmap_3d(&tv, vbuf, st, a->hkv);
     if (rc) return rc;
@@ -537,10 +779,28 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
       TF_CUDA_TRY(cudaFuncSetAttribute(tf::ag_attn_fwd_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        tf::AttnSmem::kTotal));
+      TF_CUDA_TRY(cudaFuncSetAttribute(tf::ag_attn_fwd_pair_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tf::AttnPairSmem::kTotal));
       attr_done |= 1ull << dev;
     }
+    if (pair) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(static_cast<unsigned>(2 * sl / (4 * tf::kQT)), static_cast<unsigned>(a->hq));
+      cfg.blockDim = dim3(tf::kAttnThreads2);
+      cfg.dynamicSmemBytes = tf::AttnPairSmem::kTotal;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf::ag_attn_fwd_pair_kernel, tq, tk, tv, p));
+    }
     dim3 grid(static_cast<unsigned>((sl + 2 * tf::kQT - 1) / (2 * tf::kQT)), static_cast<unsigned>(a->hq));
-    tf::ag_attn_fwd_kernel<<<grid, tf::kAttnThreads2, tf::AttnSmem::kTotal, s>>>(tq, tk, tv, p);
+    if (!pair) tf::ag_attn_fwd_kernel<<<grid, tf::kAttnThreads2, tf::AttnSmem::kTotal, s>>>(tq, tk, tv, p);
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
       cudaFuncAttributes fa{};

@@ -70,8 +70,11 @@ def test_ag_kv_scores_validation():
 
 
 @pytest.mark.parametrize("world,sl,hq,hkv", [(1, 128, 1, 1), (1, 256, 2, 1), (2, 128, 4, 2),
-                                             (4, 256, 8, 1), (8, 128, 8, 8)])
-def test_ag_kv_attention_vs_oracle(world, sl, hq, hkv):
+                                             (4, 256, 8, 1), (8, 128, 8, 8),
+                                             (1, 512, 2, 1), (2, 512, 4, 2), (4, 1024, 8, 2)])
+@pytest.mark.parametrize("pair", ["0", "1"])  # TF_ATTN_PAIR=1: CTA-pair kernel when s_local % 512 == 0
+def test_ag_kv_attention_vs_oracle(world, sl, hq, hkv, pair, monkeypatch):
+    monkeypatch.setenv("TF_ATTN_PAIR", pair)
     from paper_2605_02953_b200.attention import ag_kv_attention
     rng = np.random.default_rng(world * 7 + sl + hq)
     d = 128
