@@ -14,9 +14,11 @@
 //                 boxes, 3-stage ring     and [256,512); half 1      per half, release the
 //                                         lags 2 k-blocks at tile    tile flag
 //                                         edges (drain overlaps)
-//   attention     wait deps, Q once, K/V  S = Q K^T, O += P V        online softmax (causal
-//                 tiles through a 5-slot  (P from TMEM, V MN-major)  mask, lazy rescale),
-//                 ring, K one tile ahead                             P -> TMEM, O / l -> bf16
+//   attention     wait deps, Q of two    per head: S = Q K^T, then  online softmax per head
+//   (2 heads of   heads once, K/V tiles  O += P V (P from TMEM,     (causal mask, lazy
+//   a KV group)   through a 4-slot ring  V MN-major) and the next   rescale), P -> TMEM;
+//                                        S in the same columns      one head's softmax
+//                                                                   overlaps the other's MMAs
 //   rmsnorm       -                       -                          - (warps 6-7: wait deps,
 //                                                                      y = x*rstd*g)
 //   allreduce_    -                       -                          - (warps 6-7: wait deps on
@@ -54,10 +56,10 @@ constexpr int kBStage = 256 * 64 * 2;         // 32 KB
 constexpr int kStage = kAStage + kBStage;     // 64 KB
 constexpr int kRegion = kRing * kStage;       // 192 KB
 constexpr int kLag = 2;                       // k-blocks the second M-half trails at tile edges
-constexpr int kQOff = 0;                      // attention aliases
-constexpr int kKVOff = 2 * kHalfBox;          // ring of 4 K-or-V slots (32 KB each)
+constexpr int kQOff = 0;                      // attention aliases: Q of up to 2 heads (64 KB)
+constexpr int kKVOff = 4 * kHalfBox;          // ring of 4 K-or-V slots (32 KB each)
 constexpr int kKVSlot = 2 * kHalfBox;
-constexpr int kKVSlots = 5;                   // P lives in TMEM (over its S buffer), not smem
+constexpr int kKVSlots = 4;                   // P lives in TMEM (over its S buffer), not smem
 constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag before O is rescaled
 constexpr int kLayerSmem = 1024 + kRegion + 512;
 constexpr int kCfgInts = 16;
@@ -162,18 +164,6 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr, long long bytes, in
   }
 }
 
-// position of K_j (kv = 0) / V_j (kv = 1) in a task's load sequence K0 K1 V0 K2 V1 ... K_{n-1}
-// V_{n-2} V_{n-1}: K runs one tile ahead so slots refill two MMA steps before use
-__device__ __forceinline__ int ring_index(int j, int kv, int n) {
-  if (!kv) return j == 0 ? 0 : 2 * j - 1;
-  return j <= n - 2 ? 2 * j + 2 : 2 * n - 1;
-}
-__device__ __forceinline__ void ring_decode(int c, int n, int& j, int& kv) {
-  if (c == 0) { j = 0; kv = 0; return; }
-  if (c == 2 * n - 1) { j = n - 1; kv = 1; return; }
-  if (c & 1) { j = (c + 1) / 2; kv = 0; } else { j = (c - 2) / 2; kv = 1; }
-}
-
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -249,17 +239,20 @@ __device__ __forceinline__ void store_bf16x32(uint16_t* dst, const float (&f)[32
 }
 
 struct AttnGeom {
-  int n_kv, kv0, hq, hkv, g, h, q_row0;
+  int n_kv, kv0, hq, hkv, g, h, q_row0, np;
 };
 
+// task = (128-query tile i, heads [h, h + np)) with np = 1 or 2 heads of one KV group
 __device__ __forceinline__ AttnGeom attn_geom(const int* cfg, const Rec& r) {
   AttnGeom a;
   a.hq = cfg[7];
   a.hkv = cfg[8];
+  a.np = cfg[14] > 1 ? 2 : 1;
   const int seq = cfg[9];
   const int causal = cfg[12];
-  const int i = r.tile / a.hq;
-  a.h = r.tile % a.hq;
+  const int per_row = a.hq / a.np;
+  const int i = r.tile / per_row;
+  a.h = (r.tile % per_row) * a.np;
   a.g = a.h / (a.hq / a.hkv);
   a.q_row0 = i * 128;
   const int tiles_per_seq = seq / 128;
@@ -281,10 +274,9 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
   uint64_t* q_empty = bars + 13;
   uint64_t* kv_full = bars + 28;        // [5] ring slots
   uint64_t* kv_empty = bars + 34;       // [5]
-  uint64_t* s_full = bars + 18;         // [2]
-  uint64_t* s_empty = bars + 20;        // [2]
-  uint64_t* p_full = bars + 22;
-  uint64_t* pv_done = bars + 23;
+  uint64_t* s_full = bars + 18;         // [2] per head stream
+  uint64_t* o_ready = bars + 20;        // [2]
+  uint64_t* p_full = bars + 22;         // [2]
   uint64_t* o_empty = bars + 24;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
@@ -303,7 +295,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&o_ready[i], 1);
+      mbar_init(&p_full[i], 4);
     }
     for (int i = 0; i < kKVSlots; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -311,8 +304,6 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     mbar_init(o_empty, 4);
     fence_barrier_init();
   }
@@ -372,12 +363,13 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         if (lane == 0) {
           if (waited) fence_proxy_async_global();
           mbar_wait(q_empty, (att_it & 1) ^ 1);
-          mbar_arrive_expect_tx(q_full, 2 * kHalfBox);
-          tma_load_3d_l(smem + kQOff, mq, q_full, 0, a.h, a.q_row0);
-          tma_load_3d_l(smem + kQOff + kHalfBox, mq, q_full, 64, a.h, a.q_row0);
-          for (int c = 0; c < 2 * a.n_kv; ++c) {
-            int j, kv;
-            ring_decode(c, a.n_kv, j, kv);
+          mbar_arrive_expect_tx(q_full, a.np * 2 * kHalfBox);
+          for (int t = 0; t < a.np; ++t) {
+            tma_load_3d_l(smem + kQOff + t * 2 * kHalfBox, mq, q_full, 0, a.h + t, a.q_row0);
+            tma_load_3d_l(smem + kQOff + t * 2 * kHalfBox + kHalfBox, mq, q_full, 64, a.h + t, a.q_row0);
+          }
+          for (int c = 0; c < 2 * a.n_kv; ++c) {  // K_j = 2j, V_j = 2j + 1
+            const int j = c >> 1, kv = c & 1;
             const int gc = ring_base + c, sl = gc % kKVSlots;
             mbar_wait(&kv_empty[sl], ((gc / kKVSlots) & 1) ^ 1);
             uint8_t* dst = smem + kKVOff + sl * kKVSlot;
@@ -471,51 +463,57 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         __syncwarp();
         ++lin_it;
       } else {
+        // per head stream t: S_t(0); then for each key tile j: PV_t(j) (A = P_t from TMEM)
+        // and S_t(j+1) into the same columns -- in that order on the in-order tensor pipe,
+        // so S_t(j+1) overwrites P_t(j) only after PV_t(j) read it and "S_t(j+1) complete"
+        // implies "PV_t(j) complete".  With two heads the softmax of one head overlaps the
+        // other head's PV + QK^T.
         const AttnGeom a = attn_geom(cfg, r);
-        const int n = a.n_kv;
+        const int n = a.n_kv, np = a.np;
         mbar_wait(q_full, att_it & 1);
         mbar_wait(o_empty, (att_it & 1) ^ 1);
         tc_fence_after();
-        auto issue_pv = [&](int gi, int jl) {
-          const int gc = ring_base + ring_index(jl, 1, n), st = gc % kKVSlots;
-          mbar_wait(&kv_full[st], (gc / kKVSlots) & 1);
-          mbar_wait(p_full, gi & 1);
-          tc_fence_after();
-          if (lane == 0) {
-            // A = P from tensor memory (packed bf16 over the first 64 columns of S[gi & 1])
-            const uint32_t pa = tmem + (gi & 1) * 128;
-            const uint32_t vb = smem_u32(smem + kKVOff + st * kKVSlot);
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-              umma_bf16_ts(t_o, pa + kk * 8, desc_mn_sw128(vb + kk * 2048, kHalfBox), idesc_pv, (jl | kk) != 0);
-            umma_commit(&kv_empty[st]);
-            umma_commit(pv_done);
-          }
-          __syncwarp();
-        };
-        for (int j = 0; j < n; ++j) {
-          const int gi = kv_it + j, st = gi & 1;
-          const int gc = ring_base + ring_index(j, 0, n), ks = gc % kKVSlots;
-          mbar_wait(&kv_full[ks], (gc / kKVSlots) & 1);
-          mbar_wait(&s_empty[st], ((gi >> 1) & 1) ^ 1);
-          tc_fence_after();
-          if (lane == 0) {
-            const uint32_t qa = smem_u32(smem + kQOff);
-            const uint32_t kb = smem_u32(smem + kKVOff + ks * kKVSlot);
+        if (lane == 0) {
+          auto issue_s = [&](int t, int sl) {
+            const uint32_t qa = smem_u32(smem + kQOff + t * 2 * kHalfBox);
+            const uint32_t kb = smem_u32(smem + kKVOff + sl * kKVSlot);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t off = (kk >> 2) * kHalfBox + (kk & 3) * 32;
-              umma_bf16(tmem + st * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off),
+              umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off),
                         idesc_s, kk != 0);
             }
-            umma_commit(&s_full[st]);
-            umma_commit(&kv_empty[ks]);
-            if (j == n - 1) umma_commit(q_empty);
+            umma_commit(&s_full[t]);
+          };
+          {
+            const int gc = ring_base, sl = gc % kKVSlots;
+            mbar_wait(&kv_full[sl], (gc / kKVSlots) & 1);
+            tc_fence_after();
+            for (int t = 0; t < np; ++t) issue_s(t, sl);
+            umma_commit(&kv_empty[sl]);
           }
-          __syncwarp();
-          if (j > 0) issue_pv(gi - 1, j - 1);
+          for (int j = 0; j < n; ++j) {
+            const int gv = ring_base + 2 * j + 1, vs = gv % kKVSlots;
+            const int gk = ring_base + 2 * j + 2, ks = gk % kKVSlots;
+            mbar_wait(&kv_full[vs], (gv / kKVSlots) & 1);
+            if (j + 1 < n) mbar_wait(&kv_full[ks], (gk / kKVSlots) & 1);
+            for (int t = 0; t < np; ++t) {
+              mbar_wait(&p_full[t], (kv_it + j) & 1);
+              tc_fence_after();
+              const uint32_t vb = smem_u32(smem + kKVOff + vs * kKVSlot);
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk)
+                umma_bf16_ts(t_o + t * 128, tmem + t * 128 + kk * 8, desc_mn_sw128(vb + kk * 2048, kHalfBox),
+                             idesc_pv, (j | kk) != 0);
+              if (j + 1 < n) issue_s(t, ks);
+              else umma_commit(&o_ready[t]);
+            }
+            umma_commit(&kv_empty[vs]);
+            if (j + 1 < n) umma_commit(&kv_empty[ks]);
+          }
+          umma_commit(q_empty);
         }
-        issue_pv(kv_it + n - 1, n - 1);
+        __syncwarp();
         kv_it += n;
         ring_base += 2 * n;
         ++att_it;
@@ -534,7 +532,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     const int et = threadIdx.x - (elem_grp ? 192 : 64);  // thread index in the group
     const int nw = gthreads / 32;
     const int ew = warp - (elem_grp ? 6 : 2);            // warp index in the group
-    int lin_it = 0, kv_it = 0;
+    int lin_it = 0, kv_it = 0, att_it = 0;
     for (int idx = 0; idx < n_tasks; ++idx) {
       Rec r;
       load_rec(p, idx, sm, r);
@@ -631,103 +629,99 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         ++lin_it;
       } else if (op == OP_ATTENTION) {
         const AttnGeom a = attn_geom(cfg, r);
-        const int n = a.n_kv;
+        const int n = a.n_kv, np = a.np;
         const int causal = __ldg(cfg + 12);
         const float scale_log2 = __int_as_float(__ldg(cfg + 10)) * 1.4426950408889634f;
-        const uint32_t t_o = tmem + 256;
-        float mrow = -INFINITY, l = 0.f;
+        float mrow[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
         for (int j = 0; j < n; ++j) {
-          const int gi = kv_it + j, st = gi & 1;
-          mbar_wait(&s_full[st], (gi >> 1) & 1);
-          tc_fence_after();
-          uint32_t sv[4][32];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + lane_off + st * 128 + c * 32, sv[c]);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[st]);
-          if (causal && j == n - 1) {  // diagonal tile only (warp-uniform branch)
+          for (int t = 0; t < 2; ++t) {
+            if (t >= np) break;
+            const uint32_t t_s = tmem + lane_off + t * 128;
+            const uint32_t t_ot = tmem + lane_off + 256 + t * 128;
+            mbar_wait(&s_full[t], (kv_it + j) & 1);
+            tc_fence_after();
+            uint32_t sv[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
+            tmem_ld_wait();
+            if (causal && j == n - 1) {  // diagonal tile only (warp-uniform branch)
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (c * 32 + i > row) sv[c][i] = __float_as_uint(-INFINITY);
+            }
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
             for (int c = 0; c < 4; ++c)
 #pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (c * 32 + i > row) sv[c][i] = __float_as_uint(-INFINITY);
-          }
-          float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              mx0 = fmaxf(mx0, __uint_as_float(sv[c][i]));
-              mx1 = fmaxf(mx1, __uint_as_float(sv[c][i + 1]));
+              for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(sv[c][i]));
+            const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+            // lazy rescale: the running max may lag the true max by up to 2^8
+            float alpha = 1.f;
+            if (mt > mrow[t] + kLazyRescale) {
+              alpha = ex2(mrow[t] - mt);
+              mrow[t] = mt;
             }
-          const float mt = fmaxf(mx0, mx1) * scale_log2;
-          // lazy rescale: the running max may lag the true max by up to 2^8
-          float alpha = 1.f;
-          if (mt > mrow + kLazyRescale) {
-            alpha = ex2(mrow - mt);
-            mrow = mt;
-          }
-          float s0 = 0.f, s1 = 0.f;
-          // P packed in place: pair (2i, 2i+1) of chunk c -> sv[c / 2][(c % 2) * 16 + i]
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -mrow));
-              const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -mrow));
-              s0 += p0;
-              s1 += p1;
-              sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
-            }
-          l = l * alpha + (s0 + s1);
-          if (j > 0) {
-            mbar_wait(pv_done, (gi - 1) & 1);
-            tc_fence_after();
-            if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            // O_t is stable (S_t(j) complete => PV_t(j-1) complete); rescale before P_t(j)
+            if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
               for (int c = 0; c < 4; ++c) {
                 uint32_t ov[32];
-                tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
+                tmem_ld_32x32b_x32(t_ot + c * 32, ov);
                 tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-                tmem_st_x32(t_o + lane_off + c * 32, ov);
+                tmem_st_x32(t_ot + c * 32, ov);
               }
-              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             }
-          }
-          // P(j) over the first 64 columns of its own S buffer (S(j) is in registers; the
-          // next write of this buffer, S(j+2), is issued after PV(j) on the in-order pipe)
-          tmem_st_x32(tmem + lane_off + st * 128, sv[0]);
-          tmem_st_x32(tmem + lane_off + st * 128 + 32, sv[1]);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(p_full);
-        }
-        mbar_wait(pv_done, (kv_it + n - 1) & 1);
-        tc_fence_after();
-        const float inv = 1.f / l;
-        const int ldo = r.d1[1];
-        uint16_t* dst = reinterpret_cast<uint16_t*>(my_base + r.off[1]) +
-                        static_cast<long long>(a.q_row0 + row) * ldo + a.h * 128;
-        const bool row_ok = a.q_row0 + row < r.d0[1];
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t ov[32];
-          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, ov);
-          tmem_ld_wait();
-          float o[32];
+            float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+            // P packed in place: pair (2i, 2i+1) of chunk c -> sv[c / 2][(c % 2) * 16 + i]
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(ov[i]) * inv;
-          if (row_ok) store_bf16x32(dst + c * 32, o, 32);
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale_log2, -mrow[t]));
+                const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale_log2, -mrow[t]));
+                sacc[i & 3] += p0 + p1;
+                sv[c >> 1][(c & 1) * 16 + i] = pack_bf16x2(p0, p1);
+              }
+            l[t] = l[t] * alpha + ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3]));
+            tmem_st_x32(t_s, sv[0]);
+            tmem_st_x32(t_s + 32, sv[1]);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[t]);
+          }
+        }
+        const int ldo = r.d1[1];
+        const bool row_ok = a.q_row0 + row < r.d0[1];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (t >= np) break;
+          mbar_wait(&o_ready[t], att_it & 1);
+          tc_fence_after();
+          const float inv = 1.f / l[t];
+          uint16_t* dst = reinterpret_cast<uint16_t*>(my_base + r.off[1]) +
+                          static_cast<long long>(a.q_row0 + row) * ldo + (a.h + t) * 128;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            tmem_ld_32x32b_x32(tmem + lane_off + 256 + t * 128 + c * 32, ov);
+            tmem_ld_wait();
+            float o[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(ov[i]) * inv;
+            if (row_ok) store_bf16x32(dst + c * 32, o, 32);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(o_empty);
         kv_it += n;
+        ++att_it;
       } else {
         // ------------------------------------------------ elementwise tasks (warps 6-7)
         // two-shot allreduce: row block b is reduced once, by rank b % world, which

@@ -157,9 +157,10 @@ def plan_allreduce_residual(io, config) -> MK.LayerPlan:
 def plan_attention(io, config) -> MK.LayerPlan:
     """Flash-attention forward over a fused qkv [T, (hq + 2 hkv) * 128] buffer
     (q heads, then k heads, then v heads), out [T, hq * 128]; sequences of
-    `seq_len` rows, causal by default.  Tile (i, h) = query rows [128 i, 128 i + 128)
-    of head h, tile id i * hq + h; emitted longest-first (descending i) so the
-    static round-robin queues start with the long causal rows."""
+    `seq_len` rows, causal by default.  Tile (i, p) = query rows [128 i, 128 i + 128)
+    of heads [p * np, p * np + np) (np = heads_per_task, 2 by default when the GQA
+    group is even), tile id i * hq / np + p; emitted longest-first (descending i) so
+    the static round-robin queues start with the long causal rows."""
     (qkv,), (o,) = io[0], io[1]
     cfg = {"heads_q": None, "heads_kv": None, "seq_len": None, "causal": True, **config}
     hq, hkv = cfg["heads_q"], cfg["heads_kv"]
@@ -175,24 +176,30 @@ def plan_attention(io, config) -> MK.LayerPlan:
         raise BuildError("seq_len must be a multiple of 128 dividing the token count")
     tps = seq // 128
     grp = hq // hkv
+    # two heads of one KV group per task when possible: they share every K/V tile and
+    # the device overlaps one head's softmax with the other head's MMAs
+    npt = cfg.get("heads_per_task") or (2 if grp % 2 == 0 else 1)
+    if npt not in (1, 2) or (npt == 2 and grp % 2):
+        raise BuildError("heads_per_task must be 1, or 2 with an even GQA group")
+    cfg["heads_per_task"] = npt
+    per_row = hq // npt
     tiles = []
     for i in sorted(range(t_rows // 128), key=lambda i: (-(i % tps), i)) if cfg["causal"] else range(t_rows // 128):
         kv0 = (i // tps) * tps
         n_kv = i - kv0 + 1 if cfg["causal"] else tps
-        for h in range(hq):
+        for hp in range(per_row):
+            h = hp * npt
             g = h // grp
-            kv_rows = dict(start_indices=(kv0 * 128, 0), data_sizes=(n_kv * 128, HEAD_DIM))
             deps = (
-                MK.InputDependencyDesc(qkv, start_indices=(i * 128, h * HEAD_DIM), data_sizes=(128, HEAD_DIM)),
+                MK.InputDependencyDesc(qkv, start_indices=(i * 128, h * HEAD_DIM), data_sizes=(128, npt * HEAD_DIM)),
                 MK.InputDependencyDesc(qkv, start_indices=(kv0 * 128, (hq + g) * HEAD_DIM),
                                        data_sizes=(n_kv * 128, HEAD_DIM)),
                 MK.InputDependencyDesc(qkv, start_indices=(kv0 * 128, (hq + hkv + g) * HEAD_DIM),
                                        data_sizes=(n_kv * 128, HEAD_DIM)),
             )
-            del kv_rows
-            tiles.append(MK.TileSpec(i * hq + h, deps))
-    return MK.LayerPlan("attention", io, cfg, (t_rows // 128) * hq, tiles,
-                        {o.name: MK.OutputTilingDesc((128, HEAD_DIM))})
+            tiles.append(MK.TileSpec(i * per_row + hp, deps))
+    return MK.LayerPlan("attention", io, cfg, (t_rows // 128) * per_row, tiles,
+                        {o.name: MK.OutputTilingDesc((128, npt * HEAD_DIM))})
 
 
 _ref_plan_linear = MK.get_task_builder("linear").plan
@@ -250,6 +257,7 @@ def layer_tables(program: MK.MegaProgram, built: MK.BuiltGraph):
             row[7], row[8], row[9] = hq, hkv, c["seq_len"]
             row[10] = _f32_bits(c["scale"])
             row[12] = 1 if c["causal"] else 0
+            row[14] = c["heads_per_task"]
         elif op == "rmsnorm":
             row[11] = _f32_bits(c["eps"])
         elif op == "allreduce_residual":

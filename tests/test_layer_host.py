@@ -26,20 +26,22 @@ def test_llama_graph_dependencies():
     for t in built.tasks:
         by.setdefault(t.task_id, []).append(t)
     hq = 4
-    # attention (layer 2): tile (i, h) waits on the 256-row QKV tiles of rows <= i in its sequence
+    # attention (layer 2): tile (i, head pair) waits on the 256-row QKV tiles of rows <= i
+    assert built.layer_configs[2]["heads_per_task"] == 2
+    per_row = hq // 2
     for t in by[2]:
-        i, h = divmod(t.tile_id, hq)
+        i, hp = divmod(t.tile_id, per_row)
         rows = {int(lo) // 3 for p, lo, hi in built.dep_table[t.dep_start:t.dep_end] if p == 1}
         seq0 = (i // 2) * 2
         assert rows == set(range(seq0 // 2, i // 2 + 1)), (i, rows)
     # emitted longest-first
-    firsts = [t.tile_id // hq for t in by[2]]
+    firsts = [t.tile_id // per_row for t in by[2]]
     assert firsts[0] % 2 == 1 and firsts[-1] % 2 == 0
-    # o-proj tile (tm, tn) waits on every head of the two query tiles of its 256 rows
+    # o-proj tile (tm, tn) waits on every head pair of the two query tiles of its 256 rows
     for t in by[3]:
         rows = [tuple(r) for r in built.dep_table[t.dep_start:t.dep_end]]
         tm = t.tile_id // 2
-        assert rows == [(2, 2 * tm * hq, 2 * tm * hq + hq), (2, (2 * tm + 1) * hq, (2 * tm + 2) * hq)]
+        assert rows == [(2, 2 * tm * per_row, (2 * tm + 1) * per_row), (2, (2 * tm + 1) * per_row, (2 * tm + 2) * per_row)]
     # allreduce_residual rows depend on their o_part and x rows only
     for t in by[4]:
         prods = {int(r[0]) for r in built.dep_table[t.dep_start:t.dep_end]}
