@@ -127,7 +127,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
-def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512):
+def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512, min_seconds: float = 0.0):
     """Oracle (numpy) MLP step on a bounded sample: `rows` tokens instead of 8192,
     fp32, all host threads.  Returns (TFLOP/s, seconds, cores, sample text)."""
     import numpy as np
@@ -143,10 +143,12 @@ def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512):
     flops = 2 * 2 * (mpr * tp) * HIDDEN * FFN
     O.ref_allgather_gemm(x, w1[:1])  # warm
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < steps or time.perf_counter() - t0 < min_seconds:
         h = O.ref_allgather_gemm(x, w1)
         O.ref_reduce_scatter(h, w2)
-    dt = (time.perf_counter() - t0) / steps
+        done += 1
+    dt = (time.perf_counter() - t0) / done
     sample = (f"oracle ref_allgather_gemm + ref_reduce_scatter (numpy fp32, OpenBLAS) on "
               f"{mpr * tp} of {TOKENS} tokens, TP={tp}, hidden {HIDDEN}, ffn {FFN}")
     return flops / dt / 1e12, dt, cores, sample
@@ -361,21 +363,7 @@ def bench_layer(dev, steps, warmup, peaks, flush, tp_emulated=1):
     for name, val in [("x", x), ("g_attn", g1), ("g_mlp", g2), ("rope", rope), *w.items()]:
         runner.view(name).copy_(val)
     stream = torch.cuda.current_stream(dev)
-    for _ in range(warmup):
-        runner.run(stream)
-    torch.cuda.synchronize(dev)
-    runner.check()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for e0, e1 in evs:
-        flush.zero_()
-        e0.record(stream)
-        runner.run(stream)
-        e1.record(stream)
-    torch.cuda.synchronize(dev)
-    runner.check()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     flops = layer_flops(T, H, HQ, HKV, FF)
-    out_fused = runner.view("out").clone()
 
     # ---- unfused comparator on the same tensors (gate/up de-interleaved for torch)
     wgu = w["w_gate_up"].view(FF // 128, 2, 128, H)
@@ -407,18 +395,31 @@ def bench_layer(dev, steps, warmup, peaks, flush, tp_emulated=1):
         act = F.silu(hn @ wg.t()) * (hn @ wu.t())
         return act @ w["w_down"].t() + h
 
-    ref = None
-    for _ in range(2):
+    # warm both, then alternate fused / unfused steps so both see the same clocks and
+    # temperature (the launch is energy-bound at the 1 kW cap); L2 flushed before each
+    for _ in range(warmup):
+        runner.run(stream)
         ref = unfused()
     torch.cuda.synchronize(dev)
+    runner.check()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     cevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for e0, e1 in cevs:
+    for (e0, e1), (c0, c1) in zip(evs, cevs):
         flush.zero_()
         e0.record(stream)
-        unfused()
+        runner.run(stream)
         e1.record(stream)
+        flush.zero_()
+        c0.record(stream)
+        unfused()
+        c1.record(stream)
     torch.cuda.synchronize(dev)
+    runner.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
     cms = sum(a.elapsed_time(b) for a, b in cevs) / steps
+    out_fused = runner.view("out").clone()
+    ref = unfused()
+    torch.cuda.synchronize(dev)
     rel = float((out_fused.float() - ref.float()).abs().max() / ref.float().abs().max())
     n_tasks = len(runner.built.tasks)
     runner.close()
@@ -725,16 +726,11 @@ def main_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
-        # repeat the bounded sample for ~10 s of CPU work; report the median step
-        vals, t_cpu = [], time.perf_counter()
-        while True:
-            v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=1024)
-            vals.append(v)
-            if time.perf_counter() - t_cpu > 10.0 or len(vals) >= 200:
-                break
-        cpu = {"value": round(statistics.median(vals), 6), "unit": "TFLOP/s", "cores": cores,
-               "kind": "port", "sample": sample + f"; {len(vals)} repeats, median "
-               f"({time.perf_counter() - t_cpu:.1f} s of CPU work)", "seconds_per_sample": round(dt, 3)}
+        # the bounded sample repeated for >= 10 s of timed CPU work (mean step)
+        v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=1024, min_seconds=10.0)
+        cpu = {"value": round(v, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": sample + "; repeated for >= 10 s of timed CPU work",
+               "seconds_per_step": round(dt, 3)}
 
     moe = None
     if not args.no_moe:
