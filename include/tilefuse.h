@@ -114,6 +114,16 @@ int tf_putmem(tf_team* t, int to_pe, uint64_t dst_off, const void* src, size_t n
 int tf_getmem(tf_team* t, int from_pe, uint64_t src_off, void* dst, size_t nbytes, void* stream);
 int tf_putmem_signal(tf_team* t, int to_pe, uint64_t dst_off, const void* src, size_t nbytes,
                      uint64_t sig_slot, uint64_t value, int op_add, void* stream);
+/* multimem_ld_reduce (shmem.py:335-351): out[i] = sum over the team's PEs, in
+ * ascending rank order, of the element at `offset` + i in each PE's heap copy;
+ * dtype 0 bf16 (fp32 accumulation, bf16 out), 1 fp32, 2 int64 (exact).  `out` is a
+ * device buffer on the caller's device; peers are read over P2P (NVLink).
+ * multimem_st (shmem.py:353-361): copy `src` into every PE's copy at `offset`
+ * (one copy-engine transfer per PE).  Both stream-ordered on `stream`. */
+int tf_team_reduce(tf_team* t, int pe, uint64_t offset, int dtype, int64_t count, void* out,
+                   void* stream);
+int tf_team_broadcast(tf_team* t, int from_pe, uint64_t offset, const void* src, size_t nbytes,
+                      void* stream);
 /* st / notify / atomic_add on a signal slot of PE pe (shmem.py:174-194). */
 int tf_signal_op(tf_team* t, int pe, uint64_t slot, uint64_t value, int op_add, void* stream);
 /* wait (shmem.py:208-235): stream waits until all n slots >= value. */

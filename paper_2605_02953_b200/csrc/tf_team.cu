@@ -171,6 +171,37 @@ tf::Workspace* tf_team::workspace(const std::string& key, size_t data_bytes, siz
 }
 
 
+
+namespace tf {
+struct ReducePtrs {
+  const uint8_t* p[kMaxWorld];
+};
+// out[i] = sum over PEs (ascending) of PE q's element i; bf16 accumulates in fp32
+template <int DT>
+__global__ void team_reduce_kernel(ReducePtrs src, int world, int64_t count, void* out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (DT == 0) {
+      float acc = 0.f;
+      for (int q = 0; q < world; ++q)
+        acc += __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(src.p[q])[i]) << 16);
+      // round to nearest even
+      uint32_t b = __float_as_uint(acc);
+      b += 0x7FFFu + ((b >> 16) & 1u);
+      static_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(b >> 16);
+    } else if (DT == 1) {
+      float acc = 0.f;
+      for (int q = 0; q < world; ++q) acc += reinterpret_cast<const float*>(src.p[q])[i];
+      static_cast<float*>(out)[i] = acc;
+    } else {
+      long long acc = 0;
+      for (int q = 0; q < world; ++q) acc += reinterpret_cast<const long long*>(src.p[q])[i];
+      static_cast<long long*>(out)[i] = acc;
+    }
+  }
+}
+}  // namespace tf
+
 extern "C" {
 
 const char* tf_last_error(void) { return tf::last_error_cstr(); }
@@ -446,6 +477,40 @@ int tf_getmem(tf_team* t, int from_pe, uint64_t src_off, void* dst, size_t nbyte
   if (nbytes == 0) return TF_OK;
   TF_CUDA_TRY(cudaMemcpyAsync(dst, t->pes[from_pe].base + src_off, nbytes, cudaMemcpyDefault,
                               static_cast<cudaStream_t>(stream)));
+  return TF_OK;
+}
+
+int tf_team_reduce(tf_team* t, int pe, uint64_t offset, int dtype, int64_t count, void* out,
+                   void* stream) {
+  if (!t || pe < 0 || pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
+  if (dtype < 0 || dtype > 2) return fail(TF_ERR_INVALID, "dtype must be 0 (bf16), 1 (fp32) or 2 (int64)");
+  const int esz = dtype == 0 ? 2 : dtype == 1 ? 4 : 8;
+  if (count < 0 || offset + static_cast<uint64_t>(count) * esz > t->heap_bytes)
+    return fail(TF_ERR_INVALID, "range exceeds the heap");
+  if (count == 0) return TF_OK;
+  if (offset % esz) return fail(TF_ERR_INVALID, "offset must be aligned to the element size");
+  tf::ReducePtrs src{};
+  for (int q = 0; q < t->world; ++q) src.p[q] = t->pes[q].base + offset;
+  const int threads = 256;
+  const int64_t blocks64 = std::min<int64_t>((count + threads - 1) / threads, 148 * 16);
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(blocks64, 1));
+  auto s = static_cast<cudaStream_t>(stream);
+  if (dtype == 0) tf::team_reduce_kernel<0><<<blocks, threads, 0, s>>>(src, t->world, count, out);
+  else if (dtype == 1) tf::team_reduce_kernel<1><<<blocks, threads, 0, s>>>(src, t->world, count, out);
+  else tf::team_reduce_kernel<2><<<blocks, threads, 0, s>>>(src, t->world, count, out);
+  TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}
+
+int tf_team_broadcast(tf_team* t, int from_pe, uint64_t offset, const void* src, size_t nbytes,
+                      void* stream) {
+  if (!t || from_pe < 0 || from_pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
+  if (offset + nbytes > t->heap_bytes) return fail(TF_ERR_INVALID, "range exceeds the heap");
+  for (int q = 0; q < t->world; ++q) {
+    const int pe = (from_pe + q) % t->world;  // own copy first, then the ring order
+    int rc = tf_putmem(t, pe, offset, src, nbytes, stream);
+    if (rc) return rc;
+  }
   return TF_OK;
 }
 

@@ -334,6 +334,66 @@ class SymmetricHeap:
         """Ordering of puts from one stream is already issue-order (copy engine queue)."""
         self._check_pe(from_pe)
 
+    # ------------------------------------------------------------------ node-team collectives
+    # multimem_ld_reduce / multimem_st (shmem.py:335-385): on one NVSwitch box the node
+    # team is every PE.  The reduce reads each PE's copy over P2P and sums in ascending
+    # rank order (bf16 in fp32, fp32, int64 exact); the broadcast is one copy-engine
+    # transfer per PE.  Host-initiated and stream-ordered; results are device tensors.
+    _RED_CODES = {torch.bfloat16: 0, torch.float32: 1, torch.int64: 2}
+
+    def _pe_device(self, pe: int) -> int:
+        return self.team.devices[pe] if self.team.rank is None else self.team.devices[self.team.rank]
+
+    def multimem_ld_reduce(self, handle: SymmHandle, offset: int, dtype, count: int, pe: int,
+                           stream=None) -> torch.Tensor:
+        self._check_pe(pe)
+        tdt = _torch_dtype(dtype)
+        if tdt not in self._RED_CODES:
+            raise ValueError(f"multimem_ld_reduce supports bf16, fp32, int64; got {tdt}")
+        isz = torch.empty(0, dtype=tdt).element_size()
+        _check_range(handle, offset, count * isz)
+        dev = self._pe_device(pe)
+        out = torch.empty(int(count), dtype=tdt, device=f"cuda:{dev}")
+        with torch.cuda.device(dev):
+            _lib.call("tf_team_reduce", self.team.handle, int(pe), handle.offset + int(offset),
+                      self._RED_CODES[tdt], int(count), out.data_ptr(), _stream_ptr(stream))
+        return out
+
+    def multimem_st(self, handle: SymmHandle, offset: int, vec, pe: int, stream=None) -> None:
+        self._check_pe(pe)
+        dev = self._pe_device(pe)
+        v = vec if isinstance(vec, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(vec))
+        v = v.contiguous().to(f"cuda:{dev}")
+        nbytes = v.numel() * v.element_size()
+        _check_range(handle, offset, nbytes)
+        with torch.cuda.device(dev):
+            _lib.call("tf_team_broadcast", self.team.handle, int(pe), handle.offset + int(offset),
+                      v.data_ptr(), nbytes, _stream_ptr(stream))
+        if stream is None:
+            torch.cuda.synchronize(dev)  # v may be a temporary
+
+    def multimem_ld_reduce_block(self, handle: SymmHandle, pe: int, dtype, shape, row0: int, nrows: int,
+                                 col0: int, ncols: int, stream=None) -> torch.Tensor:
+        """Team sum of rows [row0, row0 + nrows) x cols [col0, col0 + ncols) of a
+        matrix laid out with `shape` in the region (shmem.py:363-375)."""
+        rows, cols = shape
+        if row0 < 0 or nrows < 0 or row0 + nrows > rows or col0 < 0 or ncols < 0 or col0 + ncols > cols:
+            raise ValueError(f"block [{row0}:{row0 + nrows}, {col0}:{col0 + ncols}] outside {tuple(shape)}")
+        isz = torch.empty(0, dtype=_torch_dtype(dtype)).element_size()
+        full = self.multimem_ld_reduce(handle, row0 * cols * isz, dtype, nrows * cols, pe, stream)
+        return full.view(nrows, cols)[:, col0:col0 + ncols].clone()
+
+    def multimem_st_block(self, handle: SymmHandle, pe: int, block, shape, row0: int, col0: int) -> None:
+        """Write a 2-D block into every PE's copy (shmem.py:377-385)."""
+        self._check_pe(pe)
+        b = block if isinstance(block, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(block))
+        r1, c1 = row0 + b.shape[0], col0 + b.shape[1]
+        if row0 < 0 or col0 < 0 or r1 > shape[0] or c1 > shape[1]:
+            raise ValueError(f"block [{row0}:{r1}, {col0}:{c1}] outside {tuple(shape)}")
+        for r in range(self.topology.world_size):
+            dst = self.view(handle, r, b.dtype, shape)
+            dst[row0:r1, col0:c1].copy_(b.to(dst.device))
+
     def barrier_all(self, rank: int | None = None, stream=None):
         """All-rank rendezvous ordered after every prior op on the rank's stream.
         With rank=None every local PE arrives and then waits (single-process team)."""

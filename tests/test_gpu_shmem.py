@@ -103,3 +103,57 @@ def test_range_and_scope_validation():
         h.st(sig, 0, 1, pe=0, scope="cta")
     with pytest.raises(ValueError):
         h.symm_at(buf, 4)
+
+
+# -- node-team collectives: multimem_ld_reduce / multimem_st (ovs/shmem.py:335-385) -------
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_multimem_reduce_and_broadcast(world):
+    import numpy as np
+    import torch
+    from paper_2605_02953_b200 import build_topology
+    from paper_2605_02953_b200.shmem import SymmetricHeap
+    heap = SymmetricHeap(build_topology(world, 1), data_bytes=1 << 22, signal_slots=64,
+                         devices=[0] * world)
+    rng = np.random.default_rng(world)
+    h = heap.alloc(4096 * 8)
+    # int64: exact ascending sum
+    vals = [rng.integers(-1000, 1000, 4096) for _ in range(world)]
+    for r in range(world):
+        heap.view(h, r, np.int64, (4096,)).copy_(torch.from_numpy(vals[r]))
+    got = heap.multimem_ld_reduce(h, 0, np.int64, 4096, pe=world - 1)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), np.sum(vals, axis=0))
+    # fp32: ascending-rank fp32 sum, bit-exact with the same order on the host
+    f = [rng.standard_normal(1000).astype(np.float32) for _ in range(world)]
+    for r in range(world):
+        heap.view(h, r, np.float32, (1000,)).copy_(torch.from_numpy(f[r]))
+    want = f[0].copy()
+    for r in range(1, world):
+        want = want + f[r]
+    got = heap.multimem_ld_reduce(h, 0, np.float32, 1000, pe=0)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), want)
+    # bf16 block reduce
+    shape = (16, 24)
+    bl = [torch.randn(shape).to(torch.bfloat16) for _ in range(world)]
+    for r in range(world):
+        heap.view(h, r, torch.bfloat16, shape).copy_(bl[r])
+    blk = heap.multimem_ld_reduce_block(h, 0, torch.bfloat16, shape, 2, 5, 3, 7)
+    acc = bl[0].float()
+    for r in range(1, world):
+        acc = acc + bl[r].float()
+    assert torch.equal(blk.cpu(), acc.to(torch.bfloat16)[2:7, 3:10])
+    # broadcast (vector and block) lands in every PE's copy
+    v = torch.arange(300, dtype=torch.float32)
+    heap.multimem_st(h, 64, v, pe=world - 1)
+    for r in range(world):
+        assert torch.equal(heap.view(h, r, torch.float32, (316,))[16:].cpu(), v)
+    b = torch.full((2, 3), 7, dtype=torch.int64)
+    heap.multimem_st_block(h, 0, b, (8, 8), 5, 4)
+    for r in range(world):
+        assert torch.equal(heap.view(h, r, torch.int64, (8, 8))[5:7, 4:7].cpu(), b)
+    with pytest.raises(ValueError):
+        heap.multimem_ld_reduce(h, 0, np.int8, 4, pe=0)
+    heap.team.close()
