@@ -124,6 +124,14 @@ int tf_team_reduce(tf_team* t, int pe, uint64_t offset, int dtype, int64_t count
                    void* stream);
 int tf_team_broadcast(tf_team* t, int from_pe, uint64_t offset, const void* src, size_t nbytes,
                       void* stream);
+/* atomic_cas (shmem.py:196-206): acq_rel compare-and-swap of a signal slot; the
+ * old value is returned in *old_out (synchronous: the stream is drained). */
+int tf_signal_cas(tf_team* t, int pe, uint64_t slot, uint64_t cmp, uint64_t value, uint64_t* old_out,
+                  void* stream);
+/* putmem_strided (shmem.py:253-268): rows of row_bytes from src (src_pitch apart)
+ * into PE to_pe's heap at dst_off, dst_pitch bytes apart (one 2-D copy). */
+int tf_putmem_strided(tf_team* t, int to_pe, uint64_t dst_off, size_t dst_pitch, const void* src,
+                      size_t src_pitch, size_t row_bytes, size_t rows, void* stream);
 /* st / notify / atomic_add on a signal slot of PE pe (shmem.py:174-194). */
 int tf_signal_op(tf_team* t, int pe, uint64_t slot, uint64_t value, int op_add, void* stream);
 /* wait (shmem.py:208-235): stream waits until all n slots >= value. */

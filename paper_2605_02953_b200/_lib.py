@@ -85,6 +85,8 @@ _SIGS = {
     "tf_putmem_signal": (ci, [vp, ci, u64, vp, sz, u64, u64, ci, vp]),
     "tf_signal_op": (ci, [vp, ci, u64, u64, ci, vp]),
     "tf_team_reduce": (ci, [vp, ci, u64, ci, i64, vp, vp]),
+    "tf_signal_cas": (ci, [vp, ci, u64, u64, u64, C.POINTER(u64), vp]),
+    "tf_putmem_strided": (ci, [vp, ci, u64, sz, vp, sz, sz, sz, vp]),
     "tf_team_broadcast": (ci, [vp, ci, u64, vp, sz, vp]),
     "tf_signal_wait": (ci, [vp, ci, u64, sz, u64, vp]),
     "tf_barrier_arrive": (ci, [vp, ci, vp]),

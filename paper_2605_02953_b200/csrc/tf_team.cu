@@ -177,6 +177,9 @@ struct ReducePtrs {
   const uint8_t* p[kMaxWorld];
 };
 // out[i] = sum over PEs (ascending) of PE q's element i; bf16 accumulates in fp32
+__global__ void signal_cas_kernel(uint64_t* slot, uint64_t cmp, uint64_t val, unsigned long long* old) {
+  *old = atom_cas_sys(slot, cmp, val);
+}
 template <int DT>
 __global__ void team_reduce_kernel(ReducePtrs src, int world, int64_t count, void* out) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
@@ -499,6 +502,36 @@ int tf_team_reduce(tf_team* t, int pe, uint64_t offset, int dtype, int64_t count
   else if (dtype == 1) tf::team_reduce_kernel<1><<<blocks, threads, 0, s>>>(src, t->world, count, out);
   else tf::team_reduce_kernel<2><<<blocks, threads, 0, s>>>(src, t->world, count, out);
   TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}
+
+int tf_signal_cas(tf_team* t, int pe, uint64_t slot, uint64_t cmp, uint64_t value, uint64_t* old_out,
+                  void* stream) {
+  if (!t || pe < 0 || pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
+  if (slot >= t->signal_slots) return fail(TF_ERR_INVALID, "slot out of range");
+  if (!old_out) return fail(TF_ERR_INVALID, "old_out is NULL");
+  const int me = t->ipc ? t->my_rank : pe;
+  tf::DeviceGuard guard(t->pes[me].device);
+  auto s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dold = nullptr;
+  TF_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dold), sizeof(unsigned long long), s));
+  tf::signal_cas_kernel<<<1, 1, 0, s>>>(t->pes[pe].sig + slot, cmp, value, dold);
+  TF_CUDA_TRY(cudaGetLastError());
+  TF_CUDA_TRY(cudaMemcpyAsync(old_out, dold, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  TF_CUDA_TRY(cudaFreeAsync(dold, s));
+  TF_CUDA_TRY(cudaStreamSynchronize(s));  // the old value is the caller's answer
+  return TF_OK;
+}
+
+int tf_putmem_strided(tf_team* t, int to_pe, uint64_t dst_off, size_t dst_pitch, const void* src,
+                      size_t src_pitch, size_t row_bytes, size_t rows, void* stream) {
+  if (!t || to_pe < 0 || to_pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
+  if (rows == 0 || row_bytes == 0) return TF_OK;
+  if (dst_pitch < row_bytes || src_pitch < row_bytes) return fail(TF_ERR_INVALID, "pitch < row bytes");
+  if (dst_off + (rows - 1) * dst_pitch + row_bytes > t->heap_bytes)
+    return fail(TF_ERR_INVALID, "range exceeds the heap");
+  TF_CUDA_TRY(cudaMemcpy2DAsync(t->pes[to_pe].base + dst_off, dst_pitch, src, src_pitch, row_bytes, rows,
+                                cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
   return TF_OK;
 }
 

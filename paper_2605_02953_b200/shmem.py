@@ -282,6 +282,17 @@ class SymmetricHeap:
         slot = self._slot(sig, idx, 1, pe)
         _lib.call("tf_signal_op", self.team.handle, int(pe), slot, int(val), 1, _stream_ptr(stream))
 
+    def atomic_cas(self, sig: SigHandle, idx: int, cmp: int, val: int, pe: int,
+                   semantic: str = "release", scope: str = "gpu", stream=None) -> int:
+        """Compare-and-swap of a signal slot (shmem.py:196-206); returns the old value.
+        Synchronous (the caller needs the answer), executed on the device at .sys scope."""
+        _check_scope_semantic(scope, semantic)
+        slot = self._slot(sig, idx, 1, pe)
+        old = C.c_uint64()
+        _lib.call("tf_signal_cas", self.team.handle, int(pe), slot, int(cmp) & (2 ** 64 - 1),
+                  int(val) & (2 ** 64 - 1), C.byref(old), _stream_ptr(stream))
+        return int(old.value)
+
     def wait(self, sig: SigHandle, idx: int, num_slots: int, pe: int, scope: str = "gpu",
              semantic: str = "acquire", value: int = 1, note=None, stream=None) -> None:
         """Stream waits until every slot in [idx, idx+num_slots) >= value."""
@@ -329,6 +340,27 @@ class SymmetricHeap:
 
     putmem_nbi = putmem
     getmem_nbi = getmem
+
+    def putmem_strided(self, dest: RemoteRegion, dest_off: int, src2d: torch.Tensor, dest_pitch: int, *,
+                       from_pe: int = 0, note: str = "putmem", stream=None):
+        """2-D block into rows `dest_pitch` bytes apart (shmem.py:253-268), one 2-D copy."""
+        if src2d.dim() != 2:
+            raise ValueError("putmem_strided needs a 2-D source block")
+        rows = src2d.shape[0]
+        row_nbytes = src2d.shape[1] * src2d.element_size()
+        if rows:
+            _check_range(dest.handle, dest_off, (rows - 1) * dest_pitch + row_nbytes)
+        if rows == 0 or row_nbytes == 0:
+            return
+        if dest_pitch < row_nbytes:
+            raise ValueError("dest_pitch smaller than a row")
+        src_pitch = src2d.stride(0) * src2d.element_size()
+        if src2d.stride(1) != 1:
+            src2d = src2d.contiguous()
+            src_pitch = row_nbytes
+        _lib.call("tf_putmem_strided", self.team.handle, int(dest.pe), dest.handle.offset + int(dest_off),
+                  int(dest_pitch), src2d.data_ptr(), int(src_pitch), int(row_nbytes), int(rows),
+                  _stream_ptr(stream))
 
     def fence(self, from_pe: int) -> None:
         """Ordering of puts from one stream is already issue-order (copy engine queue)."""
@@ -393,6 +425,15 @@ class SymmetricHeap:
         for r in range(self.topology.world_size):
             dst = self.view(handle, r, b.dtype, shape)
             dst[row0:r1, col0:c1].copy_(b.to(dst.device))
+
+    def sync_all(self, rank: int | None = None, stream=None):
+        """Rendezvous (shmem.py:324-327).  Puts are stream-ordered, so the device
+        barrier is the same as barrier_all's."""
+        return self.barrier_all(rank, stream)
+
+    def node_barrier(self, rank: int | None = None, barrier=None, stream=None):
+        """Rendezvous of the node team (shmem.py:329-331): every PE on one box."""
+        return self.barrier_all(rank, stream)
 
     def barrier_all(self, rank: int | None = None, stream=None):
         """All-rank rendezvous ordered after every prior op on the rank's stream.

@@ -157,3 +157,30 @@ def test_multimem_reduce_and_broadcast(world):
     with pytest.raises(ValueError):
         heap.multimem_ld_reduce(h, 0, np.int8, 4, pe=0)
     heap.team.close()
+
+
+def test_atomic_cas_and_putmem_strided():
+    import numpy as np
+    import torch
+    from paper_2605_02953_b200 import build_topology
+    from paper_2605_02953_b200.shmem import SymmetricHeap
+    world = 2
+    heap = SymmetricHeap(build_topology(world, 1), data_bytes=1 << 20, signal_slots=64,
+                         devices=[0] * world)
+    sig = heap.alloc_signals(4)
+    assert heap.atomic_cas(sig, 1, 0, 7, pe=1) == 0       # swaps
+    assert heap.atomic_cas(sig, 1, 0, 9, pe=1) == 7       # mismatch: unchanged
+    assert heap.atomic_cas(sig, 1, 7, 11, pe=1) == 7
+    assert int(heap.sig_view(sig, 1)[1]) == 11 and int(heap.sig_view(sig, 0)[1]) == 0
+    h = heap.alloc(64 * 64 * 4)
+    region = heap.view(h, 1, torch.float32, (64, 64))
+    region.zero_()
+    block = torch.arange(5 * 7, dtype=torch.float32, device="cuda").view(5, 7)
+    heap.putmem_strided(heap.symm_at(h, 1), 3 * 64 * 4 + 2 * 4, block, 64 * 4)
+    torch.cuda.synchronize()
+    assert torch.equal(region[3:8, 2:9], block)
+    assert float(region.sum()) == float(block.sum())
+    heap.sync_all(0)
+    heap.node_barrier(1)
+    torch.cuda.synchronize()
+    heap.team.close()
