@@ -8,12 +8,14 @@ device-side flags.  See DESIGN.md.
 from .context import WorkloadContext, WorkloadRun, reduce_visit_order
 from .errors import (AllocationError, BuildError, ConfigError, DeadlockError, ProtocolError,
                      VerificationError)
-from .topology import LINK_PROFILES, LinkConfig, Topology, build_topology, local_rank_of, node_of
+from .topology import (LINK_PROFILES, LinkConfig, Topology, build_topology, local_rank_of, node_of,
+                       topology_from_config)
 
 __all__ = [
     "WorkloadContext", "WorkloadRun", "reduce_visit_order", "AllocationError", "BuildError",
     "ConfigError", "DeadlockError", "ProtocolError", "VerificationError", "LINK_PROFILES",
-    "LinkConfig", "Topology", "build_topology", "local_rank_of", "node_of",
+    "LinkConfig", "Topology", "build_topology", "local_rank_of", "node_of", "topology_from_config",
+    "Token", "consume_token",
     "ag_gemm", "gemm_rs", "gemm", "gemm_allreduce", "AllGatherGemm", "GemmReduceScatter",
     "SymmetricHeap", "Team", "ag_moe_group_gemm", "ExpertParallelMoE", "moe_route", "ag_kv_scores",
 ]
@@ -30,7 +32,7 @@ def __getattr__(name):
     if name in ("ag_kv_scores",):
         from . import attention
         return getattr(attention, name)
-    if name in ("SymmetricHeap", "Team"):
+    if name in ("SymmetricHeap", "Team", "Token", "consume_token"):
         from . import shmem
         return getattr(shmem, name)
     raise AttributeError(name)

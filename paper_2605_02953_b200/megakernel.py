@@ -347,6 +347,12 @@ register_task_builder("add", lambda io, cfg: _plan_rows("add", io, cfg, False))
 register_task_builder("allreduce", lambda io, cfg: _plan_rows("allreduce", io, cfg, True))
 
 
+@dataclass(frozen=True)
+class DeviceProp:
+    """Persistent CTAs per rank the executor may use (runner.py:27-29)."""
+    num_sms: int
+
+
 @dataclass
 class MegaProgram:
     """Heap tensors (16-byte bump offsets) and layers (runner.py:45-60)."""

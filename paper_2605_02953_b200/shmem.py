@@ -43,6 +43,21 @@ class SigHandle:
     nslots: int
 
 
+@dataclass(frozen=True)
+class Token:
+    """Ordering witness returned by wait() (shmem.py:46-52).  On the device the wait
+    is stream-ordered, so the token only records what was waited for."""
+    pe: int
+    slot: int
+    num_slots: int
+    time: float = 0.0
+
+
+def consume_token(value, token: Token):
+    """Returns `value` unchanged (shmem.py:55-57)."""
+    return value
+
+
 class _CudaMem:
     """Minimal __cuda_array_interface__ exporter for zero-copy torch views."""
 
@@ -294,7 +309,7 @@ class SymmetricHeap:
         return int(old.value)
 
     def wait(self, sig: SigHandle, idx: int, num_slots: int, pe: int, scope: str = "gpu",
-             semantic: str = "acquire", value: int = 1, note=None, stream=None) -> None:
+             semantic: str = "acquire", value: int = 1, note=None, stream=None) -> Token:
         """Stream waits until every slot in [idx, idx+num_slots) >= value."""
         _check_scope_semantic(scope, semantic)
         if num_slots < 1:
@@ -302,6 +317,7 @@ class SymmetricHeap:
         slot = self._slot(sig, idx, num_slots, pe)
         _lib.call("tf_signal_wait", self.team.handle, int(pe), slot, int(num_slots), int(value),
                   _stream_ptr(stream))
+        return Token(pe=int(pe), slot=slot, num_slots=int(num_slots))
 
     def reset_signals(self, sig: SigHandle, pe: int, stream=None) -> None:
         slot = self._slot(sig, 0, sig.nslots, pe)

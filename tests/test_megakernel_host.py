@@ -126,3 +126,25 @@ def test_dependency_structure():
         prog = MK.MegaProgram(build_topology(1, 1))
         x = prog.tensor("x", (4, 4), np.int64)
         prog.layer("softmax", [x], [x])
+
+
+def test_api_surface_extras(tmp_path):
+    """topology_from_config (topology.py:110-141), Token / consume_token (shmem.py:46-57),
+    DeviceProp (runner.py:27-29)."""
+    from paper_2605_02953_b200 import topology_from_config
+    from paper_2605_02953_b200.errors import ConfigError
+    t = topology_from_config({"world_size": 8, "profile": "b200", "num_sms": 148})
+    assert t.world_size == 8 and t.num_sms == 148 and t.intra_node_bw == 900e9
+    f = tmp_path / "topo.cfg"
+    f.write_text("# comment\n[topology]\nworld_size = 4\nnnodes = 2\nintra_node_bw = 1e11\n")
+    t2 = topology_from_config(str(f))
+    assert (t2.world_size, t2.nnodes, t2.intra_node_bw) == (4, 2, 1e11)
+    with pytest.raises(ConfigError):
+        topology_from_config({"nnodes": 1})
+    with pytest.raises(ConfigError):
+        topology_from_config({"world_size": 2, "profile": "nope"})
+    assert MK.DeviceProp(num_sms=8).num_sms == 8
+    import importlib
+    sh = importlib.import_module("paper_2605_02953_b200.shmem")
+    tok = sh.Token(pe=0, slot=3, num_slots=2)
+    assert sh.consume_token(41, tok) == 41
