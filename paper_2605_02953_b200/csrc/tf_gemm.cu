@@ -34,6 +34,9 @@ namespace tf {
 namespace {
 
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
+#ifndef TF_GEMM_LAG
+#define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
+#endif
 constexpr int UMMA_K = 16;
 constexpr int kThreads = 192;          // 6 warps
 constexpr int kEpiWarp0 = 2;
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // second half's MMAs lag by L k-blocks: the epilogue drains half 0 while
       // half 1 finishes, and the next tile's half 0 starts while half 1 drains.
       constexpr uint32_t idesc = umma_idesc_bf16(128 * CG, BN);
-      constexpr int L = 2;
+      constexpr int L = TF_GEMM_LAG;
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
