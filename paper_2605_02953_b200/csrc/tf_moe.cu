@@ -26,6 +26,8 @@
 //                      order, bf16 out
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "tf_internal.h"
@@ -187,6 +189,78 @@ __global__ void __launch_bounds__(kChunk) rank_kernel(const int32_t* __restrict_
     for (int w2 = 0; w2 < warp; ++w2) before += wc[w2 * E + e];
     sorted_pos[g] = expert_base[e] + chunk_off[static_cast<int64_t>(blockIdx.x) * E + e] + before +
                     in_warp;
+  }
+}
+
+
+// Single-pass stable counting (hist + scan + rank in one launch): every chunk CTA
+// (1024 entries) builds its per-warp and chunk histograms, publishes the chunk
+// histogram with a release flag, waits until every chunk has published (all chunk
+// CTAs are co-resident), then derives the totals, the expert bases and its own
+// chunk offsets and writes the stable send positions.  Same arithmetic as the
+// three-kernel path, so positions are identical.
+__global__ void __launch_bounds__(kChunk) count_fused_kernel(
+    const int32_t* __restrict__ idx, int64_t entries, int E, int nchunks, int32_t* chunk_hist,
+    unsigned long long* flags, unsigned long long epoch, unsigned long long timeout_ns,
+    unsigned long long* err, int32_t* __restrict__ counts, int32_t* __restrict__ expert_base,
+    int32_t* __restrict__ sorted_pos) {
+  extern __shared__ int32_t fsm[];
+  int32_t* wc = fsm;              // [32 warps][E]
+  int32_t* tot = fsm + 32 * E;    // [E]
+  int32_t* off = tot + E;         // [E]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wc[i] = 0;
+  __syncthreads();
+  const int64_t g = static_cast<int64_t>(c) * kChunk + threadIdx.x;
+  const int e = g < entries ? idx[g] : -1;
+  const unsigned same = __match_any_sync(0xffffffffu, e);
+  const int in_warp = __popc(same & ((1u << lane) - 1));
+  if (e >= 0 && in_warp == 0) wc[warp * E + e] = __popc(same);
+  __syncthreads();
+  for (int x = threadIdx.x; x < E; x += blockDim.x) {
+    int32_t sum = 0;
+    for (int w = 0; w < 32; ++w) sum += wc[w * E + x];
+    chunk_hist[static_cast<int64_t>(c) * E + x] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + c), "l"(epoch) : "memory");
+  }
+  for (int x = threadIdx.x; x < nchunks; x += blockDim.x) {
+    uint64_t v;
+    const uint64_t t0 = globaltimer_ns();
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + x) : "memory");
+      if (v >= epoch) break;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        if (err) atomicCAS(err, 0ull, 0x5200000ull | static_cast<unsigned>(x));
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < E; x += blockDim.x) {
+    int32_t t = 0, o = 0;
+    for (int cc = 0; cc < nchunks; ++cc) {
+      const int32_t v = __ldcg(chunk_hist + static_cast<int64_t>(cc) * E + x);
+      if (cc < c) o += v;
+      t += v;
+    }
+    tot[x] = t;
+    off[x] = o;
+  }
+  __syncthreads();
+  if (c == 0)
+    for (int x = threadIdx.x; x < E; x += blockDim.x) counts[x] = tot[x];
+  block_exclusive_scan(tot, E);  // expert bases (ends with __syncthreads)
+  if (c == 0)
+    for (int x = threadIdx.x; x < E; x += blockDim.x) expert_base[x] = tot[x];
+  if (e >= 0) {
+    int before = 0;
+    for (int w2 = 0; w2 < warp; ++w2) before += wc[w2 * E + e];
+    sorted_pos[g] = tot[e] + off[e] + before + in_warp;
   }
 }
 
@@ -391,6 +465,38 @@ int run_count(const int32_t* idx, int64_t entries, int E, int32_t* counts, int32
   int32_t* chunk = static_cast<int32_t*>(scratch);
   if (!ebase) ebase = chunk + static_cast<int64_t>(nchunks) * E;
   if (static_cast<size_t>(32) * E * 4 > 227 * 1024) return fail(TF_ERR_CONFIG, "too many experts");
+  {
+    // single-pass path when every chunk CTA can be co-resident
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t fsm = static_cast<size_t>(34) * E * 4;
+    static std::map<int, unsigned long long*> flag_bufs;
+    static std::map<int, unsigned long long> epochs;
+    static std::mutex mu;
+    if (entries > 0 && nchunks <= num_sms_of_current_device() && fsm <= 200 * 1024) {
+      unsigned long long* flags = nullptr;
+      unsigned long long ep = 0;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = flag_bufs.find(dev);
+        if (it == flag_bufs.end()) {
+          TF_CUDA_TRY(cudaMalloc(&flags, 1024 * sizeof(unsigned long long)));
+          TF_CUDA_TRY(cudaMemset(flags, 0, 1024 * sizeof(unsigned long long)));
+          flag_bufs[dev] = flags;
+          TF_CUDA_TRY(cudaFuncSetAttribute(count_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           200 * 1024));
+        } else {
+          flags = it->second;
+        }
+        ep = ++epochs[dev];
+      }
+      count_fused_kernel<<<nchunks, kChunk, fsm, s>>>(idx, entries, E, nchunks, chunk, flags, ep,
+                                                      20ull * 1000 * 1000 * 1000, nullptr, counts, ebase,
+                                                      sorted_pos);
+      TF_CUDA_TRY(cudaGetLastError());
+      return TF_OK;
+    }
+  }
   hist_kernel<<<nchunks, 256, E * 4, s>>>(idx, entries, E, chunk);
   scan_kernel<<<1, 1024, E * 4, s>>>(chunk, nchunks, E, counts, ebase);  // E <= 1024*4 ints
   if (entries > 0) {
