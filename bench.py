@@ -473,6 +473,105 @@ def bench_layer(dev, steps, warmup, peaks, flush, tp_emulated=1):
             "max_rel_err_vs_unfused": round(rel, 5), "tp8_emulated": tp8}
 
 
+def bench_layer_dist(dev, world, rank, steps, warmup, flush, peaks, shared_gpus, tokens=LAY_T):
+    """Config 5 at TP = world, one process per GPU: every rank launches its own
+    persistent megakernel over an IPC team (two-shot allreduce tasks over NVLink P2P).
+    Comparator: the same rank's shard unfused -- cuBLAS GEMMs, SDPA, torch elementwise
+    and two NCCL all_reduce calls.  Fused and unfused steps alternate; times are
+    max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    from paper_2605_02953_b200 import build_topology
+    from paper_2605_02953_b200 import layer as L
+    from paper_2605_02953_b200.shmem import Team
+    T, H, HQ, HKV, FF = tokens, LAY_H, LAY_HQ, LAY_HKV, LAY_F
+    hq, hkv, f = HQ // world, HKV // world, FF // world
+    prog = L.llama_layer_program(build_topology(world, 1), T, H, HQ, HKV, FF, seq_len=T)
+    built = prog.build()
+    nslots = (built.max_task_id + 1) * built.max_tiles_per_op
+    team = Team.from_process_group(heap_bytes=prog._top + 4096, signal_slots=nslots + 64)
+    runner = L.LayerRunner(prog, built, team=team)
+    gs = torch.Generator(device="cpu").manual_seed(77)              # shared across ranks
+    gr = torch.Generator(device="cpu").manual_seed(1000 + rank)     # this rank's shard
+    mk = lambda gen, *sh, sc=1.0: (torch.randn(*sh, generator=gen) * sc).to(torch.bfloat16).to(f"cuda:{dev}")
+    x = mk(gs, T, H)
+    g1 = (1 + 0.1 * torch.randn(1, H, generator=gs)).to(torch.bfloat16).to(f"cuda:{dev}")
+    g2 = (1 + 0.1 * torch.randn(1, H, generator=gs)).to(torch.bfloat16).to(f"cuda:{dev}")
+    rope = torch.from_numpy(L.rope_table(T)).to(f"cuda:{dev}")
+    w = {"w_qkv": mk(gr, (hq + 2 * hkv) * 128, H, sc=H ** -0.5), "w_o": mk(gr, H, hq * 128, sc=(HQ * 128) ** -0.5),
+         "w_gate_up": mk(gr, 2 * f, H, sc=H ** -0.5), "w_down": mk(gr, H, f, sc=FF ** -0.5)}
+    for name, val in [("x", x), ("g_attn", g1), ("g_mlp", g2), ("rope", rope), *w.items()]:
+        runner.view(name).copy_(val)
+    stream = torch.cuda.current_stream(dev)
+    wgu = w["w_gate_up"].view(f // 128, 2, 128, H)
+    wg, wu = wgu[:, 0].reshape(f, H).contiguous(), wgu[:, 1].reshape(f, H).contiguous()
+    cos, sin = rope[:, :64], rope[:, 64:]
+
+    def rms(t, gg):
+        tf = t.float()
+        return (tf * torch.rsqrt(tf.pow(2).mean(-1, keepdim=True) + 1e-5) * gg.float()).to(torch.bfloat16)
+
+    def rot(t):
+        tf = t.float()
+        a1, a2 = tf[..., :64], tf[..., 64:]
+        c, s_ = cos[:, None, :], sin[:, None, :]
+        return torch.cat([a1 * c - a2 * s_, a2 * c + a1 * s_], -1).to(torch.bfloat16)
+
+    def unfused():
+        qkv = rms(x, g1) @ w["w_qkv"].t()
+        q = rot(qkv[:, :hq * 128].view(T, hq, 128))
+        k = rot(qkv[:, hq * 128:(hq + hkv) * 128].view(T, hkv, 128))
+        v = qkv[:, (hq + hkv) * 128:].view(T, hkv, 128)
+        att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                             v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
+        o = att[0].transpose(0, 1).reshape(T, hq * 128) @ w["w_o"].t()
+        dist.all_reduce(o)
+        h = o + x
+        hn = rms(h, g2)
+        d = (F.silu(hn @ wg.t()) * (hn @ wu.t())) @ w["w_down"].t()
+        dist.all_reduce(d)
+        return d + h
+
+    do_cmp = not shared_gpus  # NCCL needs one GPU per rank
+    for _ in range(warmup):
+        runner.run(stream)
+        if do_cmp:
+            unfused()
+    torch.cuda.synchronize(dev)
+    runner.check()
+    dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    cevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for (e0, e1), (c0, c1) in zip(evs, cevs):
+        flush.zero_()
+        e0.record(stream)
+        runner.run(stream)
+        e1.record(stream)
+        if do_cmp:
+            flush.zero_()
+            c0.record(stream)
+            unfused()
+            c1.record(stream)
+    torch.cuda.synchronize(dev)
+    runner.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    cms = sum(a.elapsed_time(b) for a, b in cevs) / steps if do_cmp else 0.0
+    ms, cms = max_over_ranks([ms, cms], dev, True)
+    flops = world * layer_flops(T, H, HQ, HKV, FF, world)
+    out = {"workload": f"config 5 at TP={world}: Llama-3-70B layer, {T} tokens (one causal sequence), "
+                       "one persistent megakernel per rank, two-shot allreduce tasks over NVLink P2P",
+           "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2), "flops": flops,
+           "tasks_per_rank": len(built.tasks)}
+    if do_cmp:
+        out["comparator"] = {"impl": "unfused per rank: cuBLAS GEMMs + SDPA + torch elementwise + "
+                                     "2 x NCCL all_reduce", "ms": round(cms, 4), "speedup": round(cms / ms, 4)}
+    dist.barrier()
+    runner.close()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main_ours(args):
     import torch
@@ -744,6 +843,12 @@ def main_ours(args):
     layer = None
     if not args.no_layer and world == 1:
         layer = bench_layer(dev, max(3, args.steps // 4), 2, peaks, flush)
+    elif not args.no_layer:
+        try:  # a failure here must not cost the config-2 / MoE line of the scaling run
+            layer = bench_layer_dist(dev, world, rank, max(3, args.steps // 4), 2, flush, peaks, shared_gpus,
+                                     tokens=int(os.environ.get("TF_BENCH_LAYER_TOKENS", LAY_T)))
+        except Exception as exc:  # noqa: BLE001
+            layer = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
     if rank == 0:
