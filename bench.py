@@ -572,6 +572,77 @@ def bench_layer_dist(dev, world, rank, steps, warmup, flush, peaks, shared_gpus,
     return out
 
 
+def bench_attention_dist(dev, world, rank, steps, flush, peaks, shared_gpus):
+    """Config 3 at SP = world, one process per GPU: the fused AG-KV flash attention
+    (K/V chunks pulled from the peers while the tensor cores start on the local
+    chunk) against NCCL all_gather of K and V + SDPA on the same shard."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    from paper_2605_02953_b200.attention import AllGatherKVAttention
+    from paper_2605_02953_b200.shmem import Team
+    S, HQ, HKV, D = ATT_S, ATT_HQ, ATT_HKV, ATT_D
+    sl = S // world
+    team = Team.from_process_group(heap_bytes=4 * S * HKV * D * 2 + (16 << 20), signal_slots=256)
+    g = torch.Generator(device="cpu").manual_seed(500 + rank)
+    mk = lambda *sh: torch.randn(*sh, generator=g).to(torch.bfloat16).to(f"cuda:{dev}")
+    q, k, v = mk(sl, HQ, D), mk(sl, HKV, D), mk(sl, HKV, D)
+    out = torch.empty_like(q)
+    op = AllGatherKVAttention(team, sl, HQ, HKV, D)
+    kall = torch.empty(S, HKV, D, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    vall = torch.empty_like(kall)
+    stream = torch.cuda.current_stream(dev)
+
+    def unfused():
+        dist.all_gather_into_tensor(kall, k)
+        dist.all_gather_into_tensor(vall, v)
+        return F.scaled_dot_product_attention(q.transpose(0, 1)[None], kall.transpose(0, 1)[None],
+                                              vall.transpose(0, 1)[None], enable_gqa=True)
+
+    do_cmp = not shared_gpus
+    for _ in range(2):
+        op(q, k, v, out)
+        if do_cmp:
+            unfused()
+    torch.cuda.synchronize(dev)
+    team.check()
+    dist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    cevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for (e0, e1), (c0, c1) in zip(evs, cevs):
+        flush.zero_()
+        e0.record(stream)
+        op(q, k, v, out)
+        e1.record(stream)
+        if do_cmp:
+            flush.zero_()
+            c0.record(stream)
+            unfused()
+            c1.record(stream)
+    torch.cuda.synchronize(dev)
+    team.check()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    cms = sum(a.elapsed_time(b) for a, b in cevs) / steps if do_cmp else 0.0
+    ms, cms = max_over_ranks([ms, cms], dev, True)
+    flops = 4.0 * sl * S * D * HQ
+    nv = (world - 1) / world * S * HKV * D * 2 * 2  # K and V bytes pulled per rank
+    res = {"workload": f"config 3 at SP={world}: fused AG-KV flash attention, Q[{sl},64,128] per rank vs "
+                       f"K/V[{S},8,128] gathered over NVLink (non-causal, GQA 8:1, bf16)",
+           "ms_per_rank": round(ms, 4), "tflops_per_rank": round(flops / (ms * 1e-3) / 1e12, 2),
+           "tflops_total": round(world * flops / (ms * 1e-3) / 1e12, 2),
+           "roofline": {"bound": "tensor", "t_roof_ms": round(max(flops / (peaks.get("bf16_tflops", 1622.7) * 1e12),
+                                                                   nv / 770e9) * 1e3, 4),
+                        "frac": round(max(flops / (peaks.get("bf16_tflops", 1622.7) * 1e12), nv / 770e9)
+                                      / (ms * 1e-3), 4)}}
+    if do_cmp:
+        res["comparator"] = {"impl": "NCCL all_gather(K), all_gather(V) + torch SDPA", "ms": round(cms, 4),
+                             "speedup": round(cms / ms, 4)}
+    dist.barrier()
+    team.close()
+    return res
+
+
 # ------------------------------------------------------------------ GPU arm
 def main_ours(args):
     import torch
@@ -839,6 +910,11 @@ def main_ours(args):
     attn = None
     if not args.no_attn and world == 1:
         attn = bench_attention(dev, 3, peaks)
+    elif not args.no_attn and not shared_gpus:
+        try:  # failure-isolated, like the layer section
+            attn = bench_attention_dist(dev, world, rank, 3, flush, peaks, shared_gpus)
+        except Exception as exc:  # noqa: BLE001
+            attn = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     layer = None
     if not args.no_layer and world == 1:
