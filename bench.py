@@ -926,7 +926,10 @@ def main_ours(args):
         except Exception as exc:  # noqa: BLE001
             layer = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
-    launches_per_step = 2 if world == 1 else (3 + 4)  # N>1: AG barrier x2 + GEMM; RS barrier x2 + GEMM + reduce
+    # our kernels per timed step: N=1 -> AG GEMM + its split-K tail fix-up (1792 pair tiles leave a
+    # partial last wave) + RS GEMM (profiles/r01_launches_v2.txt); N>1 adds the barrier
+    # arrive/wait kernels of both ops and the RS owner-reduce kernel
+    launches_per_step = 3 if world == 1 else (3 + 2 + 2 + 1)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
