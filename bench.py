@@ -840,7 +840,7 @@ def main_ours(args):
         y_dev = [torch.empty_like(y) for _ in range(nb)]
         h2d_s = torch.cuda.Stream(device=dev)
         d2h_s = torch.cuda.Stream(device=dev)
-        n_e2e = args.steps + 2
+        n_e2e = 3 * args.steps + 2  # a pipelined serving loop: fill/drain amortised over the steps
 
         def run_e2e(n):
             ev_h2d = [torch.cuda.Event() for _ in range(n)]
