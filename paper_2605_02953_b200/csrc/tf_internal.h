@@ -59,6 +59,7 @@ struct GemmLaunch {
 };
 
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);
+void layer_release_team(const tf_team* t);
 int num_sms_of_current_device();
 
 }  // namespace tf

@@ -1012,6 +1012,19 @@ std::mutex g_map_mu;
 std::map<std::pair<const tf_team*, int>, MapCache> g_maps;
 
 }  // namespace
+
+// drop the tensor-map tables cached for a team (called by tf_team_destroy)
+void layer_release_team(const tf_team* t) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  for (auto it = g_maps.begin(); it != g_maps.end();) {
+    if (it->first.first == t) {
+      if (it->second.dev) cudaFree(it->second.dev);
+      it = g_maps.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
 }  // namespace tf
 
 using tf::fail;
