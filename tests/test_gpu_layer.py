@@ -118,3 +118,15 @@ def test_layer_ragged_tiles(tokens, seq, hidden, ffn):
         assert compare(run.outputs[name][0], inter[name]) <= TOL, name
     for r in range(2):
         assert compare(run.outputs["out"][r], want) <= TOL
+
+
+@pytest.mark.parametrize("heads_q,heads_kv", [(4, 4), (6, 2)])
+def test_layer_one_head_per_attention_task(heads_q, heads_kv):
+    """Odd GQA groups (MHA, group of 3) run one head per attention task."""
+    prog, inputs, want, inter = make_case(1, tokens=256, hidden=512, heads_q=heads_q, heads_kv=heads_kv,
+                                          ffn=1024, seq=128, seed=heads_q * 10 + heads_kv)
+    built = prog.build()
+    assert built.layer_configs[2]["heads_per_task"] == 1
+    run = MK.run_megakernel(prog, built, 24, inputs=inputs)
+    assert compare(run.outputs["attn"][0], inter["attn"]) <= TOL
+    assert compare(run.outputs["out"][0], want) <= TOL
