@@ -34,9 +34,10 @@ def test_llama_graph_dependencies():
         rows = {int(lo) // 3 for p, lo, hi in built.dep_table[t.dep_start:t.dep_end] if p == 1}
         seq0 = (i // 2) * 2
         assert rows == set(range(seq0 // 2, i // 2 + 1)), (i, rows)
-    # emitted longest-first
+    # emitted shortest-first by default (position in sequence ascending)
     firsts = [t.tile_id // per_row for t in by[2]]
-    assert firsts[0] % 2 == 1 and firsts[-1] % 2 == 0
+    assert built.layer_configs[2]["order"] == "shortest_first"
+    assert firsts[0] % 2 == 0 and firsts[-1] % 2 == 1
     # o-proj tile (tm, tn) waits on every head pair of the two query tiles of its 256 rows
     for t in by[3]:
         rows = [tuple(r) for r in built.dep_table[t.dep_start:t.dep_end]]
