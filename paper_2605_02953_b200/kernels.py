@@ -346,6 +346,11 @@ class AllGatherGemm:
         self.team, self.m, self.k, self.n = team, m, k, n_local
         self.out_dtype = out_dtype
         self.block_m, self.block_n = block_m, block_n
+        # a raster group must not span more than one gathered chunk: with the gather
+        # swizzle the first group is then this rank's own rows, so the first wave of
+        # tiles needs no remote data (TP8 at 512-row tiles: 2 row tiles per chunk)
+        if team.world > 1 and swizzle:
+            group_m = max(1, min(group_m, (m // team.world) // block_m))
         self.group_m, self.num_gemm_sms = group_m, num_gemm_sms
         self.maps = {r: (tile_map_tensor(m, r, team.world, nnodes, "ag_gemm",
                                          f"cuda:{team.devices[r]}", block_m) if swizzle else None)
