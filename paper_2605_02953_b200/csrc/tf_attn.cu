@@ -11,17 +11,20 @@
 //
 // Per CTA (320 threads, two 128-query tiles A and B of one head):
 //   warp 0      TMA: Q_A and Q_B once, then K_j and V_j (128 keys x 128 dims each)
-//               through a 3-slot ring (K0 V0 K1 V1 ...).
-//   warp 1      MMA (one lane): S_t = Q_t K_j^T (M=128, N=128, K=d) for t = A, B,
-//               then O_t += P_t V_j (A = P_t from smem, K-major; B = V from smem,
-//               MN-major).
+//               through a 5-slot ring (K0 V0 K1 V1 ...).
+//   warp 1      MMA (one lane), per tile t: S_t(0) = Q_t K_0^T, then for every key
+//               tile j: O_t += P_t(j) V_j (A = P_t from TMEM, B = V from smem,
+//               MN-major) followed by S_t(j+1) into the same TMEM columns -- the
+//               in-order tensor pipe reads P_t(j) before S_t(j+1) overwrites it.
 //   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B, one query row per
 //               thread: S row from TMEM, online max/sum in fp32 (ex2.approx with
 //               the scale folded into an FFMA), lazy rescale -- the running max
 //               may lag the true max by up to 2^8 before O is rescaled in TMEM --
-//               P row to smem as bf16 (128-byte swizzled K-major), O / l as bf16.
+//               P packed to bf16 over the first 64 columns of S_t, O / l as bf16.
 // While one warpgroup is on the ALUs/SFU the tensor pipe works on the other
-// tile's QK^T and PV.  TMEM: S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
+// tile's QK^T and PV.  TMEM: S/P_A [0,128), S/P_B [128,256), O_A [256,384),
+// O_B [384,512).  An opt-in CTA-pair variant (TF_ATTN_PAIR=1) splits K and V
+// across two CTAs with cta_group::2 MMAs.
 #include <cuda.h>
 #include <cuda_runtime.h>
 

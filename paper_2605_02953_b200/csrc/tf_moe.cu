@@ -13,14 +13,17 @@
 //
 // Kernels
 //   topk_kernel        warp per token: k rounds of warp argmax (ties -> lower id)
-//   hist / scan / rank deterministic stable send order: chunk histograms in smem,
-//                      per-expert exclusive scan over chunks, in-chunk ranks via
-//                      __match_any_sync + per-warp prefix -- no atomic decides a
-//                      position, so counts, offsets and layout are bit-exact
+//   count_fused_kernel deterministic stable send order in one launch: chunk CTAs
+//                      build per-warp histograms (__match_any_sync), publish the
+//                      chunk histogram with a release flag, wait for all chunks,
+//                      then derive totals, expert bases, chunk offsets and ranks --
+//                      no atomic decides a position, so counts, offsets and layout
+//                      are bit-exact (hist / scan / rank kernels when there are
+//                      more chunks than SMs)
 //   layout_kernel      per-expert destination segment base on the owner
-//   scatter_kernel     warp per (token, slot): 16-byte vector copy of the token
-//                      row straight into the owner's receive buffer (NVLink P2P
-//                      stores for remote owners)
+//   scatter_kernel     warp per (token, <= 8 KB row piece): TMA bulk copy into smem,
+//                      bulk stores to the destination rows this rank owns, 16-byte
+//                      P2P stores over NVLink to the rows peers own
 //   combine_kernel     warp per token: pulls the k expert rows (16-byte loads,
 //                      k loads in flight per lane), fp32 weighted sum in slot
 //                      order, bf16 out
