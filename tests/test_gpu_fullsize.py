@@ -8,6 +8,9 @@ Config 4 (DeepSeek-V3-like EP=8, 4096 tok/rank, top-8 of 256, hidden 7168):
   * every routed (token, slot) is delivered exactly once: counts, receive rows
     and an fp64 checksum of all received rows are conserved;
   * combine with identity experts returns each token (weights sum to 1).
+Config 5 (Llama-3-70B layer, 8192 tokens, one causal sequence):
+  * the TP=1 megakernel matches an unfused torch computation of the same bf16
+    layer, the TP=2 graph matches TP=1, and both TP ranks hold identical outputs.
 Several ranks are emulated on one GPU.  Tolerances: bf16 outputs use the
 north-star rel 2e-2 (max-norm); checksums are compared in fp64 at 1e-2.
 """
@@ -117,3 +120,91 @@ def test_config4_moe_ep8_conservation():
     team.check()
     for r in range(world):
         assert _rel(outs[r].float(), xs[r].float()) <= 2e-2
+
+
+# -- config 5: the Llama-3-70B layer at full size -----------------------------------------
+
+
+def _layer_weights(g, T, H, HQ, HKV, FF, dev):
+    mk = lambda *s, sc=1.0: (torch.randn(*s, generator=g) * sc).to(torch.bfloat16).to(dev)
+    wq = mk(HQ * 128, H, sc=H ** -0.5)
+    wk, wv = mk(HKV * 128, H, sc=H ** -0.5), mk(HKV * 128, H, sc=H ** -0.5)
+    wo = mk(H, HQ * 128, sc=(HQ * 128) ** -0.5)
+    wg, wu = mk(FF, H, sc=H ** -0.5), mk(FF, H, sc=H ** -0.5)
+    w2 = mk(H, FF, sc=FF ** -0.5)
+    return wq, wk, wv, wo, wg, wu, w2
+
+
+def _shard_into(runner, pe, tp, r, x, g1, g2, rope, W, HQ, HKV, FF):
+    """Write rank r's TP shard of the full weights into PE pe of a layer runner."""
+    from paper_2605_02953_b200 import layer as L
+    wq, wk, wv, wo, wg, wu, w2 = W
+    hq, hkv, f = HQ // tp, HKV // tp, FF // tp
+    qkv = torch.cat([wq[r * hq * 128:(r + 1) * hq * 128], wk[r * hkv * 128:(r + 1) * hkv * 128],
+                     wv[r * hkv * 128:(r + 1) * hkv * 128]])
+    gu = torch.from_numpy(L.interleave_gate_up(wg[r * f:(r + 1) * f].float().cpu().numpy(),
+                                               wu[r * f:(r + 1) * f].float().cpu().numpy()))
+    vals = {"x": x, "g_attn": g1, "g_mlp": g2, "rope": rope, "w_qkv": qkv,
+            "w_o": wo[:, r * hq * 128:(r + 1) * hq * 128], "w_gate_up": gu,
+            "w_down": w2[:, r * f:(r + 1) * f]}
+    for name, val in vals.items():
+        v = runner.view(name, pe)
+        v.copy_(val.to(v.dtype).to(v.device))
+
+
+def test_config5_layer_full_size_tp1_tp2_and_unfused():
+    """Full-size layer (8192 tokens, hidden 8192, 64/8 heads, ffn 28672): the TP=1
+    megakernel, the TP=2 graph (two ranks on this GPU, two-shot allreduce) and an
+    unfused torch computation of the same bf16 layer agree within rel 2e-2."""
+    import torch.nn.functional as F
+
+    from paper_2605_02953_b200 import build_topology
+    from paper_2605_02953_b200 import layer as L
+    T, H, HQ, HKV, FF = TOKENS, HIDDEN, 64, 8, FFN
+    dev = "cuda:0"
+    g = torch.Generator().manual_seed(2024)
+    x = torch.randn(T, H, generator=g).to(torch.bfloat16).to(dev)
+    g1 = (1 + 0.1 * torch.randn(1, H, generator=g)).to(torch.bfloat16).to(dev)
+    g2 = (1 + 0.1 * torch.randn(1, H, generator=g)).to(torch.bfloat16).to(dev)
+    rope = torch.from_numpy(L.rope_table(T)).to(dev)
+    W = _layer_weights(g, T, H, HQ, HKV, FF, dev)
+    outs = {}
+    for tp in (1, 2):
+        prog = L.llama_layer_program(build_topology(tp, 1), T, H, HQ, HKV, FF, seq_len=T)
+        r = L.LayerRunner(prog, device=0)
+        for pe in range(tp):
+            _shard_into(r, pe, tp, pe, x, g1, g2, rope, W, HQ, HKV, FF)
+        r.run()
+        torch.cuda.synchronize()
+        r.check()
+        outs[tp] = [r.view("out", pe).clone() for pe in range(tp)]
+        r.close()
+        del r
+        torch.cuda.empty_cache()
+    # unfused reference of the same bf16 layer (torch, fp32 softmax inside SDPA)
+    wq, wk, wv, wo, wg, wu, w2 = W
+    cos, sin = rope[:, :64], rope[:, 64:]
+
+    def rms(t, gg):
+        tf = t.float()
+        return (tf * torch.rsqrt(tf.pow(2).mean(-1, keepdim=True) + 1e-5) * gg.float()).to(torch.bfloat16)
+
+    def rot(t):
+        tf = t.float()
+        a1, a2 = tf[..., :64], tf[..., 64:]
+        return torch.cat([a1 * cos[:, None] - a2 * sin[:, None], a2 * cos[:, None] + a1 * sin[:, None]],
+                         -1).to(torch.bfloat16)
+
+    xn = rms(x, g1)
+    q = rot((xn @ wq.t()).view(T, HQ, 128))
+    k = rot((xn @ wk.t()).view(T, HKV, 128))
+    v = (xn @ wv.t()).view(T, HKV, 128)
+    att = F.scaled_dot_product_attention(q.transpose(0, 1)[None], k.transpose(0, 1)[None],
+                                         v.transpose(0, 1)[None], is_causal=True, enable_gqa=True)
+    h = (att[0].transpose(0, 1).reshape(T, HQ * 128) @ wo.t()).float() + x.float()
+    hb = h.to(torch.bfloat16)
+    hn = rms(hb, g2)
+    want = ((F.silu((hn @ wg.t()).float()) * (hn @ wu.t()).float()).to(torch.bfloat16) @ w2.t()).float() + hb.float()
+    assert _rel(outs[1][0].float(), want) <= 2e-2
+    assert _rel(outs[2][0].float(), outs[1][0].float()) <= 2e-2
+    assert torch.equal(outs[2][0], outs[2][1])  # both ranks hold the same allreduced output
