@@ -566,6 +566,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                acc * S::kAccCols + h * BN;
+        if constexpr (EPI == 1 && !OUT_F32) {
+          // Scatter to the owners through a per-warp smem transpose: each 64-column chunk
+          // of the warp's 32 rows is staged (128-byte swizzled), then written out so that
+          // one store instruction covers 4 rows x 128 contiguous bytes -- full-line
+          // requests over NVLink instead of 16-byte pieces of 32 different rows.
+          const int wrow0 = row0 + quarter * 32;
+          if (p.vec_ok && !p.dbg_skip_store && (BN % 64) == 0) {
+            uint8_t* buf = epi_buf;
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 64) {
+              uint32_t v[64];
+              tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+              tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+              tmem_ld_wait();
+              __syncwarp();  // the previous chunk's reads of buf are done
+              uint8_t* my_row = buf + lane * 128;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) = make_uint4(
+                    pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                    pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+              __syncwarp();
+              const int col0 = pid_n * BN + cc;
+              const int chunk = lane & 7;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rr = i * 4 + (lane >> 3);
+                const int grow = wrow0 + rr;
+                const int cbase = col0 + chunk * 8;
+                if (grow >= p.m || cbase >= p.n) continue;
+                const uint4 q = *reinterpret_cast<const uint4*>(buf + rr * 128 + ((chunk ^ (rr & 7)) << 4));
+                const int owner = static_cast<int>(grow / p.rows_per_rank);
+                const long long orow = grow - owner * p.rows_per_rank;
+                uint16_t* dst = static_cast<uint16_t*>(p.peer_slots[owner]) +
+                                (p.rank * p.rows_per_rank + orow) * p.slot_ld + cbase;
+                if (cbase + 8 <= p.n) {
+                  *reinterpret_cast<uint4*>(dst) = q;
+                } else {
+                  const uint16_t* e = reinterpret_cast<const uint16_t*>(&q);
+                  for (int t = 0; t < p.n - cbase; ++t) dst[t] = e[t];
+                }
+              }
+            }
+            __syncwarp();
+            if constexpr (MH == 2) arrive_empty(h);  // this half drained
+            continue;
+          }
+        }
 #pragma unroll 1
         for (int cc = 0; cc < BN; cc += 32) {
           uint32_t v[32];
