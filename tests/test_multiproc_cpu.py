@@ -58,7 +58,25 @@ def _worker(rank, world, port, q):
         t = torch.tensor([1.0 + rank, 5.0 - rank])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ok_max = t.tolist() == [float(world), 5.0]
-        q.put((rank, ok_blob, ok_maps, ok_first, ok_max))
+        # 4) the TP=world layer megakernel program (one launch per rank): every rank
+        #    builds byte-identical task queues, dependency rows and device tables,
+        #    and the two-shot allreduce tiles are split evenly by owner
+        import hashlib
+
+        from paper_2605_02953_b200 import build_topology
+        from paper_2605_02953_b200 import layer as L
+        from paper_2605_02953_b200 import megakernel as MK
+        prog = L.llama_layer_program(build_topology(world, 1), 1024, 1024, 8, 2, 2048, seq_len=512)
+        built = prog.build()
+        qs, cs = MK.encode_work_queues(built.tasks, 16)
+        cfg, specs = L.layer_tables(prog, built)
+        h = hashlib.sha256(MK.queues_to_bytes(qs) + MK.deps_to_bytes(built.dep_table) + cfg.tobytes()
+                           + specs.tobytes()).hexdigest()
+        hs = [None] * world
+        dist.all_gather_object(hs, h)
+        owners = [t.tile_id % world for t in built.tasks if built.layer_ops[t.layer_id] == "allreduce_residual"]
+        ok_layer = len(set(hs)) == 1 and all(owners.count(o) == owners.count(0) for o in range(world))
+        q.put((rank, ok_blob, ok_maps, ok_first, ok_max, ok_layer))
     finally:
         dist.destroy_process_group()
 
