@@ -582,7 +582,7 @@ def bench_attention_dist(dev, world, rank, steps, flush, peaks, shared_gpus):
 
     from paper_2605_02953_b200.attention import AllGatherKVAttention
     from paper_2605_02953_b200.shmem import Team
-    S, HQ, HKV, D = ATT_S, ATT_HQ, ATT_HKV, ATT_D
+    S, HQ, HKV, D = int(os.environ.get("TF_BENCH_ATT_S", ATT_S)), ATT_HQ, ATT_HKV, ATT_D
     sl = S // world
     team = Team.from_process_group(heap_bytes=4 * S * HKV * D * 2 + (16 << 20), signal_slots=256)
     g = torch.Generator(device="cpu").manual_seed(500 + rank)
@@ -910,7 +910,7 @@ def main_ours(args):
     attn = None
     if not args.no_attn and world == 1:
         attn = bench_attention(dev, 3, peaks)
-    elif not args.no_attn and not shared_gpus:
+    elif not args.no_attn and (not shared_gpus or os.environ.get("TF_BENCH_FORCE_DIST_ATTN")):
         try:  # failure-isolated, like the layer section
             attn = bench_attention_dist(dev, world, rank, 3, flush, peaks, shared_gpus)
         except Exception as exc:  # noqa: BLE001

@@ -29,7 +29,10 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "tf_internal.h"
 #include "tf_ptx.cuh"
@@ -54,6 +57,12 @@ struct AttnParams {
   unsigned long long epoch;
   unsigned long long* err;
   unsigned long long timeout_ns;
+  // direct mode: K/V tiles of chunk c are read over NVLink straight from rank c's
+  // workspace through chunk_maps[c] (K) / chunk_maps[nchunks + c] (V), once rank c's
+  // own flag peer_flags[c] reaches the epoch -- no staging copy
+  int direct, nchunks;
+  const CUtensorMap* chunk_maps;
+  const uint64_t* peer_flags[kMaxWorld];
 };
 
 // Two 128-query tiles (A, B) per CTA share every K/V tile; each has its own
@@ -232,19 +241,20 @@ __global__ void __maxnreg__(168)
         const int j = c >> 1, kv = c & 1;
         const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
         const int chunk = kt / p.tiles_per_chunk;
-        if (!kv && p.chunk_flags && !(ready & (1u << chunk))) {
-          wait_geq_sys(p.chunk_flags + chunk, p.epoch, p.timeout_ns, p.err,
-                       0x1000000ull | static_cast<unsigned>(chunk));
+        if (!kv && !(ready & (1u << chunk)) && (p.direct || p.chunk_flags)) {
+          const uint64_t* f = p.direct ? p.peer_flags[chunk] : p.chunk_flags + chunk;
+          wait_geq_sys(f, p.epoch, p.timeout_ns, p.err, 0x1000000ull | static_cast<unsigned>(chunk));
           fence_proxy_async_global();
           ready |= 1u << chunk;
         }
         const int sl = c % S::kSlots;
         mbar_wait(&r_empty[sl], ((c / S::kSlots) & 1) ^ 1);
         uint8_t* dst = sring + sl * S::kSlot;
-        const CUtensorMap* m = kv ? &tv : &tk;
+        const CUtensorMap* m = p.direct ? p.chunk_maps + kv * p.nchunks + chunk : (kv ? &tv : &tk);
+        const int row = p.direct ? (kt - chunk * p.tiles_per_chunk) * kKT : kt * kKT;
         mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
-        tma_load_3d(dst, m, &r_full[sl], 0, g, kt * kKT);
-        tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, kt * kKT);
+        tma_load_3d(dst, m, &r_full[sl], 0, g, row);
+        tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, row);
       }
     }
   } else if (warp == 1) {
@@ -682,6 +692,44 @@ int make_tmap_3d(CUtensorMap* map, const void* base, int64_t rows, int64_t heads
   return TF_OK;
 }
 
+// Device table of 2w tensor maps (K then V) over every rank's own chunk in its
+// workspace at buf_off, cached per (team, rank, chunk addresses).
+std::mutex g_chunk_mu;
+std::map<std::string, void*> g_chunk_maps;
+
+int chunk_maps_for(tf_team* t, int rank, size_t buf_off, size_t chunk_bytes, int64_t sl, int64_t hkv,
+                   int w, void** out) {
+  std::string key(reinterpret_cast<const char*>(&t), sizeof(t));
+  key.append(reinterpret_cast<const char*>(&rank), sizeof(rank));
+  const int64_t geom[3] = {sl, hkv, w};  // a recycled address must not reuse other dims
+  key.append(reinterpret_cast<const char*>(geom), sizeof(geom));
+  std::vector<const uint8_t*> bases;
+  for (int c = 0; c < w; ++c) {
+    bases.push_back(t->pes[c].base + buf_off + c * chunk_bytes);                     // K chunk c
+    bases.push_back(t->pes[c].base + buf_off + chunk_bytes * w + c * chunk_bytes);   // V chunk c
+  }
+  key.append(reinterpret_cast<const char*>(bases.data()), bases.size() * sizeof(void*));
+  std::lock_guard<std::mutex> lk(g_chunk_mu);
+  auto it = g_chunk_maps.find(key);
+  if (it != g_chunk_maps.end()) {
+    *out = it->second;
+    return TF_OK;
+  }
+  std::vector<CUtensorMap> host(2 * w);
+  for (int c = 0; c < w; ++c) {
+    int rc = make_tmap_3d(&host[c], bases[2 * c], sl, hkv);
+    if (rc) return rc;
+    rc = make_tmap_3d(&host[w + c], bases[2 * c + 1], sl, hkv);
+    if (rc) return rc;
+  }
+  void* dev = nullptr;
+  TF_CUDA_TRY(cudaMalloc(&dev, host.size() * sizeof(CUtensorMap)));
+  TF_CUDA_TRY(cudaMemcpy(dev, host.data(), host.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  g_chunk_maps[key] = dev;
+  *out = dev;
+  return TF_OK;
+}
+
 }  // namespace
 }  // namespace tf
 
@@ -727,17 +775,28 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
     const size_t buf_off = ws->data_off + par * 2 * chunk_bytes * w;
     uint8_t* kbuf = t->pes[rank].base + buf_off;
     uint8_t* vbuf = kbuf + chunk_bytes * w;
+    // CTA-pair variant (TF_ATTN_PAIR=1) when the local sequence splits into groups of
+    // 4 query tiles; measured slower than the single-CTA kernel at config 3 (4.75 vs
+    // 3.88 ms/rank: the pair's softmax warpgroups run in lockstep across two SMs), so
+    // it is opt-in
+    const char* pair_env = getenv("TF_ATTN_PAIR");
+    const bool pair = pair_env && atoi(pair_env) && sl % (4 * tf::kQT) == 0;
+    // single-CTA kernel: K/V read over NVLink straight from each owner's chunk (no
+    // staging copy; TF_ATTN_DIRECT=0 restores the copy-engine pull into this rank's
+    // workspace); the pair variant keeps the pull
+    const char* direct_env = getenv("TF_ATTN_DIRECT");
+    const bool direct = !pair && (!direct_env || atoi(direct_env));
     if (w > 1) {
       rc = tf::team_barrier_wait(t, rank, s);
       if (rc) return rc;
-      if (cs != s) {
+      if (cs != s && !direct) {
         cudaEvent_t ev;
         TF_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         TF_CUDA_TRY(cudaEventRecord(ev, s));
         TF_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
         cudaEventDestroy(ev);
       }
-      for (int i = 1; i < w; ++i) {
+      for (int i = 1; i < w && !direct; ++i) {
         const int src = (rank + i) % w;  // pull order of ag_gemm.py:64-69
         const uint8_t* pk = t->pes[src].base + buf_off;
         TF_CUDA_TRY(cudaMemcpyAsync(kbuf + src * chunk_bytes, pk + src * chunk_bytes, chunk_bytes,
@@ -748,12 +807,6 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
         if (rc) return rc;
       }
     }
-    // CTA-pair variant (TF_ATTN_PAIR=1) when the local sequence splits into groups of
-    // 4 query tiles; measured slower than the single-CTA kernel at config 3 (4.75 vs
-    // 3.88 ms/rank: the pair's softmax warpgroups run in lockstep across two SMs), so
-    // it is opt-in
-    const char* pair_env = getenv("TF_ATTN_PAIR");
-    const bool pair = pair_env && atoi(pair_env) && sl % (4 * tf::kQT) == 0;
     CUtensorMap tq, tk, tv;
     rc = tf::make_tmap_3d(&tq, a->q, sl, a->hq);
     if (rc) return rc;
@@ -772,6 +825,15 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
     p.scale_log2 = a->scale * 1.4426950408889634f;
     p.out = a->out;
     p.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
+    p.direct = direct ? 1 : 0;
+    p.nchunks = w;
+    if (direct) {
+      for (int c = 0; c < w; ++c) p.peer_flags[c] = t->pes[c].sig + ws->sig_base + par * w + c;
+      void* maps = nullptr;
+      rc = tf::chunk_maps_for(t, rank, buf_off, chunk_bytes, sl, a->hkv, w, &maps);
+      if (rc) return rc;
+      p.chunk_maps = static_cast<const CUtensorMap*>(maps);
+    }
     p.epoch = e;
     p.err = t->err_word(rank);
     p.timeout_ns = t->timeout_ns;
