@@ -43,6 +43,19 @@ namespace {
 constexpr int kChunk = 1024;  // (token, slot) entries per ranking chunk
 
 // ---------------------------------------------------------------- routing
+// Order-preserving float -> u32 (larger float => larger key); 0 marks "taken".
+__device__ __forceinline__ uint32_t f2key(float f) {
+  const uint32_t b = __float_as_uint(f + 0.0f);  // -0 -> +0: equal logits tie on the id
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// Warp per token.  Each lane keeps its best remaining logit (first index on
+// ties); a round is two warp reductions on the integer pipe (`redux.sync`: max
+// key, then min expert id among lanes holding it), so picks are identical to a
+// stable sort by (-logit, expert id).
 template <int VPL>  // logits per lane (E <= 32 * VPL)
 __global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, int E, int k,
                             int32_t* __restrict__ idx, float* __restrict__ w) {
@@ -50,38 +63,37 @@ __global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, in
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= tokens) return;
   const float* row = logits + t * E;
-  float v[VPL];
+  uint32_t key[VPL];
 #pragma unroll
   for (int c = 0; c < VPL; ++c) {  // coalesced: lane + 32c
     const int e = lane + 32 * c;
-    v[c] = e < E ? __ldg(row + e) : -INFINITY;
+    key[c] = e < E ? f2key(__ldg(row + e)) : 0u;
   }
-  float sel0 = 0.f, z = 0.f;
-  float my_val = 0.f;
+  auto lane_best = [&](uint32_t& bk, uint32_t& bi) {
+    bk = key[0];
+    bi = lane;
+#pragma unroll
+    for (int c = 1; c < VPL; ++c)
+      if (key[c] > bk) { bk = key[c]; bi = lane + 32 * c; }  // strict: first index wins
+  };
+  uint32_t bk, bi;
+  lane_best(bk, bi);
+  float sel0 = 0.f, z = 0.f, my_val = 0.f;
   int my_idx = 0;
   for (int r = 0; r < k; ++r) {
-    float best = -INFINITY;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int c = 0; c < VPL; ++c) {
-      const int e = lane + 32 * c;
-      if (e < E && (v[c] > best || (v[c] == best && e < bi))) { best = v[c]; bi = e; }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    if ((bi & 31) == lane) {
+    const uint32_t m = __reduce_max_sync(0xffffffffu, bk);
+    const uint32_t wi = __reduce_min_sync(0xffffffffu, bk == m ? bi : 0xFFFFFFFFu);
+    if ((wi & 31) == static_cast<uint32_t>(lane)) {
 #pragma unroll
       for (int c = 0; c < VPL; ++c)
-        if (c == (bi >> 5)) v[c] = -INFINITY;  // taken (ties resolve to lower id: stable)
+        if (c == static_cast<int>(wi >> 5)) key[c] = 0u;  // taken
+      lane_best(bk, bi);
     }
+    const float best = key2f(m);
     if (r == 0) sel0 = best;
     const float ez = __expf(best - sel0);
     z += ez;
-    if (lane == r) { my_val = ez; my_idx = bi; }
+    if (lane == r) { my_val = ez; my_idx = static_cast<int>(wi); }
   }
   if (lane < k) {
     idx[t * k + lane] = my_idx;
@@ -208,9 +220,12 @@ __global__ void __launch_bounds__(kChunk) count_fused_kernel(
     unsigned long long* err, int32_t* __restrict__ counts, int32_t* __restrict__ expert_base,
     int32_t* __restrict__ sorted_pos) {
   extern __shared__ int32_t fsm[];
-  int32_t* wc = fsm;              // [32 warps][E]
-  int32_t* tot = fsm + 32 * E;    // [E]
-  int32_t* off = tot + E;         // [E]
+  const int parts = max(1, kChunk / E);  // threads per expert for the cross-chunk sums
+  int32_t* wc = fsm;                // [32 warps][E] -> exclusive prefix over warps
+  int32_t* tot = fsm + 32 * E;      // [E]
+  int32_t* off = tot + E;           // [E]
+  int32_t* part_t = off + E;        // [parts][E]
+  int32_t* part_o = part_t + parts * E;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) wc[i] = 0;
@@ -223,7 +238,12 @@ __global__ void __launch_bounds__(kChunk) count_fused_kernel(
   __syncthreads();
   for (int x = threadIdx.x; x < E; x += blockDim.x) {
     int32_t sum = 0;
-    for (int w = 0; w < 32; ++w) sum += wc[w * E + x];
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) {  // in place: per-warp counts -> exclusive prefix
+      const int32_t v = wc[w * E + x];
+      wc[w * E + x] = sum;
+      sum += v;
+    }
     chunk_hist[static_cast<int64_t>(c) * E + x] = sum;
   }
   __syncthreads();
@@ -244,12 +264,25 @@ __global__ void __launch_bounds__(kChunk) count_fused_kernel(
     }
   }
   __syncthreads();
+  // totals and this chunk's offsets: `parts` threads per expert, strided chunks
+  for (int i = threadIdx.x; i < parts * E; i += blockDim.x) {
+    const int x = i % E, part = i / E;
+    int32_t t = 0, o = 0;
+#pragma unroll 8
+    for (int cc = part; cc < nchunks; cc += parts) {
+      const int32_t v = __ldcg(chunk_hist + static_cast<int64_t>(cc) * E + x);
+      o += cc < c ? v : 0;
+      t += v;
+    }
+    part_t[part * E + x] = t;
+    part_o[part * E + x] = o;
+  }
+  __syncthreads();
   for (int x = threadIdx.x; x < E; x += blockDim.x) {
     int32_t t = 0, o = 0;
-    for (int cc = 0; cc < nchunks; ++cc) {
-      const int32_t v = __ldcg(chunk_hist + static_cast<int64_t>(cc) * E + x);
-      if (cc < c) o += v;
-      t += v;
+    for (int part = 0; part < parts; ++part) {
+      t += part_t[part * E + x];
+      o += part_o[part * E + x];
     }
     tot[x] = t;
     off[x] = o;
@@ -260,11 +293,7 @@ __global__ void __launch_bounds__(kChunk) count_fused_kernel(
   block_exclusive_scan(tot, E);  // expert bases (ends with __syncthreads)
   if (c == 0)
     for (int x = threadIdx.x; x < E; x += blockDim.x) expert_base[x] = tot[x];
-  if (e >= 0) {
-    int before = 0;
-    for (int w2 = 0; w2 < warp; ++w2) before += wc[w2 * E + e];
-    sorted_pos[g] = tot[e] + off[e] + before + in_warp;
-  }
+  if (e >= 0) sorted_pos[g] = tot[e] + off[e] + wc[warp * E + e] + in_warp;
 }
 
 // ---------------------------------------------------------------- exchange / layout
@@ -456,6 +485,72 @@ __global__ void __launch_bounds__(256) combine_kernel(
   }
 }
 
+// k <= 8: U hidden vectors per lane per iteration, so a warp keeps U*k 16-byte
+// loads in flight (read-once rows: no L1 allocation).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) combine8_kernel(
+    int64_t tokens, int64_t vec_per_row, int k, int E, int world,
+    const int32_t* __restrict__ idx, const float* __restrict__ w,
+    const int32_t* __restrict__ dest_row, PeerPtrs yout, uint4* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int epr = E / world;
+  for (int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; t < tokens;
+       t += nwarps) {
+    // lane j < k resolves slot j, then the warp shares it
+    const uint4* my_row = nullptr;
+    float my_w = 0.f;
+    if (lane < k) {
+      const int e = idx[t * k + lane];
+      my_row = static_cast<const uint4*>(yout.p[e / epr]) +
+               static_cast<int64_t>(dest_row[t * k + lane]) * vec_per_row;
+      my_w = w[t * k + lane];
+    }
+    const uint4* rows[8];
+    float wt[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      rows[j] = reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_row), j));
+      wt[j] = __shfl_sync(0xffffffffu, my_w, j);
+    }
+    for (int64_t v0 = lane; v0 < vec_per_row; v0 += 32 * U) {
+      uint4 val[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < k && v0 + 32 * u < vec_per_row) val[u][j] = ld_stream(rows[j] + v0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v0 + 32 * u >= vec_per_row) break;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j < k) {
+            const uint32_t q4[4] = {val[u][j].x, val[u][j].y, val[u][j].z, val[u][j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc[2 * q] = fmaf(wt[j], __uint_as_float(q4[q] << 16), acc[2 * q]);
+              acc[2 * q + 1] = fmaf(wt[j], __uint_as_float(q4[q] & 0xFFFF0000u), acc[2 * q + 1]);
+            }
+          }
+        }
+        out[t * vec_per_row + v0 + 32 * u] =
+            make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+      }
+    }
+  }
+}
+
 int64_t count_scratch_bytes(int64_t entries, int E) {
   const int64_t nchunks = (entries + kChunk - 1) / kChunk;
   return (std::max<int64_t>(nchunks, 1) * E + E) * 4 + 256;
@@ -472,7 +567,7 @@ int run_count(const int32_t* idx, int64_t entries, int E, int32_t* counts, int32
     // single-pass path when every chunk CTA can be co-resident
     int dev = 0;
     cudaGetDevice(&dev);
-    const size_t fsm = static_cast<size_t>(34) * E * 4;
+    const size_t fsm = (static_cast<size_t>(34) * E + 2 * static_cast<size_t>(std::max(1, kChunk / E)) * E) * 4;
     static std::map<int, unsigned long long*> flag_bufs;
     static std::map<int, unsigned long long> epochs;
     static std::mutex mu;
@@ -701,9 +796,28 @@ int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* 
     tf::PeerPtrs y{};
     for (int p = 0; p < w; ++p) y.p[p] = t->pes[p].base + m.yout_off;
     if (a->tokens > 0)
-      tf::combine_kernel<<<tf::grid_for(a->tokens), 256, 0, s>>>(
-          a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
-          static_cast<uint4*>(a->out));
+    {
+      static const int cv = [] {
+        const char* e = getenv("TF_MOE_COMBINE_U");
+        return e ? atoi(e) : 2;
+      }();
+      if (a->k <= 8 && cv == 2)
+        tf::combine8_kernel<2><<<tf::grid_for(a->tokens), 256, 0, s>>>(
+            a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
+            static_cast<uint4*>(a->out));
+      else if (a->k <= 8 && cv == 4)
+        tf::combine8_kernel<4><<<tf::grid_for(a->tokens), 256, 0, s>>>(
+            a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
+            static_cast<uint4*>(a->out));
+      else if (a->k <= 8 && cv == 1)
+        tf::combine8_kernel<1><<<tf::grid_for(a->tokens), 256, 0, s>>>(
+            a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
+            static_cast<uint4*>(a->out));
+      else
+        tf::combine_kernel<<<tf::grid_for(a->tokens), 256, 0, s>>>(
+            a->tokens, a->hidden / 8, a->k, a->n_experts, w, a->topk_idx, a->topk_w, a->dest_row, y,
+            static_cast<uint4*>(a->out));
+    }
     TF_CUDA_TRY(cudaGetLastError());
   }
   return TF_OK;
