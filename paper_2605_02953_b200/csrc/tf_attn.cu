@@ -157,8 +157,29 @@ __device__ __forceinline__ float ex2(float x) {
 #ifndef TF_ATTN_SPLIT_P
 #define TF_ATTN_SPLIT_P 1  // release P's first 64 keys to the MMA before the rest
 #endif
+#ifndef TF_ATTN_MMA_POLL
+#define TF_ATTN_MMA_POLL 0
+#endif
+#if TF_ATTN_MMA_POLL == 1
+#define MMA_WAIT mbar_wait_poll
+#elif TF_ATTN_MMA_POLL == 2
+#define MMA_WAIT mbar_wait
+#else
+#define MMA_WAIT mbar_wait_spin
+#endif
+#ifndef TF_ATTN_SM_SLEEP
+#define TF_ATTN_SM_SLEEP 0
+#endif
+#if TF_ATTN_SM_SLEEP
+#define SM_WAIT mbar_wait
+#else
+#define SM_WAIT mbar_wait_spin
+#endif
+#ifndef TF_ATTN_STAGGER
+#define TF_ATTN_STAGGER 0  // per-CTA rotation inside a chunk: measured neutral (no L2 hot spot)
+#endif
 #ifndef TF_EXP2_EMU_MASK
-#define TF_EXP2_EMU_MASK -1  // off: measured slower on B200 (4.43 -> 4.83 ms at 25%); 3 -> 25%, 1 -> 50%
+#define TF_EXP2_EMU_MASK 7  // 1 pair in 8 on the FMA pipe (12.5%): 3.63 vs 3.70 ms; 25% is slower (3.84)
 #endif
 __device__ __forceinline__ float ex2_fma(float x) {
   const float y = fmaxf(x, -126.f);
@@ -166,6 +187,48 @@ __device__ __forceinline__ float ex2_fma(float x) {
   const float f = y - (t - 12582912.f);
   const float pl = fmaf(fmaf(fmaf(0.0555041f, f, 0.2402265f), f, 0.6931472f), f, 1.0f);
   return __int_as_float(__float_as_int(pl) + (__float_as_int(t) << 23));
+}
+
+// Blackwell paired-fp32 ops (FFMA2 / FADD2) and the 3-input max (FMNMX3): the
+// softmax is issue-bound, these halve its FMA/ADD/MAX instruction count.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// two 2^x on the FMA pipe with paired ops (same polynomial as ex2_fma)
+__device__ __forceinline__ void ex2_fma2(float x0, float x1, float& r0, float& r1) {
+  const uint64_t y = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = fadd2(y, f2pack(12582912.f, 12582912.f));
+  const uint64_t k = fadd2(t, f2pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(k, f2pack(-1.f, -1.f), y);
+  uint64_t pl = ffma2(f2pack(0.0555041f, 0.0555041f), f, f2pack(0.2402265f, 0.2402265f));
+  pl = ffma2(pl, f, f2pack(0.6931472f, 0.6931472f));
+  pl = ffma2(pl, f, f2pack(1.0f, 1.0f));
+  float p0, p1, t0, t1;
+  f2unpack(pl, p0, p1);
+  f2unpack(t, t0, t1);
+  r0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
 // D[tmem] (+)= A[tmem] * B[smem]^T: the A operand (P, bf16 pairs packed per 32-bit
@@ -179,6 +242,17 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+
+#ifdef TF_ATTN_TRACE
+// debug: SM clock stamps of CTA (0, 0) per key tile: [j][0..1] softmax t got S,
+// [2..3] softmax t released P, [4..5] MMA issued PV_t, [6..7] MMA issued S_t(j+1),
+// [8] MMA has V_j and K_j+1, [9] producer issues K_j, [10] producer issues V_j
+__device__ long long g_attn_trace[512][16];
+#define ATTN_STAMP(j, e) \
+  do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 512) g_attn_trace[j][e] = clock64(); } while (0)
+#else
+#define ATTN_STAMP(j, e) do { } while (0)
+#endif
 
 __global__ void __maxnreg__(168)
     ag_attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -237,9 +311,14 @@ __global__ void __maxnreg__(168)
         tma_load_3d(sq + t * S::kQ + kHalf, &tq, q_full, 64, h, q0 + t * kQT);
       }
       uint32_t ready = 0;
+      // gather order: own chunk first, chunks in rank order; inside a chunk each CTA
+      // starts at its own offset so the CTAs sharing a KV head do not all request the
+      // same tile from L2 at once (same-line hot spots stretched loads to ~3.6k clk)
+      const int tpc = p.tiles_per_chunk;
+      const int rot = TF_ATTN_STAGGER ? static_cast<int>((blockIdx.x * 8 + blockIdx.y % 8) % tpc) : 0;
       for (int c = 0; c < 2 * n; ++c) {  // K_j = 2j, V_j = 2j + 1
         const int j = c >> 1, kv = c & 1;
-        const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
+        const int kt = ((p.start_tile / tpc + j / tpc) % (n / tpc)) * tpc + (rot + j) % tpc;
         const int chunk = kt / p.tiles_per_chunk;
         if (!kv && !(ready & (1u << chunk)) && (p.direct || p.chunk_flags)) {
           const uint64_t* f = p.direct ? p.peer_flags[chunk] : p.chunk_flags + chunk;
@@ -253,6 +332,7 @@ __global__ void __maxnreg__(168)
         const CUtensorMap* m = p.direct ? p.chunk_maps + kv * p.nchunks + chunk : (kv ? &tv : &tk);
         const int row = p.direct ? (kt - chunk * p.tiles_per_chunk) * kKT : kt * kKT;
         mbar_arrive_expect_tx(&r_full[sl], S::kSlot);
+        ATTN_STAMP(j, 9 + kv);
         tma_load_3d(dst, m, &r_full[sl], 0, g, row);
         tma_load_3d(dst + kHalf, m, &r_full[sl], 64, g, row);
       }
@@ -265,7 +345,7 @@ __global__ void __maxnreg__(168)
     constexpr uint32_t idesc_s = umma_idesc_bf16(kQT, kKT);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(kQT, kD) | (1u << 16);  // B (V) MN-major
     if (lane == 0) {
-      mbar_wait_spin(q_full, 0);
+      MMA_WAIT(q_full, 0);
       tc_fence_after();
       auto issue_s = [&](int t, int sl) {
         const uint32_t qa = smem_u32(sq + t * S::kQ);
@@ -278,30 +358,34 @@ __global__ void __maxnreg__(168)
         }
         umma_commit(&s_full[t]);
       };
-      mbar_wait_spin(&r_full[0], 0);
+      MMA_WAIT(&r_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < nq; ++t) issue_s(t, 0);
       umma_commit(&r_empty[0]);
       for (int j = 0; j < n; ++j) {
         const int cv = 2 * j + 1, vs = cv % S::kSlots;
         const int ck = 2 * j + 2, ks = ck % S::kSlots;
-        mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
-        if (j + 1 < n) mbar_wait_spin(&r_full[ks], (ck / S::kSlots) & 1);
+        MMA_WAIT(&r_full[vs], (cv / S::kSlots) & 1);
+        ATTN_STAMP(j, 11);
+        if (j + 1 < n) MMA_WAIT(&r_full[ks], (ck / S::kSlots) & 1);
+        ATTN_STAMP(j, 8);
         for (int t = 0; t < nq; ++t) {
           const uint32_t vb = smem_u32(sring + vs * S::kSlot);
           // keys 0-63 of P_t(j) as soon as the softmax has them, keys 64-127 after
-          mbar_wait_spin(&p_half[t], j & 1);
+          MMA_WAIT(&p_half[t], j & 1);
           tc_fence_after();
+          ATTN_STAMP(j, 4 + t);
 #pragma unroll
           for (int kk = 0; kk < kKT / 32; ++kk)
             umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                          umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (j | kk) != 0);
-          mbar_wait_spin(&p_full[t], j & 1);
+          MMA_WAIT(&p_full[t], j & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = kKT / 32; kk < kKT / 16; ++kk)
             umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                          umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, 1);
+          ATTN_STAMP(j, 6 + t);
           if (j + 1 < n) issue_s(t, ks);
           else umma_commit(&o_ready[t]);
         }
@@ -320,21 +404,20 @@ __global__ void __maxnreg__(168)
       const uint32_t t_o = tmem + lane_off + 256 + t * 128;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
-        mbar_wait_spin(&s_full[t], j & 1);
+        SM_WAIT(&s_full[t], j & 1);
         tc_fence_after();
+        if (threadIdx.x % 128 == 64) ATTN_STAMP(j, t);
         uint32_t sv[4][32];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
         tmem_ld_wait();
-        float mx0 = -INFINITY, mx1 = -INFINITY;
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            mx0 = fmaxf(mx0, __uint_as_float(sv[c][i]));
-            mx1 = fmaxf(mx1, __uint_as_float(sv[c][i + 1]));
-          }
-        const float mt = fmaxf(mx0, mx1) * p.scale_log2;
+          for (int i = 0; i < 32; i += 2)
+            mx[c] = fmax3(mx[c], __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
         // lazy rescale: keep a stale running max unless the new one exceeds it by > 8
         float alpha = 1.f;
         if (mt > m + kLazyRescale) {
@@ -354,7 +437,8 @@ __global__ void __maxnreg__(168)
             tmem_st_32x32b_x16(t_o + c * 16, ov);
           }
         }
-        float s0 = 0.f, s1 = 0.f;
+        uint64_t sum2 = f2pack(0.f, 0.f);
+        const uint64_t scale2 = f2pack(p.scale_log2, p.scale_log2), negm2 = f2pack(-m, -m);
         // P row packed in place of the first 64 S columns (the whole row is in registers),
         // in two halves of 64 keys: PV on the first half overlaps the second half's exps
 #pragma unroll
@@ -364,18 +448,23 @@ __global__ void __maxnreg__(168)
             const int c = 2 * hk + cc;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float a0 = fmaf(__uint_as_float(sv[c][2 * i]), p.scale_log2, -m);
-              const float a1 = fmaf(__uint_as_float(sv[c][2 * i + 1]), p.scale_log2, -m);
+              float a0, a1;
+              f2unpack(ffma2(f2pack(__uint_as_float(sv[c][2 * i]), __uint_as_float(sv[c][2 * i + 1])),
+                             scale2, negm2), a0, a1);
               const bool emu = TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0;
 #ifdef TF_ATTN_EXP_CHEAP  // bottleneck experiment: no SFU work
               const float p0 = a0 * 0.001f, p1 = a1 * 0.001f;
               (void)emu;
 #else
-              const float p0 = emu ? ex2_fma(a0) : ex2(a0);
-              const float p1 = emu ? ex2_fma(a1) : ex2(a1);
+              float p0, p1;
+              if (emu) {
+                ex2_fma2(a0, a1, p0, p1);
+              } else {
+                p0 = ex2(a0);
+                p1 = ex2(a1);
+              }
 #endif
-              s0 += p0;
-              s1 += p1;
+              sum2 = fadd2(sum2, f2pack(p0, p1));
               sv[hk][cc * 16 + i] = pack_bf16x2(p0, p1);
             }
           }
@@ -385,6 +474,9 @@ __global__ void __maxnreg__(168)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(hk == 0 ? &p_half[t] : &p_full[t]);
+          if (hk == 1 && threadIdx.x % 128 == 64) ATTN_STAMP(j, 2 + t);
+          if (hk == 1 && threadIdx.x % 128 == 0) ATTN_STAMP(j, 14 + t);
+          if (hk == 1 && threadIdx.x % 128 == 32) ATTN_STAMP(j, 12 + t);
 #else
           if (hk == 1) {
             tmem_st_wait();
@@ -397,6 +489,8 @@ __global__ void __maxnreg__(168)
           }
 #endif
         }
+        float s0, s1;
+        f2unpack(sum2, s0, s1);
         l = l * alpha + (s0 + s1);
       }
       mbar_wait_spin(&o_ready[t], 0);
@@ -887,3 +981,9 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
   }
   return TF_OK;
 }
+
+#ifdef TF_ATTN_TRACE
+extern "C" int tf_attn_trace_dump(long long* out) {
+  return cudaMemcpyFromSymbol(out, tf::g_attn_trace, sizeof(tf::g_attn_trace)) == cudaSuccess ? 0 : 5;
+}
+#endif
