@@ -933,7 +933,7 @@ def main_ours(args):
     attn = None
     if not args.no_attn and world == 1:
         attn = bench_attention(dev, 3, peaks)
-    elif not args.no_attn and (not shared_gpus or os.environ.get("TF_BENCH_FORCE_DIST_ATTN")):
+    elif not args.no_attn:
         try:  # failure-isolated, like the layer section
             attn = bench_attention_dist(dev, world, rank, 3, flush, peaks, shared_gpus)
         except Exception as exc:  # noqa: BLE001
