@@ -435,6 +435,93 @@ __global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores globally done
 }
 
+// Persistent, double-buffered variant: each warp walks (token, piece) tasks with a
+// grid stride and keeps two row pieces in shared memory, so the bulk load of task
+// i+1 is in flight while task i's bulk / P2P stores drain.
+constexpr int kScatter2Warps = 4;
+constexpr int kScatter2Buf = 8192;  // bytes per buffer, two buffers per warp
+
+__global__ void __launch_bounds__(32 * kScatter2Warps) scatter2_kernel(
+    const uint4* __restrict__ x, int64_t tokens, int64_t vec_per_row, int k, int E, int world,
+    const int32_t* __restrict__ idx, const int32_t* __restrict__ sorted_pos,
+    const int32_t* __restrict__ expert_base, const int32_t* __restrict__ seg_base,
+    int32_t* __restrict__ dest_row, PeerPtrs recv, int64_t max_recv, unsigned long long* err, int rank) {
+  extern __shared__ __align__(128) uint8_t sbuf[];
+  __shared__ uint64_t bar[2 * kScatter2Warps];
+  __shared__ uint4* sdst[kScatter2Warps][16];  // this task's destinations (lane j -> slot j)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* const buf0 = sbuf + (2 * wib) * kScatter2Buf;  // buffer b at buf0 + b * kScatter2Buf
+  uint64_t* bars = bar + 2 * wib;
+  if (lane == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  uint32_t phases = 0;  // bit b: parity of buffer b's barrier
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int epr = E / world;
+  constexpr int64_t kPiece = kScatter2Buf / 16;  // uint4 per piece
+  const int64_t npieces = (vec_per_row + kPiece - 1) / kPiece;
+  const int64_t ntasks = tokens * npieces;
+  auto piece_bytes = [&](int64_t wi) {
+    const int64_t v0 = (wi % npieces) * kPiece;
+    return static_cast<uint32_t>((min(v0 + kPiece, vec_per_row) - v0) * 16);
+  };
+  auto issue_load = [&](int64_t wi, int b) {  // lane 0 only
+    const int64_t t = wi / npieces, v0 = (wi % npieces) * kPiece;
+    const uint32_t bytes = piece_bytes(wi);
+    mbar_arrive_expect_tx(&bars[b], bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(buf0 + b * kScatter2Buf)),
+        "l"(x + t * vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bars[b]))
+        : "memory");
+  };
+  int64_t wi = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (lane == 0 && wi < ntasks) issue_load(wi, 0);
+  for (int b = 0; wi < ntasks; wi += nwarps, b ^= 1) {
+    const int64_t t = wi / npieces, piece = wi % npieces;
+    const int64_t v0 = piece * kPiece;
+    const uint32_t bytes = piece_bytes(wi);
+    uint4* my_dst = nullptr;
+    int my_remote = 0;
+    if (lane < k) {
+      const int64_t slot = t * k + lane;
+      const int e = idx[slot];
+      const int64_t row = static_cast<int64_t>(seg_base[e]) + (sorted_pos[slot] - expert_base[e]);
+      if (piece == 0) dest_row[slot] = static_cast<int32_t>(row);
+      if (row < max_recv) my_dst = static_cast<uint4*>(recv.p[e / epr]) + row * vec_per_row + v0;
+      else if (err) atomicCAS(err, 0ull, 0x5000000ull | 0xFFFFFFull);
+      my_remote = (e / epr) != rank;
+    }
+    if (lane < k) sdst[wib][lane] = my_dst;
+    __syncwarp();
+    const unsigned remote = __ballot_sync(0xffffffffu, my_remote != 0 && my_dst != nullptr);
+    mbar_wait(&bars[b], (phases >> b) & 1);  // task wi's piece is in buffer b
+    phases ^= 1u << b;
+    if (lane == 0) {
+      // the other buffer's stores (task wi - nwarps) must have finished reading it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (wi + nwarps < ntasks) issue_load(wi + nwarps, b ^ 1);
+      for (int j = 0; j < k; ++j)
+        if (sdst[wib][j] != nullptr && !((remote >> j) & 1))
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[wib][j]),
+                       "r"(smem_u32(buf0 + b * kScatter2Buf)), "r"(bytes)
+                       : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (int j = 0; j < k; ++j) {
+      if (!((remote >> j) & 1)) continue;
+      uint4* d = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(my_dst), j));
+      const uint4* sb = reinterpret_cast<const uint4*>(buf0 + b * kScatter2Buf);
+      for (int v = lane; v < static_cast<int>(bytes / 16); v += 32) d[v] = sb[v];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores globally done
+}
+
 // after the scatter kernel (stream order): release "source `rank` delivered" on every owner
 __global__ void release_kernel(PeerSig flags, int world, int rank, uint64_t epoch) {
   if (threadIdx.x < world) {
@@ -755,10 +842,36 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
       attr_done |= 1ull << dev;
     }
     if (entries > 0)
-      tf::scatter_kernel<<<tf::grid_for(a->tokens * ((a->hidden / 8 + 511) / 512)), 32 * tf::kScatterWarps,
-                           tf::kScatterWarps * tf::kScatterBuf, s>>>(
-          static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
-          a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank), rank);
+    {
+      static const int sv = [] {
+        const char* e = getenv("TF_MOE_SCATTER");
+        return e ? atoi(e) : 2;
+      }();
+      if (sv == 2) {
+        static uint64_t attr2 = 0;
+        constexpr int smem2 = 2 * tf::kScatter2Warps * tf::kScatter2Buf;
+        if (!(attr2 & (1ull << dev))) {
+          TF_CUDA_TRY(cudaFuncSetAttribute(tf::scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           smem2));
+          attr2 |= 1ull << dev;
+        }
+        int per_sm = 0;
+        TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tf::scatter2_kernel,
+                                                                  32 * tf::kScatter2Warps, smem2));
+        const int64_t tasks = a->tokens * ((a->hidden / 8 + tf::kScatter2Buf / 16 - 1) / (tf::kScatter2Buf / 16));
+        const int64_t cap = static_cast<int64_t>(tf::num_sms_of_current_device()) * std::max(per_sm, 1);
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, (tasks + tf::kScatter2Warps - 1) /
+                                                                                        tf::kScatter2Warps)));
+        tf::scatter2_kernel<<<grid, 32 * tf::kScatter2Warps, smem2, s>>>(
+            static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
+            a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank), rank);
+      } else {
+        tf::scatter_kernel<<<tf::grid_for(a->tokens * ((a->hidden / 8 + 511) / 512)), 32 * tf::kScatterWarps,
+                             tf::kScatterWarps * tf::kScatterBuf, s>>>(
+            static_cast<const uint4*>(a->x), a->tokens, a->hidden / 8, a->k, E, w, a->topk_idx,
+            a->sorted_pos, ebase, seg_base, a->dest_row, recv, a->max_recv, t->err_word(rank), rank);
+      }
+    }
     if (w > 1) tf::release_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
@@ -824,3 +937,4 @@ int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* 
 }
 
 }  // extern "C"
+

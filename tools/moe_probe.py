@@ -56,6 +56,16 @@ def main():
     yo = ep.expert_out()[:n]
     res["read_470MB_sum"] = timed(lambda: yo.sum(dtype=torch.float32))
     res["copy_470MB"] = timed(lambda: big.copy_(yo.view(-1).view(torch.uint8)))
+    try:  # driver memset: the write-only ceiling for the dispatch's 470 MB of row writes
+        import ctypes
+        import nvidia.cuda_runtime as ncr
+        rt = ctypes.CDLL(os.path.join(os.path.dirname(ncr.__file__), "lib", "libcudart.so.12"))
+        st = torch.cuda.current_stream().cuda_stream
+        res["cudaMemset_470MB"] = timed(lambda: rt.cudaMemsetAsync(ctypes.c_void_p(big.data_ptr()), 0,
+                                                                   ctypes.c_size_t(rows), ctypes.c_void_p(st)))
+        print(f"memset write {rows / res['cudaMemset_470MB'] / 1e6:.0f} GB/s")
+    except Exception as e:  # noqa: BLE001
+        print("cudaMemset probe failed:", e)
     for k_, v in res.items():
         print(f"{k_:16s} {v * 1e3:8.1f} us")
     print(f"dispatch bytes {(xb + rows) / 1e6:.0f} MB -> {(xb + rows) / res['dispatch'] / 1e6:.0f} GB/s;"
