@@ -231,6 +231,37 @@ __device__ __forceinline__ void ex2_fma2(float x0, float x1, float& r0, float& r
   r1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
+// Warp-converged issue: every lane runs the MMA loop (so descriptor math stays on
+// the uniform datapath) and elect.sync picks the one lane that issues.
+__device__ __forceinline__ void umma_ss_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]^T: the A operand (P, bf16 pairs packed per 32-bit
 // column, rows = lanes) is read from tensor memory, so P never touches shared memory
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
@@ -247,7 +278,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 // debug: SM clock stamps of CTA (0, 0) per key tile: [j][0..1] softmax t got S,
 // [2..3] softmax t released P, [4..5] MMA issued PV_t, [6..7] MMA issued S_t(j+1),
 // [8] MMA has V_j and K_j+1, [9] producer issues K_j, [10] producer issues V_j
-__device__ long long g_attn_trace[512][16];
+__device__ long long g_attn_trace[512][20];
 #define ATTN_STAMP(j, e) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 512) g_attn_trace[j][e] = clock64(); } while (0)
 #else
@@ -344,24 +375,36 @@ __global__ void __maxnreg__(168)
     // the softmax's rescale)
     constexpr uint32_t idesc_s = umma_idesc_bf16(kQT, kKT);
     constexpr uint32_t idesc_pv = umma_idesc_bf16(kQT, kD) | (1u << 16);  // B (V) MN-major
-    if (lane == 0) {
+    {  // all 32 lanes: uniform control flow, one elected lane issues
       MMA_WAIT(q_full, 0);
       tc_fence_after();
+      // descriptors as (low word + compile-time delta, constant high word): the per-MMA
+      // address math is one add, so the single MMA thread issues without long gaps
+      // (it shares its SMSP with two softmax warps)
+      constexpr uint32_t kDescHi = (1024 >> 4) | (1u << (46 - 32)) | (2u << (61 - 32));
+      constexpr uint32_t kLoK = 1u << 16;                    // K-major SW128, LBO field 1
+      constexpr uint32_t kLoV = ((kHalf >> 4) & 0x3FFF) << 16;  // MN-major V, LBO = kHalf
+      auto mk = [](uint32_t lo) {
+        uint64_t d;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(kDescHi));
+        return d;
+      };
+      const uint32_t q_lo0 = ((smem_u32(sq) & 0x3FFFF) >> 4) | kLoK;
+      const uint32_t ring_lo = (smem_u32(sring) & 0x3FFFF) >> 4;
       auto issue_s = [&](int t, int sl) {
-        const uint32_t qa = smem_u32(sq + t * S::kQ);
-        const uint32_t kb = smem_u32(sring + sl * S::kSlot);
+        const uint32_t qa = q_lo0 + t * (S::kQ >> 4);
+        const uint32_t kb = (ring_lo + sl * (S::kSlot >> 4)) | kLoK;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalf + (kk & 3) * 32;
-          umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off), idesc_s,
-                    kk != 0);
+          const uint32_t off = (kk >> 2) * (kHalf >> 4) + (kk & 3) * 2;
+          umma_ss_elect(tmem + t * 128, mk(qa + off), mk(kb + off), idesc_s, kk != 0);
         }
-        umma_commit(&s_full[t]);
+        umma_commit_elect(&s_full[t]);
       };
       MMA_WAIT(&r_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < nq; ++t) issue_s(t, 0);
-      umma_commit(&r_empty[0]);
+      umma_commit_elect(&r_empty[0]);
       for (int j = 0; j < n; ++j) {
         const int cv = 2 * j + 1, vs = cv % S::kSlots;
         const int ck = 2 * j + 2, ks = ck % S::kSlots;
@@ -369,28 +412,29 @@ __global__ void __maxnreg__(168)
         ATTN_STAMP(j, 11);
         if (j + 1 < n) MMA_WAIT(&r_full[ks], (ck / S::kSlots) & 1);
         ATTN_STAMP(j, 8);
+        const uint32_t vb = (ring_lo + vs * (S::kSlot >> 4)) | kLoV;
         for (int t = 0; t < nq; ++t) {
-          const uint32_t vb = smem_u32(sring + vs * S::kSlot);
+          const uint32_t pa = tmem + t * 128, od = tmem + 256 + t * 128;
           // keys 0-63 of P_t(j) as soon as the softmax has them, keys 64-127 after
+          if (t == 0) ATTN_STAMP(j, 16);
           MMA_WAIT(&p_half[t], j & 1);
+          if (t == 0) ATTN_STAMP(j, 17);
           tc_fence_after();
           ATTN_STAMP(j, 4 + t);
 #pragma unroll
           for (int kk = 0; kk < kKT / 32; ++kk)
-            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                         umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, (j | kk) != 0);
+            umma_ts_elect(od, pa + kk * 8, mk(vb + kk * (2048 >> 4)), idesc_pv, (j | kk) != 0);
           MMA_WAIT(&p_full[t], j & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = kKT / 32; kk < kKT / 16; ++kk)
-            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                         umma_desc_mn_sw128(vb + kk * 2048, kHalf), idesc_pv, 1);
+            umma_ts_elect(od, pa + kk * 8, mk(vb + kk * (2048 >> 4)), idesc_pv, 1);
           ATTN_STAMP(j, 6 + t);
           if (j + 1 < n) issue_s(t, ks);
-          else umma_commit(&o_ready[t]);
+          else umma_commit_elect(&o_ready[t]);
         }
-        umma_commit(&r_empty[vs]);
-        if (j + 1 < n) umma_commit(&r_empty[ks]);
+        umma_commit_elect(&r_empty[vs]);
+        if (j + 1 < n) umma_commit_elect(&r_empty[ks]);
       }
     }
     __syncwarp();

@@ -15,11 +15,11 @@ import bench  # noqa: E402
 from paper_2605_02953_b200 import _lib  # noqa: E402
 
 print(bench.bench_attention(0, 2, {}))
-buf = np.zeros((512, 16), dtype=np.int64)
+buf = np.zeros((512, 20), dtype=np.int64)
 lib = _lib.lib() if callable(getattr(_lib, "lib", None)) else _lib._LIB
 assert lib.tf_attn_trace_dump(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
 t0 = buf[0, 0]
-names = ["gotS_A", "gotS_B", "relP_A", "relP_B", "PV_A", "PV_B", "S+_A", "S+_B", "mmaKV", "ldK", "ldV", "mmaV", "relP_A1", "relP_B1", "relP_A0", "relP_B0"]
+names = ["gotS_A", "gotS_B", "relP_A", "relP_B", "PV_A", "PV_B", "S+_A", "S+_B", "mmaKV", "ldK", "ldV", "mmaV", "relP_A1", "relP_B1", "relP_A0", "relP_B0", "preHalfA", "postHalfA", "-", "-"]
 print("j  " + " ".join(f"{n:>8s}" for n in names) + "   period")
 for j in list(range(0, 6)) + list(range(100, 112)) + list(range(250, 256)):
     row = buf[j] - buf[j, 0]
