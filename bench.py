@@ -97,9 +97,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def wait_first(self, timeout=3.0):
+        """Block until nvidia-smi has produced a sample (its start-up takes ~0.3 s)."""
+        t_end = time.time() + timeout
+        while self.proc is not None and not self.lines and time.time() < t_end:
+            time.sleep(0.01)
+
+    def stop(self, t0=None, t1=None):
+        """Summarise the samples taken inside [t0, t1] (the timed region; the
+        nearest later sample if none fell inside)."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -107,9 +115,13 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        lines = [ln for ts, ln in self.lines if t0 is None or (t0 <= ts <= t1 + 0.05)]
+        if not lines and t0 is not None:
+            later = [ln for ts, ln in self.lines if ts >= t0]
+            lines = later[:1]
         sms, maxes, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -784,7 +796,8 @@ def main_ours(args):
         torch.cuda.synchronize()
         clocks = ClockSampler(dev)
         clocks.start()
-        time.sleep(0.3)
+        clocks.wait_first()
+        t_clk0 = time.time()
         for i in range(args.steps):
             flush.zero_()  # evict L2 between steps (outside the per-step events)
             ev[i][0].record(stream)
@@ -793,9 +806,10 @@ def main_ours(args):
             rs(h, w2, y)
             ev[i][2].record(stream)
         torch.cuda.synchronize()
+        t_clk1 = time.time()
         barrier()
         torch.cuda.synchronize()
-        clk = clocks.stop()
+        clk = clocks.stop(t_clk0, t_clk1)
     team.check()
     ag_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(n_events)]
     rs_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(n_events)]
