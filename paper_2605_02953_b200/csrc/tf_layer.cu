@@ -183,15 +183,19 @@ __device__ __forceinline__ void tma_load_3d_l(void* smem_dst, const void* tmap, 
       : "memory");
 }
 
-__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t lbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
+// Descriptor = (low word, constant high word): per-MMA address math is one add on
+// the low word (the single MMA thread shares its SMSP with epilogue/softmax warps).
+constexpr uint32_t kDescHi = (1024 >> 4) | (1u << (46 - 32)) | (2u << (61 - 32));
+__device__ __forceinline__ uint64_t desc_from_lo(uint32_t lo) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(kDescHi));
   return d;
 }
+__device__ __forceinline__ uint32_t desc_lo_k(uint32_t addr) { return ((addr & 0x3FFFF) >> 4) | (1u << 16); }
+__device__ __forceinline__ uint32_t desc_lo_mn(uint32_t addr, uint32_t lbo) {
+  return ((addr & 0x3FFFF) >> 4) | (((lbo >> 4) & 0x3FFF) << 16);
+}
+
 
 // D[tmem] (+)= A[tmem] * B[smem]^T (A = P, bf16 pairs packed per 32-bit column)
 __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
@@ -413,12 +417,12 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const uint32_t tph = lin_it & 1;
         const bool lagged = nkb >= 2 * kLag + 1;
         auto issue = [&](int st, int h, int kb) {
-          const uint32_t a_addr = smem_u32(smem + st * kStage) + h * kHalfBox;
-          const uint32_t b_addr = smem_u32(smem + st * kStage) + kAStage;
+          const uint32_t a_lo = desc_lo_k(smem_u32(smem + st * kStage) + h * kHalfBox);
+          const uint32_t b_lo = desc_lo_k(smem_u32(smem + st * kStage) + kAStage);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tmem + h * 256, umma_desc_k_sw128(a_addr + kk * 32),
-                      umma_desc_k_sw128(b_addr + kk * 32), idesc_lin, (kb | kk) != 0);
+            umma_bf16(tmem + h * 256, desc_from_lo(a_lo + kk * 2), desc_from_lo(b_lo + kk * 2), idesc_lin,
+                      (kb | kk) != 0);
         };
         mbar_wait(&tempty[0], tph ^ 1);
         if (!lagged) mbar_wait(&tempty[1], tph ^ 1);
@@ -475,13 +479,12 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         tc_fence_after();
         if (lane == 0) {
           auto issue_s = [&](int t, int sl) {
-            const uint32_t qa = smem_u32(smem + kQOff + t * 2 * kHalfBox);
-            const uint32_t kb = smem_u32(smem + kKVOff + sl * kKVSlot);
+            const uint32_t qa = desc_lo_k(smem_u32(smem + kQOff + t * 2 * kHalfBox));
+            const uint32_t kb = desc_lo_k(smem_u32(smem + kKVOff + sl * kKVSlot));
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-              const uint32_t off = (kk >> 2) * kHalfBox + (kk & 3) * 32;
-              umma_bf16(tmem + t * 128, umma_desc_k_sw128(qa + off), umma_desc_k_sw128(kb + off),
-                        idesc_s, kk != 0);
+              const uint32_t off = (kk >> 2) * (kHalfBox >> 4) + (kk & 3) * 2;
+              umma_bf16(tmem + t * 128, desc_from_lo(qa + off), desc_from_lo(kb + off), idesc_s, kk != 0);
             }
             umma_commit(&s_full[t]);
           };
@@ -500,10 +503,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
             for (int t = 0; t < np; ++t) {
               mbar_wait(&p_full[t], (kv_it + j) & 1);
               tc_fence_after();
-              const uint32_t vb = smem_u32(smem + kKVOff + vs * kKVSlot);
+              const uint32_t vb = desc_lo_mn(smem_u32(smem + kKVOff + vs * kKVSlot), kHalfBox);
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk)
-                umma_bf16_ts(t_o + t * 128, tmem + t * 128 + kk * 8, desc_mn_sw128(vb + kk * 2048, kHalfBox),
+                umma_bf16_ts(t_o + t * 128, tmem + t * 128 + kk * 8, desc_from_lo(vb + kk * (2048 >> 4)),
                              idesc_pv, (j | kk) != 0);
               if (j + 1 < n) issue_s(t, ks);
               else umma_commit(&o_ready[t]);
