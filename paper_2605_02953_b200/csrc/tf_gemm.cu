@@ -33,6 +33,16 @@ namespace tf {
 
 namespace {
 
+// K-major SW128 descriptor = (low word, constant high word): one add per MMA operand
+constexpr uint32_t kDescHiK = (1024 >> 4) | (1u << (46 - 32)) | (2u << (61 - 32));
+__device__ __forceinline__ uint64_t desc_from_lo(uint32_t lo) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(kDescHiK));
+  return d;
+}
+__device__ __forceinline__ uint32_t desc_lo_k(uint32_t addr) { return ((addr & 0x3FFFF) >> 4) | (1u << 16); }
+
+
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
 #ifndef TF_GEMM_LAG
 #define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
@@ -302,12 +312,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int local = 0;
       auto issue = [&](int st, int h, int kb) {
-        const uint32_t a_addr = smem_u32(smem_a + st * S::kABytes) + h * S::kABlock;
-        const uint32_t b_addr = smem_u32(smem_b + st * S::kBBytes);
+        const uint32_t a_lo = desc_lo_k(smem_u32(smem_a + st * S::kABytes) + h * S::kABlock);
+        const uint32_t b_lo = desc_lo_k(smem_u32(smem_b + st * S::kBBytes));
 #pragma unroll
         for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-          const uint64_t ad = umma_desc_k_sw128(a_addr + kk * UMMA_K * 2);
-          const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
+          const uint64_t ad = desc_from_lo(a_lo + kk * (UMMA_K * 2 >> 4));
+          const uint64_t bd = desc_from_lo(b_lo + kk * (UMMA_K * 2 >> 4));
           if constexpr (CG == 2) umma_bf16_pair(tmem_base + h * BN, ad, bd, idesc, (kb | kk) != 0);
           else umma_bf16(tmem_base + h * BN, ad, bd, idesc, (kb | kk) != 0);
         }
@@ -390,14 +400,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a_addr = smem_u32(smem_a + stage * S::kABytes);
-            const uint32_t b_addr = smem_u32(smem_b + stage * S::kBBytes);
+            const uint32_t a_lo = desc_lo_k(smem_u32(smem_a + stage * S::kABytes));
+            const uint32_t b_lo = desc_lo_k(smem_u32(smem_b + stage * S::kBBytes));
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-              const uint64_t bd = umma_desc_k_sw128(b_addr + kk * UMMA_K * 2);
+              const uint64_t bd = desc_from_lo(b_lo + kk * (UMMA_K * 2 >> 4));
 #pragma unroll
               for (int h = 0; h < MH; ++h) {
-                const uint64_t ad = umma_desc_k_sw128(a_addr + h * S::kABlock + kk * UMMA_K * 2);
+                const uint64_t ad = desc_from_lo(a_lo + (h * S::kABlock >> 4) + kk * (UMMA_K * 2 >> 4));
                 if constexpr (CG == 2)
                   umma_bf16_pair(d_tmem + h * BN, ad, bd, idesc, (kb | kk) != 0);
                 else
