@@ -134,13 +134,33 @@ int tf_putmem_strided(tf_team* t, int to_pe, uint64_t dst_off, size_t dst_pitch,
                       size_t src_pitch, size_t row_bytes, size_t rows, void* stream);
 /* st / notify / atomic_add on a signal slot of PE pe (shmem.py:174-194). */
 int tf_signal_op(tf_team* t, int pe, uint64_t slot, uint64_t value, int op_add, void* stream);
-/* wait (shmem.py:208-235): stream waits until all n slots >= value. */
+/* wait (shmem.py:208-235): stream waits until all n slots >= value (epoch flags). */
 int tf_signal_wait(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, void* stream);
+/* wait with an explicit comparison: TF_CMP_EQ is the reference's semantics
+ * (shmem.py:223-224, every slot == value); TF_CMP_GE the epoch-flag form. */
+#define TF_CMP_GE 0
+#define TF_CMP_EQ 1
+int tf_signal_wait_cmp(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, int cmp,
+                       void* stream);
+/* atomic_add returning the old value (shmem.py:184-194); synchronous like
+ * tf_signal_cas.  tf_signal_op(op_add=1) is the stream-ordered, no-return form. */
+int tf_signal_fetch_add(tf_team* t, int pe, uint64_t slot, uint64_t value, uint64_t* old_out,
+                        void* stream);
 /* barrier_all (shmem.py:319-322), split so a single host thread can drive
  * several PEs that share one stream: arrive, then wait. */
 int tf_barrier_arrive(tf_team* t, int rank, void* stream);
 int tf_barrier_wait(tf_team* t, int rank, void* stream);
 int tf_barrier_all(tf_team* t, int rank, void* stream);
+
+/* ------------------------------------------------------------------ float32 operands
+ * The reference's float32 contract (oracles.py:12-27; tests/test_kernels.py:365-381
+ * pin unordered float paths to norm-relative 1e-5).  Splits fp32 rows [rows, k]
+ * (ld_src elements apart) into three bf16 terms and writes the 6-term K-expanded
+ * operand [rows, 6*kp] bf16 (role 0 = A order a0 a0 a1 a0 a1 a2, role 1 = B order
+ * b0 b1 b0 b2 b1 b0; columns k..kp zero), so the bf16 GEMM of the expanded
+ * operands is the fp32 product up to ~2^-24 relative terms.  Stream-ordered. */
+int tf_split_f32_bf16x3(const float* src, int64_t rows, int64_t k, int64_t ld_src, void* dst, int64_t kp,
+                        int role, void* stream);
 
 /* ------------------------------------------------------------------ GEMM tile
  * Core GEMM (the tile body of ag_gemm.py:93-94 / gemm_rs.py:123): persistent,

@@ -89,6 +89,9 @@ _SIGS = {
     "tf_putmem_strided": (ci, [vp, ci, u64, sz, vp, sz, sz, sz, vp]),
     "tf_team_broadcast": (ci, [vp, ci, u64, vp, sz, vp]),
     "tf_signal_wait": (ci, [vp, ci, u64, sz, u64, vp]),
+    "tf_signal_wait_cmp": (ci, [vp, ci, u64, sz, u64, ci, vp]),
+    "tf_split_f32_bf16x3": (ci, [vp, i64, i64, i64, vp, i64, ci, vp]),
+    "tf_signal_fetch_add": (ci, [vp, ci, u64, u64, C.POINTER(u64), vp]),
     "tf_barrier_arrive": (ci, [vp, ci, vp]),
     "tf_barrier_wait": (ci, [vp, ci, vp]),
     "tf_barrier_all": (ci, [vp, ci, vp]),

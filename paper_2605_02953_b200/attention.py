@@ -63,8 +63,8 @@ def ag_kv_scores(q_shards, k_shards, ctx: WorkloadContext, n_kv_heads: int | Non
             x = np.concatenate([x, np.zeros((sl, heads, dp - d), x.dtype)], axis=2)
         return x.reshape(sl, heads * dp)
 
-    pq = K._prepare([flat(q, hq) for q in q_shards], devices, hq * dp)
-    pk = K._prepare([flat(k, hkv) for k in k_shards], devices, hkv * dp)
+    pq = K._prepare([flat(q, hq) for q in q_shards], devices, hq * dp, split=False)
+    pk = K._prepare([flat(k, hkv) for k in k_shards], devices, hkv * dp, split=False)
     K._exact_bound_check(pq, pk, d)
     odt = K._out_dtype(ctx.out_dtype, pq)
     st = sl * world
@@ -162,9 +162,10 @@ def ag_kv_attention(q_shards, k_shards, v_shards, ctx: WorkloadContext, scale: f
     team = Team(world, devices, 2 * 2 * st * hkv * d * 2 + (1 << 20), 4 * world + 64)
     heap = SymmetricHeap(topo, team=team)
     outs = [torch.empty_like(q) for q in q_shards]
-    args = {r: _fwd_args(q_shards[r].contiguous(), k_shards[r].contiguous(), v_shards[r].contiguous(),
-                         outs[r], sl, hq, hkv, d, scale) for r in range(world)}
+    # materialise the contiguous operands first and keep them alive for the launch:
+    # the ctypes args hold raw pointers into exactly these tensors
     keep = [(q_shards[r].contiguous(), k_shards[r].contiguous(), v_shards[r].contiguous()) for r in range(world)]
+    args = {r: _fwd_args(*keep[r], outs[r], sl, hq, hkv, d, scale) for r in range(world)}
     for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
         for r in range(world):
             with torch.cuda.device(devices[r]):

@@ -318,6 +318,23 @@ __device__ __forceinline__ bool wait_geq_sys(const uint64_t* p, uint64_t want,
   return true;
 }
 
+// Equality variant (the reference's wait semantics, shmem.py:208-235: every slot == value).
+__device__ __forceinline__ bool wait_eq_sys(const uint64_t* p, uint64_t want, uint64_t timeout_ns,
+                                            unsigned long long* err, unsigned long long tag) {
+  if (ld_acquire_sys(p) == want) return true;
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t backoff = 32;
+  while (ld_acquire_sys(p) != want) {
+    __nanosleep(backoff);
+    if (backoff < 1024) backoff <<= 1;
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      if (err) atomicCAS(err, 0ull, tag);
+      return false;
+    }
+  }
+  return true;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));

@@ -46,10 +46,16 @@ __global__ void signal_op_kernel(uint64_t* p, uint64_t v, int add) {
   else st_release_sys(p, v);
 }
 
-__global__ void signal_wait_kernel(const uint64_t* p, int n, uint64_t v, uint64_t timeout_ns,
+__global__ void signal_wait_kernel(const uint64_t* p, int n, uint64_t v, int eq, uint64_t timeout_ns,
                                    unsigned long long* err) {
   const int i = threadIdx.x;
-  if (i < n) wait_geq_sys(p + i, v, timeout_ns, err, 0x2000000ull | static_cast<unsigned>(i));
+  if (i >= n) return;
+  if (eq) wait_eq_sys(p + i, v, timeout_ns, err, 0x2000000ull | static_cast<unsigned>(i));
+  else wait_geq_sys(p + i, v, timeout_ns, err, 0x2000000ull | static_cast<unsigned>(i));
+}
+
+__global__ void signal_fetch_add_kernel(uint64_t* p, uint64_t v, unsigned long long* old) {
+  *old = atom_add_release_sys(p, v);
 }
 
 struct PeerSigs {
@@ -565,16 +571,41 @@ int tf_signal_op(tf_team* t, int pe, uint64_t slot, uint64_t value, int op_add, 
   return TF_OK;
 }
 
-int tf_signal_wait(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, void* stream) {
+int tf_signal_wait_cmp(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, int cmp,
+                       void* stream) {
   if (!t || pe < 0 || pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
   if (n < 1 || n > 1024) return fail(TF_ERR_INVALID, "wait needs 1 <= num_slots <= 1024");
   if (slot + n > t->signal_slots) return fail(TF_ERR_INVALID, "slots out of range");
+  if (cmp != TF_CMP_GE && cmp != TF_CMP_EQ) return fail(TF_ERR_INVALID, "cmp must be TF_CMP_GE or TF_CMP_EQ");
   const int me = t->ipc ? t->my_rank : pe;
   tf::signal_wait_kernel<<<1, static_cast<unsigned>((n + 31) / 32 * 32), 0,
                            static_cast<cudaStream_t>(stream)>>>(t->pes[pe].sig + slot,
                                                                 static_cast<int>(n), value,
-                                                                t->timeout_ns, t->err_word(me));
+                                                                cmp == TF_CMP_EQ, t->timeout_ns,
+                                                                t->err_word(me));
   TF_CUDA_TRY(cudaGetLastError());
+  return TF_OK;
+}
+
+int tf_signal_wait(tf_team* t, int pe, uint64_t slot, size_t n, uint64_t value, void* stream) {
+  return tf_signal_wait_cmp(t, pe, slot, n, value, TF_CMP_GE, stream);
+}
+
+int tf_signal_fetch_add(tf_team* t, int pe, uint64_t slot, uint64_t value, uint64_t* old_out,
+                        void* stream) {
+  if (!t || pe < 0 || pe >= t->world) return fail(TF_ERR_INVALID, "pe out of range");
+  if (slot >= t->signal_slots) return fail(TF_ERR_INVALID, "slot out of range");
+  if (!old_out) return fail(TF_ERR_INVALID, "old_out is NULL");
+  const int me = t->ipc ? t->my_rank : pe;
+  tf::DeviceGuard guard(t->pes[me].device);
+  auto s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dold = nullptr;
+  TF_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dold), sizeof(unsigned long long), s));
+  tf::signal_fetch_add_kernel<<<1, 1, 0, s>>>(t->pes[pe].sig + slot, value, dold);
+  TF_CUDA_TRY(cudaGetLastError());
+  TF_CUDA_TRY(cudaMemcpyAsync(old_out, dold, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  TF_CUDA_TRY(cudaFreeAsync(dold, s));
+  TF_CUDA_TRY(cudaStreamSynchronize(s));  // the old value is the caller's answer
   return TF_OK;
 }
 

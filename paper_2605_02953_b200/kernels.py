@@ -41,11 +41,12 @@ def side_stream(device: int) -> torch.cuda.Stream:
 
 # ----------------------------------------------------------------- input prep
 class _Prepared:
-    def __init__(self, tensors, kind, np_dtype, k_orig):
+    def __init__(self, tensors, kind, np_dtype, k_orig, kdim):
         self.tensors = tensors
         self.kind = kind          # "torch" | "exact" | "float"
         self.np_dtype = np_dtype
         self.k = k_orig
+        self.kdim = kdim          # K of the device operands (6*kp for split float32)
 
 
 def _is_torch(x) -> bool:
@@ -80,21 +81,41 @@ def _pad_k(t: torch.Tensor, kp: int) -> torch.Tensor:
     return out
 
 
-def _prepare(shards, devices, kp: int) -> _Prepared:
+def split_f32(x: torch.Tensor, kp: int, role: int) -> torch.Tensor:
+    """fp32 [rows, k] CUDA tensor -> the 6-term bf16 operand [rows, 6*kp] (role 0 = A,
+    1 = B) whose bf16 GEMM reproduces the fp32 product (tf_prep.cu)."""
+    x = x.contiguous()
+    rows, k = x.shape
+    out = torch.empty((rows, 6 * kp), dtype=torch.bfloat16, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.call("tf_split_f32_bf16x3", x.data_ptr(), rows, k, k, out.data_ptr(), kp, role,
+                  torch.cuda.current_stream(x.device).cuda_stream)
+    return out
+
+
+def _prepare(shards, devices, kp: int, role: int = 0, split: bool = True) -> _Prepared:
+    """Device operands for one side of a GEMM.  float32 numpy inputs (the
+    reference's float contract) become the 6-term split operand (split=False:
+    rounded to bf16, for operators whose kernels index K per head); int64 "exact"
+    inputs must be bf16-exact integers and stay one term."""
     dt = check_dtype(*shards)
     k = shards[0].shape[1]
     if dt is torch.bfloat16:
-        return _Prepared([_pad_k(s, kp) for s in shards], "torch", None, k)
+        return _Prepared([_pad_k(s, kp) for s in shards], "torch", None, k, kp)
     kind = "exact" if dt == np.int64 else "float"
     out = []
     for s, dev in zip(shards, devices):
         arr = np.asarray(s)
-        if kind == "exact" and arr.size and np.abs(arr).max() > 256:
-            raise ValueError("exact mode needs integers with |x| <= 256 (exact in bf16)")
-        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(torch.bfloat16)
-        t = _pad_k(t, kp) if kp != k else t
-        out.append(t.to(f"cuda:{dev}"))
-    return _Prepared(out, kind, dt, k)
+        if kind == "exact" or not split:
+            if kind == "exact" and arr.size and np.abs(arr).max() > 256:
+                raise ValueError("exact mode needs integers with |x| <= 256 (exact in bf16)")
+            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(torch.bfloat16)
+            t = _pad_k(t, kp) if kp != k else t
+            out.append(t.to(f"cuda:{dev}"))
+        else:
+            f = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(f"cuda:{dev}")
+            out.append(split_f32(f, kp, role))
+    return _Prepared(out, kind, dt, k, 6 * kp if (kind == "float" and split) else kp)
 
 
 def _exact_bound_check(prep_a: _Prepared, prep_b: _Prepared, k: int, extra_terms: int = 1):
@@ -234,10 +255,11 @@ def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     m = m_per_rank * world
     kp = (k + 7) // 8 * 8
     devices = _devices_for(ctx, a_shards)
-    pa = _prepare(a_shards, devices, kp)
-    pb = _prepare(b_shards, devices, kp)
+    pa = _prepare(a_shards, devices, kp, 0)
+    pb = _prepare(b_shards, devices, kp, 1)
     _exact_bound_check(pa, pb, k)
     odt = _out_dtype(ctx.out_dtype, pa)
+    kp = pa.kdim
     heap_bytes = 2 * m * kp * 2 + (1 << 20)
     team = Team(world, devices, heap_bytes, 4 * world + 64)
     heap = SymmetricHeap(topo, team=team)
@@ -285,10 +307,11 @@ def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
     mpr = m // world
     kp = (k_local + 7) // 8 * 8
     devices = _devices_for(ctx, input_shards)
-    px = _prepare(input_shards, devices, kp)
-    pw = _prepare(weight_shards, devices, kp)
+    px = _prepare(input_shards, devices, kp, 0)
+    pw = _prepare(weight_shards, devices, kp, 1)
     _exact_bound_check(px, pw, k_local, extra_terms=world)
     odt = _out_dtype(ctx.out_dtype, px)
+    kp = px.kdim
     esz = 4 if odt == torch.float32 else 2
     ld = (n + 7) // 8 * 8
     heap_bytes = m * ld * esz + (1 << 20)
@@ -450,10 +473,11 @@ def gemm_allreduce(a_shards, b_shards, ctx: WorkloadContext, use_multimem_st: bo
     two_shot = ctx.use_multimem_st if use_multimem_st is None else use_multimem_st
     kp = (k + 7) // 8 * 8
     devices = _devices_for(ctx, a_shards)
-    pa = _prepare(a_shards, devices, kp)
-    pb = _prepare(b_shards, devices, kp)
+    pa = _prepare(a_shards, devices, kp, 0)
+    pb = _prepare(b_shards, devices, kp, 1)
     _exact_bound_check(pa, pb, k, extra_terms=world)
     odt = _out_dtype(ctx.out_dtype, pa)
+    kp = pa.kdim
     esz = 4 if odt == torch.float32 else 2
     ld = (n + 7) // 8 * 8
     nblocks = (m + 127) // 128

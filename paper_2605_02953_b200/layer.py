@@ -326,7 +326,7 @@ def task_cost_us(built: MK.BuiltGraph, program: MK.MegaProgram, t) -> float:
     if op == "linear":
         return 2.0 * BLOCK_M * BLOCK_N * ins[0].shape[1] / _RATE_LINEAR * 1e6
     if op == "attention":
-        i = t.tile_id // c["heads_q"]
+        i = t.tile_id // (c["heads_q"] // c.get("heads_per_task", 1))  # tile = i * (hq / np) + hp
         tps = c["seq_len"] // 128
         n_kv = (i % tps) + 1 if c["causal"] else tps
         return 4.0 * 128 * 128 * HEAD_DIM * n_kv / _RATE_ATTN * 1e6 + 2.0
@@ -503,6 +503,12 @@ class LayerRunner:
                 _lib.call("tf_barrier_all", self.team.handle, int(self.rank), s.cuda_stream)
             _lib.call("tf_layer_megakernel_run", self.team.handle, int(self.rank), C.byref(args),
                       s.cuda_stream)
+            if self.rank >= 0 and self.world > 1:
+                # two-shot allreduce tiles this rank does not own are P2P-stored into its
+                # outputs by their owners; nothing in this launch waits for them, so close
+                # the epoch with a second stream-ordered barrier: work enqueued after run()
+                # on this stream sees every peer's rows
+                _lib.call("tf_barrier_all", self.team.handle, int(self.rank), s.cuda_stream)
 
     def check(self) -> None:
         self.team.check()

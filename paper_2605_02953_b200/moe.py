@@ -131,7 +131,9 @@ class ExpertParallelMoE:
         for xx, ii in items.values():
             if xx.dtype != torch.bfloat16 or xx.shape[1] != self.H or not xx.is_contiguous():
                 raise ValueError("x must be a contiguous bf16 [T, hidden] tensor")
-        per = {r: self._fill(r, xx.contiguous(), ii.contiguous()) for r, (xx, ii) in items.items()}
+        # the ctypes args hold raw pointers: keep the exact tensors they point into alive
+        items = {r: (xx, ii.contiguous()) for r, (xx, ii) in items.items()}
+        per = {r: self._fill(r, xx, ii) for r, (xx, ii) in items.items()}
         self._keep = items
         self._drive("tf_moe_dispatch", per)
         if isinstance(topk_idx, torch.Tensor):
@@ -173,7 +175,8 @@ class ExpertParallelMoE:
                 oo = torch.empty((ii.shape[0], self.H), dtype=torch.bfloat16,
                                  device=f"cuda:{t.devices[r]}")
             outs[r] = oo
-            per[r] = self._fill(r, None, ii.contiguous(), ww.contiguous().float(), oo)
+            items[r] = (ii.contiguous(), ww.contiguous().float(), oo)
+            per[r] = self._fill(r, None, *items[r])
         self._keep2 = (items, outs)
         self._drive("tf_moe_combine", per)
         return outs[next(iter(outs))] if single else [outs[r] for r in range(t.world)]
@@ -215,8 +218,9 @@ def ag_moe_group_gemm(token_shards, expert_weights, routing, ctx: WorkloadContex
                 raise ValueError("ragged expert weights")
     kp = (k + 7) // 8 * 8
     devices = K._devices_for(ctx, token_shards)
-    pt = K._prepare(token_shards, devices, kp)
-    pw = [K._prepare(list(expert_weights[r]), [devices[r]] * n_experts, kp) for r in range(world)]
+    pt = K._prepare(token_shards, devices, kp, 0)
+    pw = [K._prepare(list(expert_weights[r]), [devices[r]] * n_experts, kp, 1) for r in range(world)]
+    kp = pt.kdim
     if pt.kind == "exact":
         for p in pw:
             K._exact_bound_check(pt, p, k)

@@ -290,12 +290,19 @@ class SymmetricHeap:
         self.st(sig, idx, value, pe, scope="sys", semantic=semantic, name="notify", stream=stream)
 
     def atomic_add(self, sig: SigHandle, idx: int, val: int, pe: int, semantic: str = "release",
-                   scope: str = "gpu", stream=None) -> None:
-        """Stream-ordered release add.  Unlike the reference it does not return
-        the old value (a host round trip would serialise the device)."""
+                   scope: str = "gpu", stream=None, fetch: bool = True):
+        """Release add on a signal slot (shmem.py:184-194).  With fetch=True (the
+        reference's contract) it returns the old value, which drains the stream;
+        fetch=False is the stream-ordered form and returns None."""
         _check_scope_semantic(scope, semantic)
         slot = self._slot(sig, idx, 1, pe)
-        _lib.call("tf_signal_op", self.team.handle, int(pe), slot, int(val), 1, _stream_ptr(stream))
+        if not fetch:
+            _lib.call("tf_signal_op", self.team.handle, int(pe), slot, int(val), 1, _stream_ptr(stream))
+            return None
+        old = C.c_uint64()
+        _lib.call("tf_signal_fetch_add", self.team.handle, int(pe), slot, int(val) & (2 ** 64 - 1),
+                  C.byref(old), _stream_ptr(stream))
+        return int(old.value)
 
     def atomic_cas(self, sig: SigHandle, idx: int, cmp: int, val: int, pe: int,
                    semantic: str = "release", scope: str = "gpu", stream=None) -> int:
@@ -309,14 +316,19 @@ class SymmetricHeap:
         return int(old.value)
 
     def wait(self, sig: SigHandle, idx: int, num_slots: int, pe: int, scope: str = "gpu",
-             semantic: str = "acquire", value: int = 1, note=None, stream=None) -> Token:
-        """Stream waits until every slot in [idx, idx+num_slots) >= value."""
+             semantic: str = "acquire", value: int = 1, note=None, stream=None,
+             cmp: str = "eq") -> Token:
+        """Stream waits until every slot in [idx, idx+num_slots) == value (the
+        reference's semantics, shmem.py:208-235); cmp="ge" waits for >= value
+        (epoch-valued flags that only grow)."""
         _check_scope_semantic(scope, semantic)
         if num_slots < 1:
             raise ValueError("wait needs num_slots >= 1")
+        if cmp not in ("eq", "ge"):
+            raise ValueError(f"cmp must be 'eq' or 'ge', got {cmp!r}")
         slot = self._slot(sig, idx, num_slots, pe)
-        _lib.call("tf_signal_wait", self.team.handle, int(pe), slot, int(num_slots), int(value),
-                  _stream_ptr(stream))
+        _lib.call("tf_signal_wait_cmp", self.team.handle, int(pe), slot, int(num_slots), int(value),
+                  1 if cmp == "eq" else 0, _stream_ptr(stream))
         return Token(pe=int(pe), slot=slot, num_slots=int(num_slots))
 
     def reset_signals(self, sig: SigHandle, pe: int, stream=None) -> None:
@@ -442,11 +454,6 @@ class SymmetricHeap:
             dst = self.view(handle, r, b.dtype, shape)
             dst[row0:r1, col0:c1].copy_(b.to(dst.device))
 
-    def sync_all(self, rank: int | None = None, stream=None):
-        """Rendezvous (shmem.py:324-327).  Puts are stream-ordered, so the device
-        barrier is the same as barrier_all's."""
-        return self.barrier_all(rank, stream)
-
     def node_barrier(self, rank: int | None = None, barrier=None, stream=None):
         """Rendezvous of the node team (shmem.py:329-331): every PE on one box."""
         return self.barrier_all(rank, stream)
@@ -463,6 +470,8 @@ class SymmetricHeap:
             with torch.cuda.device(self.team.devices[r]):
                 _lib.call("tf_barrier_wait", self.team.handle, r, _stream_ptr(stream))
 
+    # sync_all (shmem.py:324-327) is rendezvous-only in the reference; here every put
+    # is stream-ordered before the arrival, so the rendezvous also drains them.
     sync_all = barrier_all
 
 

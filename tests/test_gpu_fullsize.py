@@ -19,6 +19,8 @@ import numpy as np
 import pytest
 import torch
 
+from tests._devices import devices_for
+
 pytestmark = pytest.mark.gpu
 TOKENS, HIDDEN, FFN = 8192, 8192, 28672
 
@@ -37,7 +39,7 @@ def _rel(got, want):
 def _ctx(world, **kw):
     from paper_2605_02953_b200 import WorkloadContext, build_topology
     args = dict(block_m=512, block_n=256, group_m=8, num_gemm_sms=0, num_comm_sms=0,
-                devices=[0] * world)
+                devices=devices_for(world))
     args.update(kw)
     return WorkloadContext(topology=build_topology(world, 1), **args)
 
@@ -92,7 +94,7 @@ def test_config4_moe_ep8_conservation():
     world, e, k, t, h = 8, 256, 8, 4096, 7168
     g = torch.Generator(device="cuda").manual_seed(4)
     max_recv = 2 * t * k  # per rank; uniform routing needs ~t*k
-    team = Team(world, [0] * world, heap_bytes=2 * max_recv * h * 2 + (64 << 20), signal_slots=1024)
+    team = Team(world, devices_for(world), heap_bytes=2 * max_recv * h * 2 + (64 << 20), signal_slots=1024)
     ep = M.ExpertParallelMoE(team, e, h, k, max_tokens=t, max_recv=max_recv)
     xs = [torch.randn(t, h, device="cuda", generator=g).to(torch.bfloat16) for _ in range(world)]
     routed = [M.moe_route(torch.randn(t, e, device="cuda", generator=g), k) for _ in range(world)]

@@ -13,6 +13,8 @@ import numpy as np
 import pytest
 import torch
 
+from tests._devices import devices_for
+
 from oracle import collectives as O
 from tests import _golden as G
 
@@ -35,7 +37,7 @@ def _k():
 def _ctx(world, **kw):
     from paper_2605_02953_b200 import WorkloadContext, build_topology
     args = dict(block_m=128, block_n=256, block_k=64, group_m=4, num_gemm_sms=0,
-                num_comm_sms=0, devices=[0] * world)
+                num_comm_sms=0, devices=devices_for(world))
     args.update(kw)
     return WorkloadContext(topology=build_topology(world, 1), **args)
 
@@ -238,6 +240,53 @@ def test_gemm_ar_validation():
     b = [rng.integers(-8, 8, (6, 4)) for _ in range(2)]
     with pytest.raises(ValueError):
         K.gemm_allreduce(a, b, _ctx(2, block_n=4))  # N=6 not divisible by block_n=4
-    multi = WorkloadContext(topology=build_topology(4, 2), devices=[0] * 4)
+    multi = WorkloadContext(topology=build_topology(4, 2), devices=devices_for(4))
     with pytest.raises(ValueError):
         K.gemm_allreduce([rng.integers(-8, 8, (4, 4))] * 4, [rng.integers(-8, 8, (4, 4))] * 4, multi)
+
+
+def _norm_rel_err(got, want):
+    # the reference's metric (tests/test_kernels.py:43-46): max-abs error / max-abs value
+    diff = np.abs(np.asarray(got, np.float64) - np.asarray(want, np.float64)).max(initial=0.0)
+    scale = np.abs(np.asarray(want, np.float64)).max(initial=0.0) or 1.0
+    return float(diff / scale)
+
+
+def test_float_fractional_tolerance_unordered():
+    """Reference tests/test_kernels.py:365-381: fractional float32 gemm_rs (ring
+    order) and gemm_allreduce (one- and two-shot) within norm-relative 1e-5 of the
+    fp32 oracle -- the float32 contract, met with the 6-term bf16 split (tf_prep.cu)."""
+    K = _k()
+    rng = np.random.default_rng(18)
+    world = 4
+    frac = lambda shape: rng.standard_normal(shape).astype(np.float32)
+    inp = [frac((world * 8, 16)) for _ in range(world)]
+    w = [frac((12, 16)) for _ in range(world)]
+    ref = O.ref_reduce_scatter(inp, w)
+    run = K.gemm_rs(inp, w, _ctx(world, reduce_order="ring"))
+    for got, want in zip(run.outputs, ref):
+        assert got.dtype == np.float32
+        assert _norm_rel_err(got, want) <= 1e-5
+    a = [frac((8, 16)) for _ in range(world)]
+    b = [frac((8, 16)) for _ in range(world)]
+    want = O.ref_allreduce(a, b)
+    for ts in (False, True):
+        run = K.gemm_allreduce(a, b, _ctx(world, block_m=4, block_n=4, block_k=4), use_multimem_st=ts)
+        for got in run.outputs:
+            assert _norm_rel_err(got, want) <= 1e-5
+
+
+@pytest.mark.parametrize("world,mpr,n,k", [(2, 256, 384, 512), (4, 100, 136, 1000)])
+def test_float32_ag_gemm_fp32_accuracy(world, mpr, n, k):
+    """float32 AG-GEMM at non-trivial K: norm-relative error vs the float64 product
+    is at float32 level (<= 1e-6), far below the bf16 rounding (~3e-3)."""
+    K = _k()
+    rng = np.random.default_rng(world * 31 + k)
+    a = [rng.standard_normal((mpr, k)).astype(np.float32) for _ in range(world)]
+    b = [rng.standard_normal((n, k)).astype(np.float32) for _ in range(world)]
+    run = K.ag_gemm(a, b, _ctx(world))
+    full = np.concatenate(a).astype(np.float64)
+    for r in range(world):
+        want = full @ b[r].astype(np.float64).T
+        assert run.outputs[r].dtype == np.float32
+        assert _norm_rel_err(run.outputs[r], want) <= 1e-6

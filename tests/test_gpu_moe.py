@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 import torch
 
+from tests._devices import devices_for
+
 from oracle import collectives as OC
 from oracle import moe as OM
 from tests import _golden as G
@@ -58,7 +60,7 @@ def test_counts_and_send_order_bit_exact(t, e, k):
 
 def _team(world):
     from paper_2605_02953_b200.shmem import Team
-    return Team(world, [0] * world, heap_bytes=1 << 30, signal_slots=1024)
+    return Team(world, devices_for(world), heap_bytes=1 << 30, signal_slots=1024)
 
 
 @pytest.mark.parametrize("world,e,k,t,h", [(1, 8, 2, 16, 64), (2, 8, 2, 37, 64), (4, 16, 4, 50, 128),
@@ -133,7 +135,7 @@ def test_ag_moe_group_gemm_exact_vs_reference_fixture(case):
     edges = np.concatenate([[0], np.cumsum(routing.sum(axis=1))])
     toks = [c["moe_tok"][edges[r]:edges[r + 1]] for r in range(w)]
     ctx = WorkloadContext(topology=build_topology(w, 1), block_m=2, num_gemm_sms=0,
-                          num_comm_sms=0, devices=[0] * w)
+                          num_comm_sms=0, devices=devices_for(w))
     run = M.ag_moe_group_gemm(toks, [list(x) for x in c["moe_w"]], routing, ctx)
     for r in range(w):
         assert np.array_equal(run.outputs[r], c["moe_y"][r]), (case, r)

@@ -7,6 +7,8 @@ import numpy as np
 import pytest
 import torch
 
+from tests._devices import devices_for
+
 pytestmark = pytest.mark.gpu
 
 
@@ -20,7 +22,7 @@ def _heap(world=4, data=1 << 20, slots=256):
     from paper_2605_02953_b200 import build_topology
     from paper_2605_02953_b200.shmem import SymmetricHeap
     return SymmetricHeap(build_topology(world, 1), data_bytes=data, signal_slots=slots,
-                         devices=[0] * world)
+                         devices=devices_for(world))
 
 
 def test_alloc_symmetric_aligned_and_disjoint():
@@ -115,7 +117,7 @@ def test_multimem_reduce_and_broadcast(world):
     from paper_2605_02953_b200 import build_topology
     from paper_2605_02953_b200.shmem import SymmetricHeap
     heap = SymmetricHeap(build_topology(world, 1), data_bytes=1 << 22, signal_slots=64,
-                         devices=[0] * world)
+                         devices=devices_for(world))
     rng = np.random.default_rng(world)
     h = heap.alloc(4096 * 8)
     # int64: exact ascending sum
@@ -166,7 +168,7 @@ def test_atomic_cas_and_putmem_strided():
     from paper_2605_02953_b200.shmem import SymmetricHeap
     world = 2
     heap = SymmetricHeap(build_topology(world, 1), data_bytes=1 << 20, signal_slots=64,
-                         devices=[0] * world)
+                         devices=devices_for(world))
     sig = heap.alloc_signals(4)
     assert heap.atomic_cas(sig, 1, 0, 7, pe=1) == 0       # swaps
     assert heap.atomic_cas(sig, 1, 0, 9, pe=1) == 7       # mismatch: unchanged
@@ -184,3 +186,22 @@ def test_atomic_cas_and_putmem_strided():
     heap.node_barrier(1)
     torch.cuda.synchronize()
     heap.team.close()
+
+
+def test_wait_equality_and_fetch_add_old_value():
+    """Reference semantics: wait() is all-of '== value' (shmem.py:223-224) and
+    atomic_add returns the old value (shmem.py:184-194)."""
+    h = _heap()
+    sig = h.alloc_signals(2)
+    assert h.atomic_add(sig, 0, 3, pe=1) == 0
+    assert h.atomic_add(sig, 0, 4, pe=1) == 3
+    assert h.atomic_add(sig, 0, 1, pe=1, fetch=False) is None
+    torch.cuda.synchronize()
+    assert h.sig_view(sig, 1).tolist() == [8, 0]
+    h.wait(sig, 0, 1, pe=1, value=8)          # == passes
+    h.wait(sig, 0, 1, pe=1, value=5, cmp="ge")  # >= passes
+    h.wait(sig, 1, 1, pe=1, value=0)          # == 0 passes on a fresh slot
+    torch.cuda.synchronize()
+    h.team.check()
+    with pytest.raises(ValueError):
+        h.wait(sig, 0, 1, pe=1, value=8, cmp="gt")

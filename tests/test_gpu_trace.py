@@ -7,6 +7,8 @@ import numpy as np
 import pytest
 import torch
 
+from tests._devices import devices_for
+
 pytestmark = pytest.mark.gpu
 
 
@@ -19,7 +21,7 @@ def _need_gpu():
 def _ctx(world, **kw):
     from paper_2605_02953_b200 import WorkloadContext, build_topology
     args = dict(block_m=128, block_n=128, group_m=2, num_gemm_sms=0, num_comm_sms=0,
-                devices=[0] * world)
+                devices=devices_for(world))
     args.update(kw)
     return WorkloadContext(topology=build_topology(world, 1), **args)
 
