@@ -32,6 +32,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AG-GEMM/GEMM-RS TFLOPS at 1/2/4/8 B200 vs roofline; MoE a2a GB/s"
 TOKENS, HIDDEN, FFN = 8192, 8192, 28672
+# NVLink roofline: north_star's "link bandwidth" = NVLink 5 nominal 900 GB/s per direction;
+# the measured peer copy (B200_PROFILING.md) is reported beside it
+NVLINK_GBS, NVLINK_MEASURED_GBS = 900.0, 770.0
 
 
 def parse():
@@ -138,13 +141,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-# ------------------------------------------------------------------ CPU baseline (oracle)
-def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512, min_seconds: float = 0.0):
-    """Oracle (numpy) MLP step on a bounded sample: `rows` tokens instead of 8192,
-    fp32, all host threads.  Returns (TFLOP/s, seconds, cores, sample text)."""
+# ------------------------------------------------------------------ CPU baseline / reference arm
+CPU_ROWS = 1024  # the bounded sample both CPU legs use: 1024 of the 8192 tokens
+
+
+def _ref_package():
+    """The unmodified reference (overlapsim) installed in baseline/_ref, or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "overlapsim")) and path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import overlapsim  # noqa: F401
+        return path
+    except ImportError:
+        return None
+
+
+def cpu_sample(tp: int, rows: int = CPU_ROWS, steps: int = 1, min_seconds: float = 0.0):
+    """One config-2 MLP step of the reference's CPU path on a bounded sample
+    (`rows` tokens, TP=tp ranks simulated, hidden 8192, ffn 28672, fp32, all host
+    threads).  With baseline/_ref installed this is the reference's own public
+    operators -- overlapsim ag_gemm + gemm_rs (ovs/kernels/ag_gemm.py:20,
+    gemm_rs.py:31) with block 128x256x64 and num_gemm_sms=144 --
+    kind "reference"; otherwise the numpy oracle port, kind "port".  Returns a dict
+    with TFLOP/s, seconds per step, cores, kind, sample text and the reference
+    oracle (ref_allgather_gemm + ref_reduce_scatter) on the same sample."""
     import numpy as np
 
-    from oracle import collectives as O
     cores = len(os.sched_getaffinity(0))
     rng = np.random.default_rng(0)
     f_tp = FFN // tp
@@ -153,45 +176,89 @@ def cpu_sample_tflops(tp: int, steps: int = 1, rows: int = 512, min_seconds: flo
     w1 = [rng.standard_normal((f_tp, HIDDEN), dtype=np.float32) for _ in range(tp)]
     w2 = [rng.standard_normal((HIDDEN, f_tp), dtype=np.float32) for _ in range(tp)]
     flops = 2 * 2 * (mpr * tp) * HIDDEN * FFN
-    O.ref_allgather_gemm(x, w1[:1])  # warm
+    if _ref_package():
+        from overlapsim import build_topology
+        from overlapsim.kernels.ag_gemm import ag_gemm
+        from overlapsim.kernels.context import WorkloadContext
+        from overlapsim.kernels.gemm_rs import gemm_rs
+        from overlapsim.kernels.oracles import ref_allgather_gemm, ref_reduce_scatter
+        topo = build_topology(tp, 1, num_sms=148)
+        kw = dict(topology=topo, block_m=128, block_n=256, block_k=64, num_gemm_sms=144, num_comm_sms=4)
+        ctx_ag, ctx_rs = WorkloadContext(**kw), WorkloadContext(fuse_scatter=True, **kw)
+
+        def step():
+            h = ag_gemm(x, w1, ctx_ag).outputs
+            gemm_rs(h, w2, ctx_rs)
+        kind = "reference"
+        what = ("reference overlapsim ag_gemm + gemm_rs (baseline/_ref, unmodified; block 128x256x64, "
+                "num_gemm_sms=144, fuse_scatter)")
+    else:
+        from oracle import collectives as O
+        ref_allgather_gemm, ref_reduce_scatter = O.ref_allgather_gemm, O.ref_reduce_scatter
+
+        def step():
+            ref_reduce_scatter(ref_allgather_gemm(x, w1), w2)
+        kind = "port"
+        what = "oracle port of ref_allgather_gemm + ref_reduce_scatter (baseline/_ref not installed)"
     t0 = time.perf_counter()
     done = 0
     while done < steps or time.perf_counter() - t0 < min_seconds:
-        h = O.ref_allgather_gemm(x, w1)
-        O.ref_reduce_scatter(h, w2)
+        step()
         done += 1
     dt = (time.perf_counter() - t0) / done
-    sample = (f"oracle ref_allgather_gemm + ref_reduce_scatter (numpy fp32, OpenBLAS) on "
-              f"{mpr * tp} of {TOKENS} tokens, TP={tp}, hidden {HIDDEN}, ffn {FFN}")
-    return flops / dt / 1e12, dt, cores, sample
+    t1 = time.perf_counter()
+    ref_reduce_scatter(ref_allgather_gemm(x, w1), w2)
+    dt_oracle = time.perf_counter() - t1
+    sample = (f"{what}, numpy fp32 (OpenBLAS, {cores} threads) on {mpr * tp} of {TOKENS} tokens, "
+              f"TP={tp} simulated ranks, hidden {HIDDEN}, ffn {FFN}")
+    return {"value": flops / dt / 1e12, "seconds_per_step": dt, "cores": cores, "kind": kind,
+            "sample": sample, "oracle_tflops": flops / dt_oracle / 1e12, "steps": done}
+
+
+def cpu_sample_1thread(tp: int, rows: int = CPU_ROWS):
+    """The same step with one host thread (OPENBLAS_NUM_THREADS=1 must be set
+    before numpy loads, hence a subprocess)."""
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1")
+    code = (f"import json,sys; sys.path.insert(0, {ROOT!r}); import bench; "
+            f"print(json.dumps(bench.cpu_sample({tp}, {rows})))")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                             timeout=600)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"value": round(d["value"], 6), "seconds_per_step": round(d["seconds_per_step"], 3),
+                "oracle_tflops": round(d["oracle_tflops"], 6), "cores": 1}
+    except Exception as exc:  # noqa: BLE001
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (the oracle port of
-    ovs/kernels/oracles.py, since the reference is pure Python) on host cores."""
+    """--impl reference: the reference's own CPU path (baseline/_ref overlapsim
+    ag_gemm + gemm_rs, else the oracle port) on the host cores, each step the
+    bounded 1024-token sample of config 2 at TP = --gpus (the same sample as the
+    GPU arm's cpu_baseline).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
     tp = args.gpus
-    vals = []
-    cores = None
-    sample = ""
+    runs = []
     for i in range(args.warmup + args.steps):
-        v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=256)
+        d = cpu_sample(tp)
         if i >= args.warmup:
-            vals.append((v, dt))
-    value = statistics.median(v for v, _ in vals)
-    ms = statistics.median(dt for _, dt in vals) * 1e3
+            runs.append(d)
+    value = statistics.median(d["value"] for d in runs)
+    ms = statistics.median(d["seconds_per_step"] for d in runs) * 1e3
+    last = runs[-1]
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"llama3-70b MLP AG-GEMM+GEMM-RS, TP={tp}, sampled on 256 tokens",
-                   "tokens": TOKENS, "hidden": HIDDEN, "ffn": FFN, "tp": tp},
-        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores,
-                         "kind": "port", "sample": sample},
+        "config": {"workload": f"llama3-70b MLP AG-GEMM+GEMM-RS, TP={tp}, sampled on {CPU_ROWS} tokens",
+                   "tokens": TOKENS, "hidden": HIDDEN, "ffn": FFN, "tp": tp, "sample_tokens": CPU_ROWS},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": last["cores"],
+                         "kind": last["kind"], "sample": last["sample"],
+                         "oracle_tflops": round(statistics.median(d["oracle_tflops"] for d in runs), 6)},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -271,9 +338,10 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
                            "bytes_per_phase": hbm}
     else:
         ach = remote / (max(d_ms, c_ms) * 1e-3) / 1e9
-        out["roofline"] = {"bound": "nvlink", "achieved": round(ach, 1), "peak": 770.0,
-                           "unit": "GB/s per rank per direction (measured peer copy, B200_PROFILING.md)",
-                           "frac": round(ach / 770.0, 4)}
+        out["roofline"] = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_GBS,
+                           "unit": "GB/s per rank per direction (NVLink 5 link bandwidth)",
+                           "frac": round(ach / NVLINK_GBS, 4),
+                           "frac_vs_measured_p2p": round(ach / NVLINK_MEASURED_GBS, 4)}
     return out
 
 
@@ -667,8 +735,8 @@ def bench_attention_dist(dev, world, rank, steps, flush, peaks, shared_gpus):
            "ms_per_rank": round(ms, 4), "tflops_per_rank": round(flops / (ms * 1e-3) / 1e12, 2),
            "tflops_total": round(world * flops / (ms * 1e-3) / 1e12, 2),
            "roofline": {"bound": "tensor", "t_roof_ms": round(max(flops / (peaks.get("bf16_tflops", 1622.7) * 1e12),
-                                                                   nv / 770e9) * 1e3, 4),
-                        "frac": round(max(flops / (peaks.get("bf16_tflops", 1622.7) * 1e12), nv / 770e9)
+                                                                   nv / (NVLINK_GBS * 1e9)) * 1e3, 4),
+                        "frac": round(max(flops / (peaks.get("bf16_tflops", 1622.7) * 1e12), nv / (NVLINK_GBS * 1e9))
                                       / (ms * 1e-3), 4)}}
     if do_cmp:
         res["comparator"] = {"impl": "NCCL all_gather(K), all_gather(V) + torch SDPA", "ms": round(cms, 4),
@@ -917,27 +985,42 @@ def main_ours(args):
                        "previous/next step's GEMMs (double-buffered)"}
 
     # ---- roofline of the dominant kernel (the tcgen05 GEMM; one launch per op at N=1)
+    # achieved = algorithmic FLOPs per launch / the MEAN event-timed duration of the two
+    # fused ops (each is one launch of the GEMM kernel at N=1; at N>1 the op's time
+    # includes its exchange); per-op rooflines use the north_star definition
+    # t_roof = max(FLOPs / tensor peak, NVLink bytes / 900 GB/s link bandwidth)
     peak = peaks.get("bf16_tflops", 1622.7)
     peak_sus = peaks.get("bf16_tflops_sustained", peak)
-    gemm_ms = min(ag_avg, rs_avg) if world == 1 else ag_avg
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12
     nv_bytes = (world - 1) / world * m * HIDDEN * 2 if world > 1 else 0
+    mean_ms = 0.5 * (ag_avg + rs_avg)
+    achieved = gemm_flops / (mean_ms * 1e-3) / 1e12
+
+    def op_roof(ms):
+        t_tc, t_nv = gemm_flops / (peak * 1e12), nv_bytes / NVLINK_GBS / 1e9
+        t_nv_meas = nv_bytes / NVLINK_MEASURED_GBS / 1e9
+        return {"ms": round(ms, 4), "tflops": round(gemm_flops / (ms * 1e-3) / 1e12, 2),
+                "t_roof_ms": round(max(t_tc, t_nv) * 1e3, 4), "frac": round(max(t_tc, t_nv) / (ms * 1e-3), 4),
+                "frac_vs_measured_p2p": round(max(t_tc, t_nv_meas) / (ms * 1e-3), 4),
+                "nvlink_bytes": nv_bytes}
     roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "frac_of_sustained": round(achieved / peak_sus, 4),
             "peak_kind": f"{peaks_kind} burst bf16 (MEASURED_PEAKS.json bf16_tflops)",
+            "achieved_def": "2*M*N*K per launch / mean(ag_gemm ms, gemm_rs ms)",
             "traffic": _committed_traffic(), "kernel": "gemm_sm100_kernel<CG=2,MH=2,BN=256,bf16> (512x256 tile per CTA pair)",
-            "group_m": args.group_m,
-            "flops_per_launch": gemm_flops, "nvlink_bytes_per_ag": nv_bytes,
-            "per_op_ms": {"ag_gemm": round(ag_avg, 4), "gemm_rs": round(rs_avg, 4)}}
+            "group_m": args.group_m, "flops_per_launch": gemm_flops,
+            "nvlink_gbs": {"link": NVLINK_GBS, "measured_p2p": NVLINK_MEASURED_GBS},
+            "per_op": {"ag_gemm": op_roof(ag_avg), "gemm_rs": op_roof(rs_avg)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
-        # the bounded sample repeated for >= 10 s of timed CPU work (mean step)
-        v, dt, cores, sample = cpu_sample_tflops(tp, steps=1, rows=1024, min_seconds=10.0)
-        cpu = {"value": round(v, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-               "sample": sample + "; repeated for >= 10 s of timed CPU work",
-               "seconds_per_step": round(dt, 3)}
+        # the same bounded sample as the reference arm, repeated for >= 10 s of timed CPU work
+        d = cpu_sample(tp, min_seconds=10.0)
+        cpu = {"value": round(d["value"], 6), "unit": "TFLOP/s", "cores": d["cores"], "kind": d["kind"],
+               "sample": d["sample"] + f"; {d['steps']} steps, >= 10 s of timed CPU work",
+               "seconds_per_step": round(d["seconds_per_step"], 3),
+               "oracle_tflops": round(d["oracle_tflops"], 6),
+               "one_thread": cpu_sample_1thread(tp)}
 
     moe = None
     if not args.no_moe:

@@ -114,3 +114,37 @@ def combine(expert_out_shards, topk_idx_shards, topk_w_shards, n_experts: int):
                 acc[tok] += w[tok, j] * y
         outs.append(acc)
     return outs
+
+
+def dispatch_layout_fast(topk_idx_shards, n_experts: int, world: int):
+    """Vectorised dispatch_layout (same results, numpy lexsort instead of Python
+    loops) for the full-size config-4 parity test: returns
+    (counts [world, E], recv_src [world] of int64 arrays, recv_tok [world],
+    slot_row [world] of [T, k] int64).  Receive order = expert, then source rank,
+    then the source's (token, slot) order -- gather_tokens_by_expert
+    (ovs/kernels/oracles.py:38-50) restricted to each owner's experts."""
+    if n_experts % world:
+        raise ValueError("n_experts must divide across ranks")
+    epr = n_experts // world
+    counts = routing_counts(topk_idx_shards, n_experts)
+    es, ss, ts, ls = [], [], [], []
+    for s, idx in enumerate(topk_idx_shards):
+        idx = np.asarray(idx)
+        t, k = idx.shape
+        es.append(idx.reshape(-1).astype(np.int64))
+        ss.append(np.full(t * k, s, np.int64))
+        ts.append(np.repeat(np.arange(t, dtype=np.int64), k))
+        ls.append(np.tile(np.arange(k, dtype=np.int64), t))
+    e, s, tok, sl = (np.concatenate(v) if v else np.zeros(0, np.int64) for v in (es, ss, ts, ls))
+    order = np.lexsort((sl, tok, s, e))
+    e, s, tok, sl = e[order], s[order], tok[order], sl[order]
+    owner = e // epr
+    bounds = np.searchsorted(owner, np.arange(world + 1), side="left")
+    pos = np.arange(e.size, dtype=np.int64) - bounds[owner]
+    slot_row = [np.full(np.asarray(i).shape, -1, dtype=np.int64) for i in topk_idx_shards]
+    for src in range(len(topk_idx_shards)):
+        m = s == src
+        slot_row[src][tok[m], sl[m]] = pos[m]
+    recv_src = [s[bounds[d]:bounds[d + 1]] for d in range(world)]
+    recv_tok = [tok[bounds[d]:bounds[d + 1]] for d in range(world)]
+    return counts, recv_src, recv_tok, slot_row

@@ -123,3 +123,18 @@ def test_topk_rule_ties_to_lower_expert():
     idx, w = M.topk_route(lg, 2)
     assert idx.tolist() == [[1, 2]]
     assert np.allclose(w, [[0.5, 0.5]])
+
+
+def test_dispatch_layout_fast_equals_loop_oracle():
+    """The vectorised layout used at full config-4 size equals the loop oracle."""
+    rng = np.random.default_rng(7)
+    for world, e, k, t in [(1, 8, 2, 5), (2, 8, 2, 37), (4, 16, 4, 50), (8, 64, 8, 96), (8, 256, 8, 64)]:
+        idx = [np.stack([rng.choice(e, size=k, replace=False) for _ in range(t)]).astype(np.int32)
+               for _ in range(world)]
+        counts, recv, slot_row = M.dispatch_layout(idx, e, world)
+        c2, rsrc, rtok, sr2 = M.dispatch_layout_fast(idx, e, world)
+        assert np.array_equal(counts, c2)
+        for d in range(world):
+            assert [(s, t_) for s, t_, _ in recv[d]] == list(zip(rsrc[d].tolist(), rtok[d].tolist()))
+        for s in range(world):
+            assert np.array_equal(slot_row[s], sr2[s])
