@@ -313,6 +313,33 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
  * out[t] = sum_j w[t,j] * y[row(t,j)] in fp32 (slot order), bf16 out. */
 int tf_moe_combine(tf_team* t, int rank, const tf_moe_args* a, int phase, void* stream);
 
+/* AllGather + grouped GEMM for expert-routed tokens (ag_moe_group_gemm,
+ * ovs/kernels/ag_moe.py:20-142).  Per rank: tokens = this rank's rows [rows_r, k]
+ * bf16 grouped by expert (rows_r = sum(routing[rank])), weights = this rank's
+ * stacked expert shards [n_experts, n, k] bf16, out = [total_rows, n]
+ * expert-major (row expert_base[e] + source-major offset).  routing is a HOST
+ * [world, n_experts] int64 count matrix, identical on every rank.
+ *   PRE  = tile schedule (swizzle_ag_moe order, swizzle.py:225-286, or plain tile
+ *          order when swizzle = 0) and piece tables to the device; local rows ->
+ *          own workspace at their expert-major rows; own arrival counter :=
+ *          target; barrier arrive                        (ag_moe.py:104-108)
+ *   MAIN = barrier wait, then ONE launch: num_comm_sms pull-engine CTAs copy the
+ *          peers' pieces in (rank+i)%w order and release a per-source arrival
+ *          counter (ag_moe.py:109-117); the grouped tcgen05 GEMM CTAs walk the
+ *          schedule and acquire-wait sources [segment_start, segment_end] of
+ *          each tile before its TMA loads (ag_moe.py:120-142).
+ * max_rows bounds total_rows (workspace sizing; 0 = this call's total).
+ * block_m 128 (one CTA) or 256 (CTA pair); n % 8 == 0, k % 8 == 0. */
+typedef struct tf_agmoe_args {
+  const void* tokens;
+  const void* weights;
+  void* out;
+  const int64_t* routing;
+  int64_t n_experts, n, k, max_rows, lda, ldo;
+  int32_t out_dtype, block_m, block_n, num_gemm_sms, num_comm_sms, swizzle;
+} tf_agmoe_args;
+int tf_ag_moe_group_gemm(tf_team* t, int rank, const tf_agmoe_args* a, int phase, void* stream);
+
 /* ------------------------------------------------------------------ task-level megakernel
  * Executor for the reference's task graphs (ovs/megakernel/):
  * queues = int32 [slots][num_sms][30] task records (encoding.py:20-166),

@@ -60,6 +60,15 @@ class AttnFwdArgs(C.Structure):
     ]
 
 
+class AgMoeArgs(C.Structure):
+    _fields_ = [
+        ("tokens", vp), ("weights", vp), ("out", vp), ("routing", vp),
+        ("n_experts", i64), ("n", i64), ("k", i64), ("max_rows", i64), ("lda", i64), ("ldo", i64),
+        ("out_dtype", i32), ("block_m", i32), ("block_n", i32), ("num_gemm_sms", i32),
+        ("num_comm_sms", i32), ("swizzle", i32),
+    ]
+
+
 _SIGS = {
     "tf_last_error": (C.c_char_p, []),
     "tf_version": (C.c_char_p, []),
@@ -112,6 +121,7 @@ _SIGS = {
     "tf_moe_buffers": (ci, [vp, ci, C.POINTER(MoeArgs), C.POINTER(vp), C.POINTER(vp)]),
     "tf_moe_dispatch": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
     "tf_moe_combine": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
+    "tf_ag_moe_group_gemm": (ci, [vp, ci, C.POINTER(AgMoeArgs), ci, vp]),
 }
 
 _lib = None

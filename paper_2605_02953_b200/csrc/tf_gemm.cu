@@ -84,6 +84,25 @@ struct KParams {
   int trace_cap;
   int trace_rank;
   int hint_a, hint_b;                 // L2 policy of the A / B TMA loads (l2_policy kinds)
+  // Grouped (MoE) mode, ag_moe.py:120-142: work item -> (slot, pid_n), slot record
+  // {expert, first gathered row, rows, seg_start | seg_end << 16}; B is the stacked
+  // [E * moe_n, K] expert weights.  Tiles acquire-wait the arrival counters of the
+  // source ranks [seg_start, seg_end] their rows come from (ag_moe.py:131-132).
+  const int4* moe_tab;
+  int moe_n;
+  const uint64_t* src_flags;          // [world] arrival counters (nullptr: no waits)
+  unsigned long long src_target;      // value a source's counter reaches when it has landed
+  // Pull engine (grouped AG): the first comm_ctas CTAs of the grid copy every peer's
+  // expert-major rows into this rank's workspace, source (rank+i)%w at step i
+  // (ag_moe.py:99-117), and release-add own_flags[src] when their share has landed.
+  int comm_ctas;
+  const uint8_t* peer_ws[kMaxWorld];
+  uint8_t* own_ws;
+  const int32_t* irb;                 // [world][E+1] row offsets of each expert in a source chunk
+  const int32_t* dstb;                // [world][E]   gathered row of (source, expert) piece
+  int n_experts;
+  long long row_bytes;
+  uint64_t* own_flags;
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -122,6 +141,35 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int step, int& pid
   pid_n = r / rows;
   if (p.tile_map) pid_m = __ldg(p.tile_map + pid_m);
   if (p.tile_map_n) pid_n = __ldg(p.tile_map_n + pid_n);
+}
+
+// Geometry of one output tile: first row, row limit (exclusive), first B row.
+struct TileGeo {
+  int pid_m, pid_n;
+  int row0, row_lim, b_row0;
+  int seg;  // grouped: seg_start | seg_end << 16
+};
+template <bool GROUPED, int TILE_M, int BN>
+__device__ __forceinline__ TileGeo tile_geo(const KParams& p, int step) {
+  TileGeo g;
+  if constexpr (GROUPED) {
+    // the reference's step -> (slot, pid_n) split, ag_moe.py:123-124
+    const int slot = step / p.num_pid_n;
+    g.pid_m = slot;
+    g.pid_n = step - slot * p.num_pid_n;
+    const int4 t = __ldg(p.moe_tab + slot);
+    g.row0 = t.y;
+    g.row_lim = t.y + t.z;
+    g.b_row0 = t.x * p.moe_n + g.pid_n * BN;
+    g.seg = t.w;
+  } else {
+    tile_coords(p, step, g.pid_m, g.pid_n);
+    g.row0 = g.pid_m * TILE_M;
+    g.row_lim = p.m;
+    g.b_row0 = g.pid_n * BN;
+    g.seg = 0;
+  }
+  return g;
 }
 
 // Row offset, inside the tile, of this CTA's A block h: MMA h covers tile rows
@@ -167,7 +215,127 @@ __device__ __forceinline__ void trace_rec(const KParams& p, unsigned kind, int t
   e[3] = payload;
 }
 
-template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+// ---------------------------------------------------------------- MoE pull engine
+// The reference's _pull_engine (ag_moe.py:99-117) as leading CTAs of the grouped
+// GEMM launch: for step i = 1..w-1, source s = (rank+i)%w, this CTA copies its
+// share (an even split of s's rows) of s's expert-major pieces from s's workspace
+// into the same offsets of this rank's workspace.  Every workspace holds its own
+// chunk at the gathered positions already (PRE), so a (source, expert) piece is one
+// contiguous byte range at identical offsets on every PE.  One thread drives a
+// ring of kPullSlots bulk copies (global -> shared -> global on the TMA engine);
+// after the last piece of a source it waits for its stores to land and
+// release-adds the source's arrival counter (target = comm_ctas).
+constexpr int kPullPiece = 32768;
+constexpr int kPullSlots = 6;
+
+__device__ __forceinline__ void bulk_wait_read_le(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+  }
+}
+
+struct PieceIt {
+  int e;
+  long long off;     // bytes already produced from the current run
+  long long lo, hi;  // this CTA's rows of the source chunk
+};
+
+__device__ __forceinline__ bool next_piece(const KParams& p, int s, PieceIt& it, const uint8_t*& src,
+                                           uint8_t*& dst, uint32_t& bytes) {
+  const int32_t* irb = p.irb + static_cast<long long>(s) * (p.n_experts + 1);
+  while (it.e < p.n_experts) {
+    const long long b0 = __ldg(irb + it.e), b1 = __ldg(irb + it.e + 1);
+    const long long r0 = max(it.lo, b0), r1 = min(it.hi, b1);
+    const long long run = (r1 - r0) * p.row_bytes;
+    if (r1 > r0 && it.off < run) {
+      const long long drow = __ldg(p.dstb + static_cast<long long>(s) * p.n_experts + it.e) + (r0 - b0);
+      const long long off = drow * p.row_bytes + it.off;
+      src = p.peer_ws[s] + off;
+      dst = p.own_ws + off;
+      bytes = static_cast<uint32_t>(min(static_cast<long long>(kPullPiece), run - it.off));
+      it.off += bytes;
+      return true;
+    }
+    if (b0 >= it.hi) break;
+    ++it.e;
+    it.off = 0;
+  }
+  it.e = p.n_experts;
+  return false;
+}
+
+__device__ void moe_pull_engine(const KParams& p, uint8_t* smem) {
+  if (threadIdx.x != 0) return;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kPullSlots * kPullPiece);
+  for (int i = 0; i < kPullSlots; ++i) mbar_init(&bar[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int c = blockIdx.x, C = p.comm_ctas;
+  uint8_t* dst_of[kPullSlots];
+  uint32_t bytes_of[kPullSlots];
+  unsigned long long nl = 0, ns = 0;  // pieces loaded / stored so far (all sources)
+  for (int i = 1; i < p.world; ++i) {
+    const int s = (p.rank + i) % p.world;
+    const int32_t* irb = p.irb + static_cast<long long>(s) * (p.n_experts + 1);
+    const long long rows = __ldg(irb + p.n_experts);
+    PieceIt it;
+    it.lo = rows * c / C;
+    it.hi = rows * (c + 1) / C;
+    it.off = 0;
+    // first expert whose run ends after lo
+    int lo_e = 0, hi_e = p.n_experts;
+    while (lo_e < hi_e) {
+      const int mid = (lo_e + hi_e) >> 1;
+      if (__ldg(irb + mid + 1) <= it.lo) lo_e = mid + 1;
+      else hi_e = mid;
+    }
+    it.e = lo_e;
+    bool more = it.hi > it.lo;
+    for (;;) {
+      while (more && nl - ns < static_cast<unsigned long long>(kPullSlots)) {
+        const uint8_t* src;
+        uint8_t* dst;
+        uint32_t bytes;
+        if (!next_piece(p, s, it, src, dst, bytes)) {
+          more = false;
+          break;
+        }
+        const int slot = static_cast<int>(nl % kPullSlots);
+        // the store that last used this slot (piece nl - kPullSlots) must have read it
+        if (nl >= static_cast<unsigned long long>(kPullSlots))
+          bulk_wait_read_le(static_cast<int>(ns - 1 - (nl - kPullSlots)));
+        mbar_arrive_expect_tx(&bar[slot], bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(smem + slot * kPullPiece)),
+            "l"(src), "r"(bytes), "r"(smem_u32(&bar[slot]))
+            : "memory");
+        dst_of[slot] = dst;
+        bytes_of[slot] = bytes;
+        ++nl;
+      }
+      if (ns == nl) break;
+      const int slot = static_cast<int>(ns % kPullSlots);
+      mbar_wait(&bar[slot], static_cast<uint32_t>((ns / kPullSlots) & 1));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_of[slot]),
+                   "r"(smem_u32(smem + slot * kPullPiece)), "r"(bytes_of[slot])
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      ++ns;
+    }
+    // this CTA's share of source s has landed: publish (notify(arrival, src), ag_moe.py:117)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    fence_proxy_async_global();
+    fence_sys();
+    red_add_release_sys(p.own_flags + s, 1);
+  }
+}
+
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
@@ -189,13 +357,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
+  if constexpr (GROUPED) {
+    // leading CTAs (whole clusters) run the pull engine and leave
+    if (static_cast<int>(blockIdx.x) < p.comm_ctas) {
+      moe_pull_engine(p, smem);
+      return;
+    }
+  }
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.num_pid_m * p.num_pid_n;
   const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = cta_rank == 0;
-  const int cluster_id = blockIdx.x / CG;
-  const int num_clusters = gridDim.x / CG;
+  const int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / CG;
+  const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -234,10 +408,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int work = cluster_id; work < p.total_work; work += num_clusters) {
         int step, kb0, kb1, slot;
         decode_work(p, work, step, kb0, kb1, slot);
-        int pid_m, pid_n;
-        tile_coords(p, step, pid_m, pid_n);
-        const int tile_m0 = pid_m * S::kTileM;
-        const int n0 = pid_n * BN + S::kBRows * cta_rank;    // this CTA's B rows
+        const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+        const int pid_m = geo.pid_m, pid_n = geo.pid_n;
+        const int tile_m0 = geo.row0;
+        const int n0 = geo.b_row0 + S::kBRows * cta_rank;    // this CTA's B rows
+        if constexpr (GROUPED) {
+          // wait(arrival, segment_start, segment_end) acquire -- ag_moe.py:131-132
+          if (p.src_flags) {
+            const int s0 = geo.seg & 0xFFFF, s1 = geo.seg >> 16;
+            const unsigned long long tw0 = p.trace ? globaltimer_ns() : 0;
+            bool waited = false;
+            for (int sr = s0; sr <= s1; ++sr) {
+              if (ready_mask & (1u << sr)) continue;
+              wait_geq_sys(p.src_flags + sr, p.src_target, p.timeout_ns, p.err,
+                           0x1000000ull | static_cast<unsigned long long>(sr));
+              ready_mask |= 1u << sr;
+              waited = true;
+            }
+            if (waited) {
+              trace_rec(p, 1, pid_m * p.num_pid_n + pid_n, tw0, globaltimer_ns(),
+                        (static_cast<unsigned long long>(s0) << 32) | static_cast<unsigned>(s1 - s0 + 1));
+              fence_proxy_async_global();
+            }
+          }
+        }
         if constexpr (AG_WAIT) {
           // wait(arrival, rank_beg, n) acquire -- ag_gemm.py:87-90 (this CTA's rows)
           bool waited = false;
@@ -374,8 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           release(&tfull_bar[1]);
           if (p.trace) {
-            int pm, pn;
-            tile_coords(p, step, pm, pn);
+            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+            const int pm = tg.pid_m, pn = tg.pid_n;
             trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
                       (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
           }
@@ -425,8 +619,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (CG == 2) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
           else umma_commit(&tfull_bar[acc]);
           if (p.trace) {
-            int pm, pn;
-            tile_coords(p, step, pm, pn);
+            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+            const int pm = tg.pid_m, pn = tg.pid_n;
             trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
                       (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
           }
@@ -449,8 +643,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
       int step, kb0, kb1, slot;
       decode_work(p, work, step, kb0, kb1, slot);
-      int pid_m, pid_n;
-      tile_coords(p, step, pid_m, pid_n);
+      const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+      const int pid_m = geo.pid_m, pid_n = geo.pid_n;
       const int acc = local % ACC;
       const uint32_t acc_phase = (local / ACC) & 1;
       if (p.trace && warp == kEpiWarp0 && lane == 0) {
@@ -513,9 +707,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int h = 0; h < MH; ++h) {
           if (MH == 2 || h == 0) wait_full(h);
-          const int wrow0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank) + quarter * 32;
+          const int wrow0 = geo.row0 + block_row<CG>(h, cta_rank) + quarter * 32;
           const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                  acc * S::kAccCols + h * BN;
+          // grouped tiles end at their expert's last row: a band that crosses it is
+          // stored row by row (a TMA box would overwrite the next expert's rows)
+          const bool band_masked = GROUPED && wrow0 + 32 > geo.row_lim;
 #pragma unroll 1
           for (int cc = 0; cc < BN; cc += kColsPerStore) {
             uint8_t* buf = epi_buf + epi_slot * S::kEpiBuf;
@@ -523,6 +720,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
             if constexpr (!OUT_F32)
               tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+            if (band_masked) {
+              tmem_ld_wait();
+              const int grow = wrow0 + lane;
+              const int col0 = pid_n * BN + cc;
+              if (grow < geo.row_lim && col0 < p.n) {
+                uint8_t* dst = static_cast<uint8_t*>(p.c) +
+                               (static_cast<long long>(grow) * p.ldc + col0) * (OUT_F32 ? 4 : 2);
+                const int ncols = min(kColsPerStore, p.n - col0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if (j * (16 / (OUT_F32 ? 4 : 2)) >= ncols) break;
+                  uint4 q;
+                  if constexpr (OUT_F32) {
+                    q = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                  } else {
+                    q = make_uint4(
+                        pack_bf16x2(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                        pack_bf16x2(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                        pack_bf16x2(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                        pack_bf16x2(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+                  }
+                  reinterpret_cast<uint4*>(dst)[j] = q;
+                }
+              }
+              continue;
+            }
             // the store issued from this buffer two rounds ago must have read it
             if (lane == 0) tma_store_wait_read<1>();
             __syncwarp();
@@ -785,11 +1008,11 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
   return TF_OK;
 }
 
-template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT>
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
              const CUtensorMap& tp, const KParams& kp, int grid, cudaStream_t stream,
              const float* tail_ws) {
-  auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT>;
+  auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT, GROUPED>;
   using S = Smem<CG, MH, BN>;
   static uint64_t attr_done = 0;  // per template instance, bit per device
   int dev = 0;
@@ -873,6 +1096,62 @@ int num_sms_of_current_device() {
   return n;
 }
 
+// Grouped (MoE) launch: tile table on the device, B = stacked expert weights,
+// optional pull-engine CTAs in front (ag_moe.py:20-142).
+int launch_grouped(const GemmLaunch& g, KParams kp, cudaStream_t stream) {
+  if (g.block_m != 128 && g.block_m != 256)
+    return fail(TF_ERR_CONFIG, "grouped GEMM: block_m must be 128 (one CTA) or 256 (CTA pair)");
+  if (!kp.vec_ok) return fail(TF_ERR_INVALID, "grouped GEMM: n must be a multiple of 8 and C rows 16-byte aligned");
+  const int cg = g.block_m == 128 ? 1 : 2;
+  kp.num_pid_m = g.moe_slots;
+  kp.moe_tab = static_cast<const int4*>(g.moe_tab);
+  kp.moe_n = static_cast<int>(g.n);
+  kp.src_flags = g.src_flags;
+  kp.src_target = g.src_target;
+  kp.comm_ctas = g.comm_ctas;
+  if (g.comm_ctas % cg) return fail(TF_ERR_CONFIG, "pull-engine CTAs must fill whole clusters");
+  for (int r = 0; r < kMaxWorld; ++r) kp.peer_ws[r] = g.peer_ws[r];
+  kp.own_ws = g.own_ws;
+  kp.irb = g.irb;
+  kp.dstb = g.dstb;
+  kp.n_experts = g.n_experts;
+  kp.row_bytes = g.row_bytes;
+  kp.own_flags = g.own_flags;
+  CUtensorMap ta, tb, tc, tp;
+  std::memset(&tp, 0, sizeof(tp));
+  int rc = make_tmap_2d(&ta, g.a, g.m, g.k, g.lda, 128);
+  if (rc) return rc;
+  rc = make_tmap_2d(&tb, g.b, static_cast<int64_t>(g.n_experts) * g.n, g.k, g.ldb, g.block_n / cg);
+  if (rc) return rc;
+  const int esz_c = g.out_f32 ? 4 : 2;
+  rc = make_tmap_2d(&tc, g.c, g.m, g.n, g.ldc, 32, esz_c, 128 / esz_c);
+  if (rc) return rc;
+  kp.tma_store = 1;
+  const int tiles = kp.num_pid_m * kp.num_pid_n;
+  kp.tail_base = tiles;
+  kp.split_s = 1;
+  kp.total_work = tiles;
+  int ctas = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
+  ctas -= g.comm_ctas;
+  int clusters = ctas / cg;
+  if (clusters < 1) clusters = 1;
+  if (tiles > 0 && clusters > tiles) clusters = tiles;
+  const int grid = g.comm_ctas + clusters * cg;
+  if (tiles == 0 && g.comm_ctas == 0) return TF_OK;
+  if (cg == 2) {
+    if (g.block_n == 256)
+      return g.out_f32 ? launch_t<2, 1, 256, true, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr)
+                       : launch_t<2, 1, 256, false, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr);
+    return g.out_f32 ? launch_t<2, 1, 128, true, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr)
+                     : launch_t<2, 1, 128, false, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr);
+  }
+  if (g.block_n == 256)
+    return g.out_f32 ? launch_t<1, 1, 256, true, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr)
+                     : launch_t<1, 1, 256, false, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr);
+  return g.out_f32 ? launch_t<1, 1, 128, true, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr)
+                   : launch_t<1, 1, 128, false, 0, false, true>(ta, tb, tc, tp, kp, grid, stream, nullptr);
+}
+
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
   if (g.m < 0 || g.n < 0 || g.k < 0) return fail(TF_ERR_INVALID, "negative GEMM dimension");
   if (g.m == 0 || g.n == 0) return TF_OK;
@@ -951,6 +1230,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     }
   }
   if (g.k == 0) return fail(TF_ERR_INVALID, "K must be >= 1");
+  if (g.moe_tab) return launch_grouped(g, kp, stream);
 
   const int cg = tile_m == 128 ? 1 : 2;
   const int mh = tile_m == 512 ? 2 : 1;

@@ -56,6 +56,19 @@ struct GemmLaunch {
   bool wait_on_b = false;            // chunk flags guard B rows (gathered N-side operand)
   const int32_t* tile_map_n = nullptr; // device [num_pid_n] permutation or nullptr
   int trace_rank = 0;                // rank tag for device trace events
+  // grouped (MoE) mode: a = gathered rows [m, k], b = stacked experts [n_experts * n, k]
+  const void* moe_tab = nullptr;     // device int4 [moe_slots] {expert, row0, rows, segs}
+  int moe_slots = 0;
+  int n_experts = 0;
+  const uint64_t* src_flags = nullptr;
+  uint64_t src_target = 0;
+  int comm_ctas = 0;                 // pull-engine CTAs in front of the GEMM CTAs
+  const uint8_t* peer_ws[kMaxWorld] = {};
+  uint8_t* own_ws = nullptr;
+  const int32_t* irb = nullptr;
+  const int32_t* dstb = nullptr;
+  int64_t row_bytes = 0;
+  uint64_t* own_flags = nullptr;
 };
 
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);

@@ -182,15 +182,107 @@ class ExpertParallelMoE:
         return outs[next(iter(outs))] if single else [outs[r] for r in range(t.world)]
 
 
+# ---------------------------------------------------------------------- AG + grouped GEMM
+def _agmoe_heap_bytes(max_rows: int, kdim: int, n_experts: int, world: int, block_m: int) -> int:
+    """Symmetric bytes tf_ag_moe_group_gemm carves per PE (two call parities of the
+    expert-major rows plus the tile/piece tables)."""
+    al = lambda x: (x + 1023) // 1024 * 1024  # noqa: E731
+    rows = al(max(max_rows, 1) * kdim * 2)
+    slots = -(-max_rows // block_m) + n_experts
+    tab = al(slots * 16 + world * (n_experts + 1) * 4 + world * n_experts * 4)
+    return 2 * (rows + tab) + (1 << 20)
+
+
+class AgMoeGroupGemm:
+    """Persistent AllGather + grouped GEMM (the reference's ag_moe_group_gemm,
+    ovs/kernels/ag_moe.py:20-142) for one team: a local team (all ranks in this
+    process, lists indexed by rank) or an IPC team (one rank per process).
+
+    Each call: routing [world, E] host counts (the same on every rank), this
+    rank's expert-grouped token rows [rows_r, K] bf16 and its stacked expert
+    weights [E, N, K] bf16 -> [total_rows, N] expert-major output.  One launch per
+    rank runs the pull engine (num_comm_sms CTAs) and the grouped tcgen05 GEMM,
+    whose tiles wait only on the source ranks their rows come from."""
+
+    def __init__(self, team: Team, n_experts: int, n: int, k: int, max_rows: int, *,
+                 block_m: int = 128, block_n: int = 256, num_gemm_sms: int = 0,
+                 num_comm_sms: int = 0, swizzle: bool = True, out_dtype=torch.bfloat16):
+        if n % 8 or k % 8:
+            raise ValueError("n and k must be multiples of 8")
+        if block_m not in (128, 256) or block_n not in (128, 256):
+            raise ValueError("block_m must be 128 or 256, block_n 128 or 256")
+        self.team, self.E, self.n, self.k, self.max_rows = team, n_experts, n, k, max_rows
+        self.block_m, self.block_n = block_m, block_n
+        self.num_gemm_sms, self.num_comm_sms, self.swizzle = num_gemm_sms, num_comm_sms, swizzle
+        self.out_dtype = out_dtype
+        self._keep = None
+
+    def _args(self, tokens, weights, out, routing_np) -> _lib.AgMoeArgs:
+        a = _lib.AgMoeArgs()
+        a.tokens = tokens.data_ptr() if tokens is not None and tokens.numel() else None
+        a.weights = weights.data_ptr()
+        a.out = out.data_ptr()
+        a.routing = routing_np.ctypes.data
+        a.n_experts, a.n, a.k, a.max_rows = self.E, self.n, self.k, self.max_rows
+        a.lda = int(tokens.stride(0)) if tokens is not None and tokens.numel() else self.k
+        a.ldo = int(out.stride(0))
+        a.out_dtype = _lib.TF_DTYPE_F32 if out.dtype == torch.float32 else _lib.TF_DTYPE_BF16
+        a.block_m, a.block_n = self.block_m, self.block_n
+        a.num_gemm_sms, a.num_comm_sms = self.num_gemm_sms, self.num_comm_sms
+        a.swizzle = 1 if self.swizzle else 0
+        return a
+
+    def __call__(self, routing, tokens, weights, out=None, phases=_lib.PHASE_ALL):
+        """Local team: tokens/weights/out are lists indexed by rank; IPC team: this
+        rank's tensors.  Returns the output(s)."""
+        t = self.team
+        routing_np = np.ascontiguousarray(np.asarray(routing, dtype=np.int64))
+        if routing_np.shape != (t.world, self.E):
+            raise ValueError(f"routing must be [{t.world}, {self.E}], got {routing_np.shape}")
+        total = int(routing_np.sum())
+        single = not isinstance(tokens, (list, tuple))
+        ranks = list(t.local_ranks())
+        toks = {ranks[0]: tokens} if single else dict(enumerate(tokens))
+        wts = {ranks[0]: weights} if single else dict(enumerate(weights))
+        outs = {}
+        for r in ranks:
+            w = wts[r]
+            if w.dtype != torch.bfloat16 or tuple(w.shape) != (self.E, self.n, self.k) or not w.is_contiguous():
+                raise ValueError(f"weights must be contiguous bf16 [{self.E}, {self.n}, {self.k}]")
+            tk = toks[r]
+            rows = int(routing_np[r].sum())
+            if tk is not None and (tk.dtype != torch.bfloat16 or tuple(tk.shape) != (rows, self.k)):
+                raise ValueError(f"rank {r} tokens must be bf16 [{rows}, {self.k}]")
+            o = None if out is None else (out if single else out[r])
+            if o is None:
+                o = torch.empty((total, self.n), dtype=self.out_dtype, device=w.device)
+            outs[r] = o
+        args = {r: self._args(toks[r], wts[r], outs[r], routing_np) for r in ranks}
+        self._keep = (routing_np, toks, wts, outs, args)
+        for ph in (_lib.PHASE_PRE, _lib.PHASE_MAIN):
+            if not ph & phases:
+                continue
+            for r in ranks:
+                dev = t.devices[r]
+                with torch.cuda.device(dev):
+                    s = torch.cuda.current_stream(dev)
+                    _lib.call("tf_ag_moe_group_gemm", t.handle, r, C.byref(args[r]), ph, s.cuda_stream)
+        return outs[ranks[0]] if single else [outs[r] for r in range(t.world)]
+
+
 # ---------------------------------------------------------------------- drop-in
 def ag_moe_group_gemm(token_shards, expert_weights, routing, ctx: WorkloadContext) -> WorkloadRun:
     """Per rank r: expert-sorted gathered tokens times rank r's weight shards
     (ovs/kernels/ag_moe.py:20).  token_shards[r]: [rows_r, K] grouped by expert;
     expert_weights[r][e]: [N_per_rank, K]; routing [world, E] counts.
 
-    Device path: copy-engine AllGather of the dynamic-size chunks into every
-    rank's symmetric workspace (rank-major, ag_moe.py:99-115), one expert-major
-    row permutation, then one tcgen05 GEMM per expert."""
+    Device path (tf_ag_moe_group_gemm): per rank ONE launch in which pull-engine
+    CTAs gather the peers' dynamic-size chunks (source (rank+i)%w at step i,
+    ag_moe.py:99-117) straight into expert-major rows of the symmetric
+    workspace, while the grouped tcgen05 GEMM walks the swizzle_ag_moe schedule
+    and acquire-waits, per tile, only the source ranks [segment_start,
+    segment_end] its rows come from (ag_moe.py:120-142).  Output rows are
+    expert-major."""
     from . import kernels as K
 
     topo = ctx.topology
@@ -220,57 +312,30 @@ def ag_moe_group_gemm(token_shards, expert_weights, routing, ctx: WorkloadContex
     devices = K._devices_for(ctx, token_shards)
     pt = K._prepare(token_shards, devices, kp, 0)
     pw = [K._prepare(list(expert_weights[r]), [devices[r]] * n_experts, kp, 1) for r in range(world)]
-    kp = pt.kdim
+    kdim = pt.kdim
     if pt.kind == "exact":
         for p in pw:
             K._exact_bound_check(pt, p, k)
     odt = K._out_dtype(ctx.out_dtype, pt)
-
-    rows_by_rank = routing.sum(axis=1)
-    chunk_base = np.concatenate([[0], np.cumsum(rows_by_rank)])
-    total = int(chunk_base[-1])
-    tokens_per_expert = routing.sum(axis=0)
-    expert_base = np.concatenate([[0], np.cumsum(tokens_per_expert)])
-    in_rank_base = np.concatenate([np.zeros((world, 1), np.int64), np.cumsum(routing, axis=1)], axis=1)
-    # expert-major row e,s,i <- rank-major row chunk_base[s] + in_rank_base[s,e] + i
-    perm = np.empty(total, dtype=np.int64)
-    pos = 0
-    for e in range(n_experts):
-        for s in range(world):
-            c = int(routing[s, e])
-            start = int(chunk_base[s] + in_rank_base[s, e])
-            perm[pos:pos + c] = np.arange(start, start + c)
-            pos += c
-
-    row_bytes = kp * 2
-    team = Team(world, devices, max(total, 1) * row_bytes + (1 << 20), 4 * world + 64)
+    total = int(routing.sum())
+    n_pad = max((n_per_rank + 7) // 8 * 8, 8)
+    block_m = 256 if ctx.hw_block_m >= 256 else 128
+    stacked = []
+    for r in range(world):
+        wr = torch.zeros((n_experts, n_pad, kdim), dtype=torch.bfloat16, device=f"cuda:{devices[r]}")
+        for e in range(n_experts):
+            wr[e, :n_per_rank] = pw[r].tensors[e]
+        stacked.append(wr)
+    team = Team(world, devices, _agmoe_heap_bytes(total, kdim, n_experts, world, block_m), 4 * world + 64)
     heap = SymmetricHeap(topo, team=team)
-    ws = heap.alloc(max(total, 1) * row_bytes, align=1024)
-    outs = []
-    # AllGather: every rank's chunk into every rank's workspace at its rank-major offset
-    for r in range(world):
-        with torch.cuda.device(devices[r]):
-            s = torch.cuda.current_stream(devices[r])
-            for d in range(world):
-                if rows_by_rank[r]:
-                    heap.putmem(heap.symm_at(ws, d), int(chunk_base[r]) * row_bytes,
-                                pt.tensors[r], from_pe=r, stream=s)
-    for d in sorted(set(devices)):
-        torch.cuda.synchronize(d)
-    for r in range(world):
-        dev = devices[r]
-        with torch.cuda.device(dev):
-            gathered = heap.view(ws, r, torch.bfloat16, (max(total, 1), kp))[:total]
-            perm_t = torch.from_numpy(perm).to(f"cuda:{dev}")
-            a_sorted = gathered.index_select(0, perm_t) if total else gathered
-            out = torch.zeros((total, n_per_rank), dtype=odt, device=f"cuda:{dev}")
-            for e in range(n_experts):
-                lo, hi = int(expert_base[e]), int(expert_base[e + 1])
-                if hi > lo and n_per_rank > 0:
-                    K.gemm(a_sorted[lo:hi], pw[r].tensors[e], out[lo:hi], out_dtype=odt,
-                           block_m=128, block_n=ctx.hw_block_n, group_m=ctx.group_m)
-            outs.append(out)
+    op = AgMoeGroupGemm(team, n_experts, n_pad, kdim, max(total, 1), block_m=block_m,
+                        block_n=ctx.hw_block_n, num_gemm_sms=ctx.num_gemm_sms,
+                        num_comm_sms=ctx.num_comm_sms, swizzle=ctx.swizzle, out_dtype=odt)
+    toks = [pt.tensors[r] if pt.tensors[r].shape[0] else None for r in range(world)]
+    outs = [torch.zeros((total, n_pad), dtype=odt, device=f"cuda:{devices[r]}") for r in range(world)]
+    if total and n_per_rank:
+        op(routing, toks, stacked, out=outs)
     for d in sorted(set(devices)):
         torch.cuda.synchronize(d)
     team.check()
-    return WorkloadRun([K._finish(o, pt) for o in outs], None, heap, {"workspace": ws})
+    return WorkloadRun([K._finish(o[:, :n_per_rank], pt) for o in outs], None, heap, {})
