@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--no-layer", action="store_true")
     p.add_argument("--only-layer", action="store_true")
     p.add_argument("--only-attn", action="store_true")
+    p.add_argument("--only-agmoe", action="store_true")
     return p.parse_args()
 
 
@@ -343,6 +344,116 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
                            "frac": round(ach / NVLINK_GBS, 4),
                            "frac_vs_measured_p2p": round(ach / NVLINK_MEASURED_GBS, 4)}
     return out
+
+
+# ------------------------------------------------------------------ AG + grouped GEMM (ag_moe_group_gemm)
+AGM_TP, AGM_N = 8, 512  # W13 of a DeepSeek-V3 expert (2 x 2048) sharded over TP=8: 512 columns per rank
+
+
+def _agm_counts(rng_seed, ranks, dev):
+    """[ranks, E] routed-row counts: top-8 of N(0,1) logits for MOE_T tokens per rank."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(rng_seed)
+    out = []
+    for _ in range(ranks):
+        idx = torch.randn(MOE_T, MOE_E, generator=g).to(f"cuda:{dev}").topk(MOE_K, dim=1).indices
+        out.append(torch.bincount(idx.flatten(), minlength=MOE_E).cpu().numpy())
+    import numpy as np
+    return np.stack(out).astype(np.int64)
+
+
+def bench_ag_moe(dev, world, rank, steps, warmup, flush, stream, distributed, peaks):
+    """The reference's MoE operator (ag_moe_group_gemm, ovs/kernels/ag_moe.py:20) with
+    expert compute: DeepSeek-V3-like 256 experts, top-8, hidden 7168, 4096 tokens per
+    source rank, W13 shard N=512 per rank (TP=8).  N=1: one rank's work of the TP=8
+    job (all 8 sources' rows gathered: 262144 rows), no exchange; N>1: a real
+    AllGather over the team with `world` sources.  Comparators: cuBLAS per-expert
+    GEMMs (torch.matmul loop) and torch._grouped_mm on the same expert-major rows."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_02953_b200 import moe as M
+    from paper_2605_02953_b200.shmem import Team
+    if world == 1:
+        routing = _agm_counts(777, AGM_TP, dev).sum(axis=0, keepdims=True)
+    else:
+        routing = _agm_counts(777, world, dev)
+    total = int(routing.sum())
+    rows_r = int(routing[rank].sum())
+    k, n, E = MOE_H, AGM_N, MOE_E
+    heap = M._agmoe_heap_bytes(total, k, E, world, 128)  # 128-row slots bound every block_m
+    team = (Team.from_process_group(heap_bytes=heap, signal_slots=256) if distributed
+            else Team(1, [dev], heap_bytes=heap, signal_slots=256))
+    g = torch.Generator(device="cpu").manual_seed(99 + rank)
+    tok = torch.empty(rows_r, k, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    for i in range(0, rows_r, 16384):  # generate in slices (host RAM)
+        j = min(rows_r, i + 16384)
+        tok[i:j] = torch.randn(j - i, k, generator=g).to(torch.bfloat16)
+    wts = (torch.randn(E, n, k, generator=g) * k ** -0.5).to(torch.bfloat16).to(f"cuda:{dev}")
+    out = torch.empty(total, n, dtype=torch.bfloat16, device=f"cuda:{dev}")
+    bm = int(os.environ.get("TF_AGM_BM", "128"))  # 128: 1.69 ms vs CTA pair 1.80 ms (tile waste on ~1k-row experts)
+    op = M.AgMoeGroupGemm(team, E, n, k, total, block_m=bm, block_n=256, num_comm_sms=8)
+
+    def timed(fn, n_steps, n_warm):
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_steps)]
+        with torch.cuda.stream(stream):
+            for i in range(n_warm + n_steps):
+                if i >= n_warm:
+                    flush.zero_()
+                    ev[i - n_warm][0].record(stream)
+                fn()
+                if i >= n_warm:
+                    ev[i - n_warm][1].record(stream)
+            torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in ev) / n_steps
+
+    if distributed:
+        dist.barrier()
+    ms = timed(lambda: op(routing, tok, wts, out=out), steps, warmup)
+    ms = max_over_ranks([ms], dev, distributed)[0]
+    team.check()
+    flops = 2.0 * total * n * k
+    peak = peaks.get("bf16_tflops", 1590.0)
+    hbm = peaks.get("hbm_gbs", 6550.1)
+    bytes_ = total * k * 2 + E * n * k * 2 + total * n * 2
+    t_tensor, t_hbm = flops / (peak * 1e12) * 1e3, bytes_ / (hbm * 1e9) * 1e3
+    res = {
+        "workload": (f"ag_moe_group_gemm: {E} experts, top-{MOE_K}, hidden {k}, {MOE_T} tokens per source "
+                     f"rank, W13 shard N={n} (TP={AGM_TP}); " +
+                     (f"one rank's work of the TP={AGM_TP} job ({total} gathered rows), no exchange"
+                      if world == 1 else f"AllGather over {world} ranks ({total} gathered rows)")),
+        "ms": round(ms, 4), "tflops": round(flops / (ms * 1e-3) / 1e12, 2), "block_m": bm,
+        "roofline": {"bound": "tensor" if t_tensor >= t_hbm else "hbm",
+                     "t_roof_ms": round(max(t_tensor, t_hbm), 4),
+                     "frac": round(max(t_tensor, t_hbm) / ms, 4), "peak_tflops": peak,
+                     "algorithmic_bytes": bytes_},
+    }
+    if world == 1 and rank == 0:
+        ebase = np.concatenate([[0], np.cumsum(routing.sum(axis=0))])
+        segs = [(int(ebase[e]), int(ebase[e + 1])) for e in range(E)]
+        out2 = torch.empty_like(out)
+
+        def per_expert():
+            for e, (lo, hi) in enumerate(segs):
+                if hi > lo:
+                    torch.matmul(tok[lo:hi], wts[e].t(), out=out2[lo:hi])
+        c_ms = timed(per_expert, max(3, steps // 2), 2)
+        cmp_ = {"cublas_per_expert": {"ms": round(c_ms, 4), "speedup": round(c_ms / ms, 4)}}
+        err = (out.float() - out2.float()).abs().max().item() / max(out2.float().abs().max().item(), 1e-30)
+        cmp_["max_rel_err_vs_cublas"] = round(err, 5)
+        try:
+            offs = torch.tensor(ebase[1:], dtype=torch.int32, device=f"cuda:{dev}")
+            wt = wts.transpose(1, 2)
+            gm_ms = timed(lambda: torch._grouped_mm(tok, wt, offs=offs), max(3, steps // 2), 2)
+            cmp_["torch_grouped_mm"] = {"ms": round(gm_ms, 4), "speedup": round(gm_ms / ms, 4)}
+        except Exception as exc:  # noqa: BLE001
+            cmp_["torch_grouped_mm"] = {"error": f"{type(exc).__name__}: {exc}"[:160]}
+        res["comparator"] = cmp_
+    team.close()
+    del tok, wts, out
+    torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------------ SP attention scores (config 3)
@@ -758,6 +869,12 @@ def main_ours(args):
         torch.cuda.set_device(0)
         print(json.dumps(bench_attention(0, max(args.steps, 3), load_peaks()[0])), flush=True)
         return
+    if args.only_agmoe:  # probe: ag_moe_group_gemm only
+        torch.cuda.set_device(0)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
+        print(json.dumps(bench_ag_moe(0, 1, 0, args.steps, args.warmup, flush, torch.cuda.Stream(), False,
+                                      load_peaks()[0])), flush=True)
+        return
     if args.only_layer:  # probe: config 5 only
         torch.cuda.set_device(0)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
@@ -1027,6 +1144,13 @@ def main_ours(args):
         moe = bench_moe(team, dev, world, rank, args.steps, args.warmup, flush, stream,
                         distributed, peaks)
 
+    agmoe = None
+    if not args.no_moe:
+        try:
+            agmoe = bench_ag_moe(dev, world, rank, max(3, args.steps // 2), 2, flush, stream, distributed, peaks)
+        except Exception as exc:  # noqa: BLE001
+            agmoe = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     attn = None
     if not args.no_attn and world == 1:
         attn = bench_attention(dev, 3, peaks)
@@ -1069,7 +1193,7 @@ def main_ours(args):
                 "tflops": round(total_flops / (cub_ms * 1e-3) / 1e12, 3),
                 "speedup": round(cub_ms / step_ms, 4)},
             "overlap": overlap,
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "attention": attn, "layer": layer,
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "ag_moe": agmoe, "attention": attn, "layer": layer,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -118,7 +118,8 @@ int make_plan(const tf_team* t, const tf_agmoe_args* a, Plan& P) {
   for (int e = 0; e < E; ++e) P.slots += (P.tokens_per_expert[e] + bm - 1) / bm;
   P.max_slots = (P.max_rows + bm - 1) / bm + E;
   P.row_bytes = a->k * 2;
-  P.rows_bytes = align_up(static_cast<size_t>(std::max<int64_t>(P.max_rows, 1)) * P.row_bytes, 1024);
+  // one rank: the caller's rows are already expert-major, no gathered copy is kept
+  P.rows_bytes = w == 1 ? 0 : align_up(static_cast<size_t>(std::max<int64_t>(P.max_rows, 1)) * P.row_bytes, 1024);
   P.tab_bytes = align_up(static_cast<size_t>(P.max_slots) * 16 + P.irb.size() * 4 + P.dstb.size() * 4, 1024);
   int cc = a->num_comm_sms > 0 ? a->num_comm_sms : 8;
   cc = (cc + P.cg - 1) / P.cg * P.cg;

@@ -187,7 +187,7 @@ def _agmoe_heap_bytes(max_rows: int, kdim: int, n_experts: int, world: int, bloc
     """Symmetric bytes tf_ag_moe_group_gemm carves per PE (two call parities of the
     expert-major rows plus the tile/piece tables)."""
     al = lambda x: (x + 1023) // 1024 * 1024  # noqa: E731
-    rows = al(max(max_rows, 1) * kdim * 2)
+    rows = al(max(max_rows, 1) * kdim * 2) if world > 1 else 0
     slots = -(-max_rows // block_m) + n_experts
     tab = al(slots * 16 + world * (n_experts + 1) * 4 + world * n_experts * 4)
     return 2 * (rows + tab) + (1 << 20)
