@@ -227,6 +227,32 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
 int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int phase,
                void* stream, void* comm_stream);
 
+/* ------------------------------------------------------------------ NVLS multicast region
+ * The B200 form of multimem_ld_reduce / multimem_st (shmem.py:335-385): one
+ * multicast object over every PE's copy of an `nvls` region, reached with
+ * multimem.ld_reduce (sum of all copies, reduced in the NVSwitch) and
+ * multimem.st (write every copy).  Opt-in: tf_nvls_supported probes
+ * CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED; creation failures return
+ * TF_ERR_CONFIG and callers keep the P2P paths.
+ *   local team: tf_team_nvls_create does everything (fd_out = -1).
+ *   IPC team  : rank 0 tf_team_nvls_create -> POSIX fd (pass it to the peers
+ *               over a Unix socket, SCM_RIGHTS); the others tf_team_nvls_import;
+ *               then every rank tf_team_nvls_add_device, a barrier, and
+ *               tf_team_nvls_bind. */
+int tf_nvls_supported(int device, int* supported);
+int tf_team_nvls_create(tf_team* t, size_t bytes, int* fd_out);
+int tf_team_nvls_import(tf_team* t, size_t bytes, int fd);
+int tf_team_nvls_add_device(tf_team* t);
+int tf_team_nvls_bind(tf_team* t);
+int tf_nvls_enabled(tf_team* t, int* enabled, size_t* bytes);
+int tf_nvls_alloc(tf_team* t, size_t nbytes, size_t align, uint64_t* offset);
+int tf_nvls_ptr(tf_team* t, int pe, uint64_t offset, void** uc, void** mc);
+/* out[0:count) = sum over PEs of region[offset:...] (dtype 0 bf16 with fp32
+ * accumulation, 1 f32, 2 int64); device out, stream-ordered on PE pe's device. */
+int tf_nvls_reduce(tf_team* t, int pe, uint64_t offset, int dtype, int64_t count, void* out, void* stream);
+/* every PE's region[offset:offset+bytes) = src (device, 16-byte aligned). */
+int tf_nvls_broadcast(tf_team* t, int pe, uint64_t offset, const void* src, size_t bytes, void* stream);
+
 /* ------------------------------------------------------------------ SP attention scores
  * AllGather-KV fused with Q.K^T (BASELINE config 3): structurally
  * ag_gemm (ag_gemm.py:20-94) with the gathered operand on the N (key) side.

@@ -122,6 +122,16 @@ _SIGS = {
     "tf_moe_dispatch": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
     "tf_moe_combine": (ci, [vp, ci, C.POINTER(MoeArgs), ci, vp]),
     "tf_ag_moe_group_gemm": (ci, [vp, ci, C.POINTER(AgMoeArgs), ci, vp]),
+    "tf_nvls_supported": (ci, [ci, C.POINTER(ci)]),
+    "tf_team_nvls_create": (ci, [vp, sz, C.POINTER(ci)]),
+    "tf_team_nvls_import": (ci, [vp, sz, ci]),
+    "tf_team_nvls_add_device": (ci, [vp]),
+    "tf_team_nvls_bind": (ci, [vp]),
+    "tf_nvls_enabled": (ci, [vp, C.POINTER(ci), C.POINTER(sz)]),
+    "tf_nvls_alloc": (ci, [vp, sz, sz, C.POINTER(u64)]),
+    "tf_nvls_ptr": (ci, [vp, ci, u64, C.POINTER(vp), C.POINTER(vp)]),
+    "tf_nvls_reduce": (ci, [vp, ci, u64, ci, i64, vp, vp]),
+    "tf_nvls_broadcast": (ci, [vp, ci, u64, vp, sz, vp]),
 }
 
 _lib = None

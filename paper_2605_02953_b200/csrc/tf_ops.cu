@@ -234,6 +234,60 @@ __global__ void __launch_bounds__(256) ar_reduce_kernel(
   }
 }
 
+// Two-shot GEMM+AllReduce over NVLS (the reference's multimem_ld_reduce +
+// multimem_st pair, gemm_ar.py:103-133): the partials live in the team's
+// multicast region; for each owned block the owner issues multimem.ld_reduce on
+// the multicast address (the NVSwitch sums every rank's copy) and multimem.st of
+// the sum (the switch writes it into every rank's result copy), 16 bytes per
+// instruction, then release-flags the block on every peer.  Requires
+// ld * esz % 16 == 0 (ld is n rounded up to 8).
+template <bool F32>
+__global__ void __launch_bounds__(256) ar_nvls_kernel(
+    const uint8_t* mc_parts, uint8_t* mc_res, long long ld, int world, int rank, long long m,
+    long long n, PeerCnt counters, unsigned long long expected, PeerFlag flags, int col_chunks,
+    unsigned long long timeout_ns, unsigned long long* err) {
+  constexpr int esz = F32 ? 4 : 2;
+  constexpr int per_vec = 16 / esz;
+  const int nblocks = static_cast<int>((m + 127) / 128);
+  const int my_blocks = (nblocks - rank + world - 1) / world;
+  const int items = my_blocks * col_chunks;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int bi = item / col_chunks;
+    const int cc = item - bi * col_chunks;
+    const int b = rank + bi * world;
+    if (threadIdx.x < world)
+      wait_geq_sys(counters.p[threadIdx.x] + b, expected, timeout_ns, err, 0x4000000ull | b);
+    __syncthreads();
+    // partials were written through the unicast alias; read them through the multicast one
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    const long long r0 = static_cast<long long>(b) * 128, r1 = min(r0 + 128, m);
+    const long long c0 = static_cast<long long>(cc) * 2048, c1 = min(c0 + 2048, ld);
+    const long long vec_per_row = (c1 - c0) / per_vec;
+    const long long total = (r1 - r0) * vec_per_row;
+    for (long long v = threadIdx.x; v < total; v += blockDim.x) {
+      const long long r = r0 + v / vec_per_row;
+      const long long c = c0 + (v % vec_per_row) * per_vec;
+      const long long off = (r * ld + c) * esz;
+      uint32_t q0, q1, q2, q3;
+      if constexpr (F32)
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3) : "l"(mc_parts + off) : "memory");
+      else
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(q0), "=r"(q1), "=r"(q2), "=r"(q3) : "l"(mc_parts + off) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_res + off),
+                   "f"(__uint_as_float(q0)), "f"(__uint_as_float(q1)), "f"(__uint_as_float(q2)),
+                   "f"(__uint_as_float(q3))
+                   : "memory");
+    }
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    fence_sys();
+    __syncthreads();
+    if (threadIdx.x < world) red_add_release_sys(flags.p[threadIdx.x] + b, 1);
+    __syncthreads();
+  }
+}
+
 // two-shot tail: wait until every block's column chunks have been flagged
 // (target = epoch * col_chunks), then copy the result buffer into `out`.
 __global__ void ar_gather_kernel(const void* result, long long ld, void* out, long long out_ld,
@@ -244,6 +298,7 @@ __global__ void ar_gather_kernel(const void* result, long long ld, void* out, lo
   for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
     if (threadIdx.x == 0) wait_geq_sys(flags + b, target, timeout_ns, err, 0x4800000ull | b);
     __syncthreads();
+    asm volatile("fence.proxy.alias;" ::: "memory");  // NVLS: results arrived through the multicast alias
     const long long r0 = static_cast<long long>(b) * 128, r1 = min(r0 + 128, m);
     const long long row_bytes = n * esz;
     for (long long r = r0; r < r1; ++r) {
@@ -564,7 +619,35 @@ int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int
     if (rc) return rc;
   }
   const uint64_t e = ws->epoch[rank];
+  // NVLS two-shot: partials and results in the team's multicast region
+  size_t nv_off = 0;
+  const bool nvls = two_shot && w > 1 && t->distinct_devices && (ld * esz) % 16 == 0 &&
+                    tf::nvls_workspace(t, key, 2 * bytes, &nv_off);
   auto launch_reduce = [&](cudaStream_t rs) -> int {
+    if (nvls) {
+      tf::PeerCnt cnt{};
+      tf::PeerFlag flg{};
+      for (int p = 0; p < w; ++p) {
+        cnt.p[p] = t->pes[p].sig + ws->sig_base;
+        flg.p[p] = t->pes[p].sig + ws->sig_base + nblocks;
+      }
+      const int64_t my_blocks = (nblocks - rank + w - 1) / w;
+      int grid = overlap ? (args->num_comm_sms > 0 ? args->num_comm_sms * 2 : 16)
+                         : tf::num_sms_of_current_device();
+      if (grid > my_blocks * col_chunks) grid = static_cast<int>(my_blocks * col_chunks);
+      if (grid < 1) grid = 1;
+      const unsigned long long expected = e * static_cast<unsigned long long>(num_pid_n);
+      const uint8_t* mp = t->nvls_mc + nv_off;
+      uint8_t* mr = t->nvls_mc + nv_off + bytes;
+      if (f32)
+        tf::ar_nvls_kernel<true><<<grid, 256, 0, rs>>>(mp, mr, ld, w, rank, m, n, cnt, expected, flg,
+                                                       col_chunks, t->timeout_ns, t->err_word(rank));
+      else
+        tf::ar_nvls_kernel<false><<<grid, 256, 0, rs>>>(mp, mr, ld, w, rank, m, n, cnt, expected, flg,
+                                                        col_chunks, t->timeout_ns, t->err_word(rank));
+      TF_CUDA_TRY(cudaGetLastError());
+      return TF_OK;
+    }
     tf::PeerBase parts{};
     tf::PeerCnt cnt{};
     tf::PeerOut res{};
@@ -597,8 +680,9 @@ int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int
   auto launch_gather = [&](cudaStream_t gs) -> int {
     const int64_t ldc = args->ldc ? args->ldc : n;
     int grid = static_cast<int>(std::min<int64_t>(nblocks, tf::num_sms_of_current_device()));
+    const uint8_t* res = nvls ? t->nvls_uc[rank] + nv_off + bytes : t->pes[rank].base + ws->data_off + bytes;
     tf::ar_gather_kernel<<<std::max(grid, 1), 256, 0, gs>>>(
-        t->pes[rank].base + ws->data_off + bytes, ld, args->c, ldc, esz, m, n,
+        res, ld, args->c, ldc, esz, m, n,
         t->pes[rank].sig + ws->sig_base + nblocks, e * static_cast<unsigned long long>(col_chunks),
         t->timeout_ns, t->err_word(rank));
     TF_CUDA_TRY(cudaGetLastError());
@@ -615,7 +699,8 @@ int tf_gemm_ar(tf_team* t, int rank, const tf_gemm_args* args, int two_shot, int
     g.rows_per_rank = m;
     g.slot_ld = ld;
     g.out_f32 = f32;
-    g.peer_slots[0] = t->pes[rank].base + ws->data_off;
+    g.peer_slots[0] = nvls ? static_cast<void*>(t->nvls_uc[rank] + nv_off)
+                           : static_cast<void*>(t->pes[rank].base + ws->data_off);
     g.peer_counts[0] = t->pes[rank].sig + ws->sig_base;
     g.err = t->err_word(rank);
     g.timeout_ns = t->timeout_ns;

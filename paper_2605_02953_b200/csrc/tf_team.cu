@@ -357,6 +357,7 @@ int tf_team_open_peers(tf_team* t, const void* blobs, size_t blob_len) {
 int tf_team_destroy(tf_team* t) {
   if (!t) return TF_OK;
   tf::layer_release_team(t);
+  tf::nvls_release(t);
   for (int p = 0; p < t->world; ++p) {
     if (!t->pes[p].base) continue;
     tf::DeviceGuard g(t->pes[p].device);

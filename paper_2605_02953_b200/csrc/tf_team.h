@@ -58,6 +58,18 @@ struct tf_team {
 
   std::map<int, std::pair<void*, size_t>> scratch_bufs;  // per-device private scratch
 
+  // NVLS multicast region (tf_nvls.cu): one multicast object over every PE's
+  // physical allocation of nvls_bytes; per local PE a unicast mapping, and one
+  // multicast VA through which multimem.ld_reduce / multimem.st reach all copies.
+  size_t nvls_bytes = 0, nvls_top = 0;
+  int nvls_state = 0;                       // 0 none, 1 object, 2 device added, 3 bound (usable)
+  unsigned long long nvls_mc_handle = 0;    // CUmemGenericAllocationHandle
+  std::vector<unsigned long long> nvls_phys;// per PE (local PEs only)
+  std::vector<uint8_t*> nvls_uc;            // per PE unicast VA (local PEs only)
+  uint8_t* nvls_mc = nullptr;               // multicast VA (this process)
+  size_t nvls_gran = 0;
+  std::map<std::string, size_t> nvls_ws;    // per-op workspaces carved from the NVLS region
+
   unsigned long long* err_word(int pe);
   void* scratch(int device, size_t bytes);
   tf::Workspace* workspace(const std::string& key, size_t data_bytes, size_t sig_slots, int* rc);
@@ -68,4 +80,8 @@ namespace tf {
 int stream_signal_set(tf_team* t, int pe, uint64_t slot, uint64_t value, cudaStream_t s);
 int team_barrier_arrive(tf_team* t, int rank, cudaStream_t s);
 int team_barrier_wait(tf_team* t, int rank, cudaStream_t s);
+void nvls_release(tf_team* t);
+// offset of an op workspace in the NVLS region (allocated on first use); false if
+// NVLS is off or the region is too small (callers then keep their P2P path)
+bool nvls_workspace(tf_team* t, const std::string& key, size_t bytes, size_t* off);
 }  // namespace tf

@@ -18,6 +18,7 @@ benchmarking: `AllGatherGemm`, `GemmReduceScatter`, and the single-GPU core
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -482,6 +483,10 @@ def gemm_allreduce(a_shards, b_shards, ctx: WorkloadContext, use_multimem_st: bo
     ld = (n + 7) // 8 * 8
     nblocks = (m + 127) // 128
     team = Team(world, devices, 2 * m * ld * esz + (1 << 20), 2 * nblocks + 64)
+    if two_shot and team.distinct_devices and world > 1 and os.environ.get("TF_NVLS", "1") != "0":
+        # two-shot through the switch (multimem.ld_reduce + multimem.st) when the
+        # box exposes NVLS; otherwise the P2P owner-reduce + broadcast below
+        team.enable_nvls(2 * m * ld * esz + (4 << 20))
     heap = SymmetricHeap(topo, team=team)
     outs, args = [], {}
     for r in range(world):

@@ -35,6 +35,7 @@ SEMANTICS = ("relaxed", "acquire", "release")
 class SymmHandle:
     offset: int
     nbytes: int
+    space: str = "heap"  # "heap" (P2P symmetric heap) or "nvls" (multicast region)
 
 
 @dataclass(frozen=True)
@@ -100,6 +101,45 @@ class RemoteRegion:
 HANDLE_BLOB = 128
 
 
+def share_fd(fd: int | None, group=None) -> int:
+    """Pass rank 0's file descriptor to every rank of the group (SCM_RIGHTS over an
+    abstract Unix socket whose name travels through torch.distributed).  Rank 0
+    returns its own fd; the others a duplicate they own.  Used for the NVLS
+    multicast handle (POSIX fd export, tf_team_nvls_create)."""
+    import os
+    import socket
+    import uuid
+
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    name = [f"\0tilefuse-fd-{os.getpid()}-{uuid.uuid4().hex}" if rank == 0 else None]
+    dist.broadcast_object_list(name, src=0, group=group)
+    if world == 1:
+        return fd
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(name[0])
+        srv.listen(world)
+        dist.barrier(group)
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"fd"], [int(fd)])
+        finally:
+            srv.close()
+        dist.barrier(group)
+        return fd
+    dist.barrier(group)
+    with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.connect(name[0])
+        _, fds, _, _ = socket.recv_fds(c, 16, 1)
+    dist.barrier(group)
+    if len(fds) != 1:
+        raise ProtocolError("file descriptor transfer failed")
+    return fds[0]
+
+
 def exchange_handles(blob: bytes, group=None) -> bytes:
     """All-gather one fixed-size IPC handle blob per rank over torch.distributed;
     returns the concatenation in rank order (what tf_team_open_peers expects).
@@ -144,8 +184,10 @@ class Team:
         self.handle = h
 
     @classmethod
-    def from_process_group(cls, heap_bytes: int, signal_slots: int = 1 << 14, group=None):
-        """IPC team over the current torch.distributed group (one GPU per rank)."""
+    def from_process_group(cls, heap_bytes: int, signal_slots: int = 1 << 14, group=None,
+                           nvls_bytes: int = 0):
+        """IPC team over the current torch.distributed group (one GPU per rank).
+        nvls_bytes > 0 also tries to create the NVLS multicast region (enable_nvls)."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         team = cls(world, heap_bytes=heap_bytes, signal_slots=signal_slots, ipc_rank=rank,
@@ -154,7 +196,69 @@ class Team:
         _lib.call("tf_team_export_handle", team.handle, blob, HANDLE_BLOB)
         allb = exchange_handles(bytes(blob), group)
         _lib.call("tf_team_open_peers", team.handle, C.c_char_p(allb), HANDLE_BLOB)
+        if nvls_bytes > 0:
+            team.enable_nvls(nvls_bytes, group)
         return team
+
+    # ------------------------------------------------------------------ NVLS
+    @staticmethod
+    def nvls_supported(device: int) -> bool:
+        ok = C.c_int()
+        _lib.call("tf_nvls_supported", int(device), C.byref(ok))
+        return bool(ok.value)
+
+    def enable_nvls(self, nbytes: int, group=None) -> bool:
+        """Create the team's NVLS multicast region (multimem_ld_reduce / multimem_st
+        in the switch, tf_nvls.cu).  Returns False -- and the team keeps its P2P
+        paths -- when the devices do not support multicast or the driver refuses
+        the object (e.g. a single-GPU lease).  IPC teams call it on every rank."""
+        if self.rank is None:
+            if not self.distinct_devices or self.world < 2:
+                return False
+            fd = C.c_int(-1)
+            rc = _lib.lib().tf_team_nvls_create(self.handle, int(nbytes), C.byref(fd))
+            return rc == 0
+        import os
+
+        import torch.distributed as dist
+        ok = [None] * self.world
+        dist.all_gather_object(ok, self.nvls_supported(self.devices[self.rank]) and self.world > 1,
+                               group=group)
+        if not all(ok):
+            return False
+        fd = C.c_int(-1)
+        status = [0]
+        if self.rank == 0:
+            status[0] = _lib.lib().tf_team_nvls_create(self.handle, int(nbytes), C.byref(fd))
+        dist.broadcast_object_list(status, src=0, group=group)
+        if status[0] != 0:
+            return False
+        got = share_fd(fd.value if self.rank == 0 else None, group)
+        rc = 0
+        if self.rank != 0:
+            rc = _lib.lib().tf_team_nvls_import(self.handle, int(nbytes), int(got))
+            os.close(got)
+        rc = rc or _lib.lib().tf_team_nvls_add_device(self.handle)
+        rcs = [None] * self.world
+        dist.all_gather_object(rcs, rc, group=group)
+        if any(rcs):
+            return False
+        _lib.call("tf_team_nvls_bind", self.handle)
+        dist.barrier(group)
+        if self.rank == 0:
+            os.close(fd.value)
+        return True
+
+    @property
+    def nvls_enabled(self) -> bool:
+        en = C.c_int()
+        _lib.call("tf_nvls_enabled", self.handle, C.byref(en), None)
+        return bool(en.value)
+
+    def nvls_ptr(self, pe: int, offset: int) -> tuple[int, int]:
+        uc, mc = C.c_void_p(), C.c_void_p()
+        _lib.call("tf_nvls_ptr", self.handle, int(pe), int(offset), C.byref(uc), C.byref(mc))
+        return int(uc.value or 0), int(mc.value or 0)
 
     @property
     def distinct_devices(self) -> bool:
@@ -221,6 +325,18 @@ class SymmetricHeap:
             raise ProtocolError(f"mismatched collective allocation sizes: {sizes}")
         return self.alloc(sizes[0])
 
+    def alloc_multimem(self, nbytes: int, align: int = 16) -> SymmHandle:
+        """Symmetric allocation in the team's NVLS multicast region (Team.enable_nvls):
+        multimem_ld_reduce / multimem_st on it run as multimem instructions reduced
+        and replicated in the NVSwitch.  Falls back to the P2P heap when NVLS is off."""
+        if nbytes < 0:
+            raise ValueError("allocation size must be >= 0")
+        if not self.team.nvls_enabled:
+            return self.alloc(nbytes, max(align, 16))
+        off = C.c_uint64()
+        _lib.call("tf_nvls_alloc", self.team.handle, int(nbytes), int(align), C.byref(off))
+        return SymmHandle(offset=int(off.value), nbytes=int(nbytes), space="nvls")
+
     def alloc_signals(self, nslots: int) -> SigHandle:
         if nslots < 0:
             raise ValueError("signal slot count must be >= 0")
@@ -243,6 +359,8 @@ class SymmetricHeap:
         dev = self.team.devices[pe] if self.team.rank is None else self.team.devices[self.team.rank]
         if nbytes == 0:
             raw = torch.empty(0, dtype=torch.uint8, device=f"cuda:{dev}")
+        elif handle.space == "nvls":
+            raw = tensor_from_ptr(self.team.nvls_ptr(pe, handle.offset + offset)[0], nbytes, dev)
         else:
             raw = tensor_from_ptr(self.team.heap_ptr(pe, handle.offset + offset), nbytes, dev)
         isz = torch.empty(0, dtype=tdtype).element_size()
@@ -414,8 +532,9 @@ class SymmetricHeap:
         _check_range(handle, offset, count * isz)
         dev = self._pe_device(pe)
         out = torch.empty(int(count), dtype=tdt, device=f"cuda:{dev}")
+        fn = "tf_nvls_reduce" if handle.space == "nvls" else "tf_team_reduce"
         with torch.cuda.device(dev):
-            _lib.call("tf_team_reduce", self.team.handle, int(pe), handle.offset + int(offset),
+            _lib.call(fn, self.team.handle, int(pe), handle.offset + int(offset),
                       self._RED_CODES[tdt], int(count), out.data_ptr(), _stream_ptr(stream))
         return out
 
@@ -426,8 +545,9 @@ class SymmetricHeap:
         v = v.contiguous().to(f"cuda:{dev}")
         nbytes = v.numel() * v.element_size()
         _check_range(handle, offset, nbytes)
+        fn = "tf_nvls_broadcast" if handle.space == "nvls" else "tf_team_broadcast"
         with torch.cuda.device(dev):
-            _lib.call("tf_team_broadcast", self.team.handle, int(pe), handle.offset + int(offset),
+            _lib.call(fn, self.team.handle, int(pe), handle.offset + int(offset),
                       v.data_ptr(), nbytes, _stream_ptr(stream))
         if stream is None:
             torch.cuda.synchronize(dev)  # v may be a temporary

@@ -2,6 +2,7 @@
 header declares, and its host-side tile tables equal the reference fixtures."""
 
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -76,3 +77,18 @@ def test_c_tile_map_validation_errors():
         _lib.call("tf_tile_map", 8, 0, 4, 3, 2, 0, buf, 8)    # world % nnodes
     with pytest.raises(ValueError):
         _lib.call("tf_tile_map", 8, 4, 4, 1, 2, 0, buf, 8)    # rank out of range
+
+
+def test_sass_has_blackwell_and_multimem_instructions():
+    """The built library carries tcgen05 MMAs, TMA, and the NVLS multimem loads
+    (LDGMC = multimem.ld_reduce; multimem.st lowers to a STG.*.STRONG.SYS on the
+    multicast address, so it has no mnemonic of its own)."""
+    import shutil
+    import subprocess
+    from paper_2605_02953_b200 import _lib
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    for op in ("UTCHMMA", "UTMALDG", "LDGMC.E.HPADD.BF16", "LDGMC.E.ADD.F32"):
+        assert op in sass, op

@@ -112,3 +112,39 @@ def test_reference_arm_rank_gating():
     line = json.loads(r0.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["unit"] == "TFLOP/s"
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _fd_worker(rank, world, port, q):
+    """share_fd (the NVLS handle transport): rank 0's pipe read end reaches every
+    rank over SCM_RIGHTS, and each rank reads rank 0's bytes through its copy."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_02953_b200.shmem import share_fd
+        r_fd = w_fd = None
+        if rank == 0:
+            r_fd, w_fd = os.pipe()
+            os.write(w_fd, b"x" * (world - 1))
+        got = share_fd(r_fd)
+        ok = True
+        if rank != 0:
+            ok = os.read(got, 1) == b"x" and got != r_fd
+            os.close(got)
+        dist.barrier()
+        if rank == 0:
+            os.close(r_fd)
+            os.close(w_fd)
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_share_fd_over_unix_socket(world):
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_fd_worker, args=(world, port, q), nprocs=world, join=True, start_method="spawn")
+    res = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(ok for _, ok in res), res
