@@ -44,6 +44,7 @@ __device__ __forceinline__ uint32_t desc_lo_k(uint32_t addr) { return ((addr & 0
 
 
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
+constexpr bool kDefaultMulticast = false;  // 4-CTA multicast clusters (TF_GEMM_MC overrides)
 #ifndef TF_GEMM_LAG
 #define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
 #endif
@@ -84,6 +85,7 @@ struct KParams {
   int trace_cap;
   int trace_rank;
   int hint_a, hint_b;                 // L2 policy of the A / B TMA loads (l2_policy kinds)
+  int ksnake;                         // odd waves walk K backwards (L2 reuse across waves)
   // Grouped (MoE) mode, ag_moe.py:120-142: work item -> (slot, pid_n), slot record
   // {expert, first gathered row, rows, seg_start | seg_end << 16}; B is the stacked
   // [E * moe_n, K] expert weights.  Tiles acquire-wait the arrival counters of the
@@ -149,8 +151,8 @@ struct TileGeo {
   int row0, row_lim, b_row0;
   int seg;  // grouped: seg_start | seg_end << 16
 };
-template <bool GROUPED, int TILE_M, int BN>
-__device__ __forceinline__ TileGeo tile_geo(const KParams& p, int step) {
+template <bool GROUPED, int TILE_M, int BN, int NPAIR = 1>
+__device__ __forceinline__ TileGeo tile_geo(const KParams& p, int step, int pair = 0) {
   TileGeo g;
   if constexpr (GROUPED) {
     // the reference's step -> (slot, pid_n) split, ag_moe.py:123-124
@@ -163,7 +165,9 @@ __device__ __forceinline__ TileGeo tile_geo(const KParams& p, int step) {
     g.b_row0 = t.x * p.moe_n + g.pid_n * BN;
     g.seg = t.w;
   } else {
+    // NPAIR = 2: a work item is a pair of adjacent N tiles (one per CTA pair of the cluster)
     tile_coords(p, step, g.pid_m, g.pid_n);
+    g.pid_n = g.pid_n * NPAIR + pair;
     g.row0 = g.pid_m * TILE_M;
     g.row_lim = p.m;
     g.b_row0 = g.pid_n * BN;
@@ -335,7 +339,7 @@ __device__ void moe_pull_engine(const KParams& p, uint8_t* smem) {
   }
 }
 
-template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false>
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false, int NPAIR = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       const __grid_constant__ CUtensorMap tmap_b,
@@ -366,15 +370,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // NPAIR = 2: a 4-CTA cluster = two CTA pairs computing adjacent N tiles of the same
+  // rows; each CTA TMA-loads half of its pair's A rows and multicasts them to the
+  // matching CTA of the other pair, so A crosses L2 -> SM once per cluster.
   const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0;
-  const bool leader = cta_rank == 0;
-  const int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / CG;
-  const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / CG;
+  const uint32_t prank = cta_rank & 1;              // rank inside the CTA pair
+  const int pair = static_cast<int>(cta_rank >> 1); // which pair of the cluster
+  const bool leader = prank == 0;
+  constexpr int kCluster = CG * NPAIR;
+  const int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / kCluster;
+  const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / kCluster;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], NPAIR);  // freed once every pair's MMAs read the stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -408,10 +418,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int work = cluster_id; work < p.total_work; work += num_clusters) {
         int step, kb0, kb1, slot;
         decode_work(p, work, step, kb0, kb1, slot);
-        const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+        const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
         const int pid_m = geo.pid_m, pid_n = geo.pid_n;
         const int tile_m0 = geo.row0;
-        const int n0 = geo.b_row0 + S::kBRows * cta_rank;    // this CTA's B rows
+        const int n0 = geo.b_row0 + S::kBRows * prank;    // this CTA's B rows
         if constexpr (GROUPED) {
           // wait(arrival, segment_start, segment_end) acquire -- ag_moe.py:131-132
           if (p.src_flags) {
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               waited = true;
             }
             if (waited) {
-              trace_rec(p, 1, pid_m * p.num_pid_n + pid_n, tw0, globaltimer_ns(),
+              trace_rec(p, 1, pid_m * p.num_pid_n * NPAIR + pid_n, tw0, globaltimer_ns(),
                         (static_cast<unsigned long long>(s0) << 32) | static_cast<unsigned>(s1 - s0 + 1));
               fence_proxy_async_global();
             }
@@ -438,10 +448,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int h = 0; h < MH; ++h) {
             // rows of the gathered operand this CTA loads: A blocks, or its B rows
-            const int m0 = p.wait_on_b ? n0 : tile_m0 + block_row<CG>(h, cta_rank);
+            const int m0 = p.wait_on_b ? n0 : tile_m0 + block_row<CG>(h, prank);
             const int lim = p.wait_on_b ? p.n : p.m;
             const int span = p.wait_on_b ? S::kBRows : 128;
-            if (m0 >= lim || (p.wait_on_b && h > 0)) continue;
+            if (m0 >= lim || (p.wait_on_b && h > 0) || (NPAIR == 2 && h != pair)) continue;
             const int r1 = min(m0 + span, lim) - 1;
             const int c_beg = static_cast<int>(m0 / p.rows_per_chunk);
             const int c_end = static_cast<int>(r1 / p.rows_per_chunk);
@@ -457,27 +467,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // wait(arrival, rank_beg, num_slots) as in the reference trace
             if (this_wait)
-              trace_rec(p, 1, pid_m * p.num_pid_n + pid_n, tw0, globaltimer_ns(),
+              trace_rec(p, 1, pid_m * p.num_pid_n * NPAIR + pid_n, tw0, globaltimer_ns(),
                         (static_cast<unsigned long long>(c_beg) << 32) |
                             static_cast<unsigned>(c_end - c_beg + 1));
           }
           // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
           if (waited) fence_proxy_async_global();
         }
-        for (int kb = kb0; kb < kb1; ++kb) {
+        // K direction: odd waves run backwards so a wave starts on the k-slices the
+        // previous wave touched last (still in L2); the MMA side is order-agnostic
+        const bool krev = p.ksnake && (((work - cluster_id) / num_clusters) & 1);
+        for (int kq = kb0; kq < kb1; ++kq) {
+          const int kb = krev ? kb1 - 1 - (kq - kb0) : kq;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem_a + stage * S::kABytes;
           uint8_t* sb = smem_b + stage * S::kBBytes;
-          if constexpr (CG == 2) {
+          if constexpr (NPAIR == 2) {
+            // both CTAs of the pair receive both A blocks (one from each pair) + own B
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            const uint16_t amask = static_cast<uint16_t>((1u << prank) | (1u << (2 + prank)));
+            tma_load_2d_pair_mc(sa + pair * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
+                                tile_m0 + block_row<CG>(pair, prank), amask);
+            tma_load_2d_pair(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
+          } else if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
 #pragma unroll
             for (int h = 0; h < MH; ++h) {
               if (p.hint_a)
                 tma_load_2d_pair_hint(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
-                                      tile_m0 + block_row<CG>(h, cta_rank), pol_a);
+                                      tile_m0 + block_row<CG>(h, prank), pol_a);
               else
                 tma_load_2d_pair(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
-                                 tile_m0 + block_row<CG>(h, cta_rank));
+                                 tile_m0 + block_row<CG>(h, prank));
             }
             if (p.hint_b) tma_load_2d_pair_hint(sb, &tmap_b, &full_bar[stage], kb * BK, n0, pol_b);
             else tma_load_2d_pair(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
@@ -486,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int h = 0; h < MH; ++h)
               tma_load_2d(sa + h * S::kABlock, &tmap_a, &full_bar[stage], kb * BK,
-                          tile_m0 + block_row<CG>(h, cta_rank));
+                          tile_m0 + block_row<CG>(h, prank));
             tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           }
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
@@ -516,8 +537,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           else umma_bf16(tmem_base + h * BN, ad, bd, idesc, (kb | kk) != 0);
         }
       };
+      // smem stages are released to every CTA whose producer writes them (both pairs
+      // with NPAIR = 2); accumulator-ready goes to this pair's two CTAs only
+      constexpr uint16_t kEmptyMask = NPAIR == 2 ? 0xF : 0x3;
+      const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pair));
       auto release = [&](uint64_t* bar) {
-        if constexpr (CG == 2) umma_commit_pair_mc(bar, 0x3);
+        if constexpr (CG == 2) umma_commit_pair_mc(bar, kEmptyMask);
+        else umma_commit(bar);
+      };
+      auto release_acc = [&](uint64_t* bar) {
+        if constexpr (CG == 2) umma_commit_pair_mc(bar, pair_mask);
         else umma_commit(bar);
       };
       for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
@@ -559,18 +588,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) {
-          release(&tfull_bar[0]);  // half 0 complete: its epilogue can start
+          release_acc(&tfull_bar[0]);  // half 0 complete: its epilogue can start
           if (lagged)
             for (int j = nkb - L; j < nkb; ++j) {
               const int st = (s0 + j) % S::kStages;
               issue(st, 1, j);
               release(&empty_bar[st]);
             }
-          release(&tfull_bar[1]);
+          release_acc(&tfull_bar[1]);
           if (p.trace) {
-            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
             const int pm = tg.pid_m, pn = tg.pid_n;
-            trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
+            trace_rec(p, 2, pm * p.num_pid_n * NPAIR + pn, tm0, globaltimer_ns(),
                       (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
           }
         }
@@ -609,19 +638,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             // smem slot free (in both CTAs) once these MMAs retire
-            if constexpr (CG == 2) umma_commit_pair_mc(&empty_bar[stage], 0x3);
+            if constexpr (CG == 2) umma_commit_pair_mc(&empty_bar[stage], NPAIR == 2 ? 0xF : 0x3);
             else umma_commit(&empty_bar[stage]);
           }
           __syncwarp();
           if (++stage == S::kStages) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) {  // accumulator ready for the epilogues
-          if constexpr (CG == 2) umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+          if constexpr (CG == 2) umma_commit_pair_mc(&tfull_bar[acc], static_cast<uint16_t>(0x3u << (2 * pair)));
           else umma_commit(&tfull_bar[acc]);
           if (p.trace) {
-            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+            const TileGeo tg = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
             const int pm = tg.pid_m, pn = tg.pid_n;
-            trace_rec(p, 2, pm * p.num_pid_n + pn, tm0, globaltimer_ns(),
+            trace_rec(p, 2, pm * p.num_pid_n * NPAIR + pn, tm0, globaltimer_ns(),
                       (static_cast<unsigned long long>(pm) << 32) | static_cast<unsigned>(pn));
           }
         }
@@ -633,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;          // TMEM lanes [32*quarter, 32*quarter+32)
     const int row_in_blk = quarter * 32 + lane;
     const uint32_t tempty_leader =
-        CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : smem_u32(&tempty_bar[0]);
+        CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 2 * pair) : smem_u32(&tempty_bar[0]);
     // TMA-store staging: this warp's two 32x128 B buffers (128-byte swizzled)
     uint8_t* epi_buf = smem_epi + (warp - kEpiWarp0) * 2 * S::kEpiBuf;
     int epi_slot = 0;
@@ -643,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
       int step, kb0, kb1, slot;
       decode_work(p, work, step, kb0, kb1, slot);
-      const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN>(p, step);
+      const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
       const int pid_m = geo.pid_m, pid_n = geo.pid_n;
       const int acc = local % ACC;
       const uint32_t acc_phase = (local / ACC) & 1;
@@ -661,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (p.trace && warp == kEpiWarp0 && lane == 0 && (MH == 1 || h == MH - 1))
-          trace_rec(p, 3, pid_m * p.num_pid_n + pid_n, epi_t0, globaltimer_ns(),
+          trace_rec(p, 3, pid_m * p.num_pid_n * NPAIR + pid_n, epi_t0, globaltimer_ns(),
                     (static_cast<unsigned long long>(pid_m) << 32) | static_cast<unsigned>(pid_n));
         const int b = MH == 2 ? h : acc;
         if (lane == 0) {
@@ -674,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int h = 0; h < MH; ++h) {
           if (MH == 2 || h == 0) wait_full(h);
-          const int prow0 = slot * S::kTileM + block_row<CG>(h, cta_rank) + quarter * 32;
+          const int prow0 = (slot * NPAIR + pair) * S::kTileM + block_row<CG>(h, prank) + quarter * 32;
           const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                  acc * S::kAccCols + h * BN;
 #pragma unroll 1
@@ -707,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int h = 0; h < MH; ++h) {
           if (MH == 2 || h == 0) wait_full(h);
-          const int wrow0 = geo.row0 + block_row<CG>(h, cta_rank) + quarter * 32;
+          const int wrow0 = geo.row0 + block_row<CG>(h, prank) + quarter * 32;
           const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
                                  acc * S::kAccCols + h * BN;
           // grouped tiles end at their expert's last row: a band that crosses it is
@@ -781,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int h = 0; h < MH; ++h) {
         if (MH == 2 || h == 0) wait_full(h);
-        const int row0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank);
+        const int row0 = pid_m * S::kTileM + block_row<CG>(h, prank);
         const int row = row0 + row_in_blk;
         const bool row_ok = row < p.m;
         uint8_t* dst_row = nullptr;
@@ -900,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == kEpiWarp0 * 32) {
 #pragma unroll 1
           for (int h = 0; h < MH; ++h) {
-            const int row0 = pid_m * S::kTileM + block_row<CG>(h, cta_rank);
+            const int row0 = pid_m * S::kTileM + block_row<CG>(h, prank);
             if (row0 >= p.m) continue;
             const int r1 = min(row0 + 128, p.m) - 1;
             const int o0 = static_cast<int>(row0 / p.rows_per_rank);
@@ -926,15 +955,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Split-K tail fix-up: tile i of the tail = sum over parts j (in order) of
 // workspace slots i*split_s + j, converted and stored to C.  One CTA per
 // (tail tile, 32-row band); 256 threads cover 256 columns... of BN.
-template <int TILE_M, int BN, bool OUT_F32>
+template <int TILE_M, int BN, bool OUT_F32, int NPAIR = 1>
 __global__ void __launch_bounds__(256) tail_fixup_kernel(const float* __restrict__ ws,
                                                          const __grid_constant__ KParams p) {
-  // one CTA per (tail tile, 32-row band), one thread per column of the tile
+  // one CTA per (tail tile, 32-row band), one thread per column of the tile; with
+  // NPAIR = 2 a tail work item holds two N tiles (pair q writes slot unit*2 + q)
   const int bands = TILE_M / 32;
   const int i = blockIdx.x / bands;
   const int band = blockIdx.x % bands;
+  const int item = i / NPAIR, q = i % NPAIR;
   int pid_m, pid_n;
-  tile_coords(p, p.tail_base + i, pid_m, pid_n);
+  tile_coords(p, p.tail_base + item, pid_m, pid_n);
+  pid_n = pid_n * NPAIR + q;
   const int c = pid_n * BN + threadIdx.x;
   for (int r = 0; r < 32; ++r) {
     const int lrow = band * 32 + r;
@@ -942,7 +974,8 @@ __global__ void __launch_bounds__(256) tail_fixup_kernel(const float* __restrict
     if (row >= p.m) break;
     float acc = 0.f;
     for (int j = 0; j < p.split_s; ++j)  // fixed order: deterministic
-      acc += ws[(static_cast<long long>(i * p.split_s + j) * TILE_M + lrow) * BN + threadIdx.x];
+      acc += ws[(static_cast<long long>((item * p.split_s + j) * NPAIR + q) * TILE_M + lrow) * BN +
+                threadIdx.x];
     if (c < p.n) {
       if constexpr (OUT_F32)
         static_cast<float*>(p.c)[static_cast<long long>(row) * p.ldc + c] = acc;
@@ -1008,18 +1041,43 @@ int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
   return TF_OK;
 }
 
-template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false>
+template <int CG, int MH, int BN, bool OUT_F32, int EPI, bool AG_WAIT, bool GROUPED = false, int NPAIR = 1>
 int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
              const CUtensorMap& tp, const KParams& kp, int grid, cudaStream_t stream,
              const float* tail_ws) {
-  auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT, GROUPED>;
+  auto kern = gemm_sm100_kernel<CG, MH, BN, OUT_F32, EPI, AG_WAIT, GROUPED, NPAIR>;
   using S = Smem<CG, MH, BN>;
   static uint64_t attr_done = 0;  // per template instance, bit per device
+  static int max_clusters[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_done & (1ull << dev))) {
     TF_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal));
+    if (NPAIR > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr_done |= 1ull << dev;
+  }
+  if (NPAIR > 1 && dev < 64) {
+    // a persistent grid must not exceed the co-resident 4-CTA clusters (GPC packing)
+    if (!max_clusters[dev]) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(grid);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = S::kTotal;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = CG * NPAIR;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, kern, &q) != cudaSuccess || mc < 1) mc = 1 << 20;
+      cudaGetLastError();
+      max_clusters[dev] = mc;
+      if (getenv("TF_GEMM_DEBUG")) fprintf(stderr, "[tf] max active %d-CTA clusters: %d\n", CG * NPAIR, mc);
+    }
+    const int cap = max_clusters[dev] * CG * NPAIR + kp.comm_ctas;
+    if (grid > cap) grid = cap;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1028,35 +1086,35 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CG * NPAIR;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tp, kp));
   if (kp.split_s > 1) {
-    const int tail_tiles = (kp.total_work - kp.tail_base) / kp.split_s;
-    tail_fixup_kernel<S::kTileM, BN, OUT_F32>
+    const int tail_tiles = (kp.total_work - kp.tail_base) / kp.split_s * NPAIR;
+    tail_fixup_kernel<S::kTileM, BN, OUT_F32, NPAIR>
         <<<tail_tiles * (S::kTileM / 32), BN, 0, stream>>>(tail_ws, kp);
     TF_CUDA_TRY(cudaGetLastError());
   }
   return TF_OK;
 }
 
-template <int CG, int MH, int BN>
+template <int CG, int MH, int BN, int NPAIR = 1>
 int dispatch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                 const CUtensorMap& tp, const KParams& kp, int grid, const GemmLaunch& g,
                 cudaStream_t s, const float* ws) {
   const bool ag = g.chunk_flags != nullptr;
   if (g.epilogue == 0) {
     if (g.out_f32)
-      return ag ? launch_t<CG, MH, BN, true, 0, true>(ta, tb, tc, tp, kp, grid, s, ws)
-                : launch_t<CG, MH, BN, true, 0, false>(ta, tb, tc, tp, kp, grid, s, ws);
-    return ag ? launch_t<CG, MH, BN, false, 0, true>(ta, tb, tc, tp, kp, grid, s, ws)
-              : launch_t<CG, MH, BN, false, 0, false>(ta, tb, tc, tp, kp, grid, s, ws);
+      return ag ? launch_t<CG, MH, BN, true, 0, true, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws)
+                : launch_t<CG, MH, BN, true, 0, false, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws);
+    return ag ? launch_t<CG, MH, BN, false, 0, true, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws)
+              : launch_t<CG, MH, BN, false, 0, false, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws);
   }
-  if (g.out_f32) return launch_t<CG, MH, BN, true, 1, false>(ta, tb, tc, tp, kp, grid, s, ws);
-  return launch_t<CG, MH, BN, false, 1, false>(ta, tb, tc, tp, kp, grid, s, ws);
+  if (g.out_f32) return launch_t<CG, MH, BN, true, 1, false, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws);
+  return launch_t<CG, MH, BN, false, 1, false, false, NPAIR>(ta, tb, tc, tp, kp, grid, s, ws);
 }
 
 // Per-(device, stream) fp32 workspace for split-K tail partials (grown on demand).
@@ -1218,6 +1276,8 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     }
     kp.hint_a = ha;
     kp.hint_b = hb;
+    const char* ks = getenv("TF_GEMM_KSNAKE");
+    kp.ksnake = ks ? atoi(ks) : 0;
   }
   {
     std::lock_guard<std::mutex> lock(g_trace_mu);
@@ -1252,12 +1312,21 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     kp.tma_store = 1;
   }
 
+  // 4-CTA clusters (two CTA pairs sharing A through TMA multicast) for the 512x256
+  // pair tile when N splits into tile pairs; TF_GEMM_MC=0 keeps 2-CTA clusters
+  int npair = 1;
+  {
+    const char* mc = getenv("TF_GEMM_MC");
+    const bool want = mc ? atoi(mc) != 0 : kDefaultMulticast;
+    if (want && mh == 2 && kp.num_pid_n % 2 == 0 && !g.wait_on_b && !g.tile_map_n) npair = 2;
+  }
+  kp.num_pid_n /= npair;  // work items are N-tile pairs
   const int tiles = kp.num_pid_m * kp.num_pid_n;
   int ctas = g.num_sms > 0 ? g.num_sms : num_sms_of_current_device();
-  int clusters = ctas / cg;
+  int clusters = ctas / (cg * npair);
   if (clusters < 1) clusters = 1;
   if (clusters > tiles) clusters = tiles;
-  const int grid = clusters * cg;
+  const int grid = clusters * cg * npair;
   // Split-K tail: when the last wave is at most half full, cut its tiles into
   // K-ranges so every cluster gets work (wave quantization on 148 SMs).
   kp.tail_base = tiles;
@@ -1275,10 +1344,10 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
         !g.wait_on_b &&
         !getenv("TF_DEBUG_NO_SPLITK")) {
       const int tile_m_rows = tile_m;
-      const size_t bytes = static_cast<size_t>(rem) * split * tile_m_rows * g.block_n * 4;
+      const size_t bytes = static_cast<size_t>(rem) * split * npair * tile_m_rows * g.block_n * 4;
       tail_ws = tail_workspace(stream, bytes);
       if (tail_ws) {
-        rc = make_tmap_2d(&tp, tail_ws, static_cast<int64_t>(rem) * split * tile_m_rows,
+        rc = make_tmap_2d(&tp, tail_ws, static_cast<int64_t>(rem) * split * npair * tile_m_rows,
                           g.block_n, g.block_n, 32, 4, 32);
         if (rc) return rc;
         kp.tail_base = tiles - rem;
@@ -1287,6 +1356,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
       }
     }
   }
+  if (mh == 2 && npair == 2) return dispatch_bn<2, 2, 256, 2>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
   if (mh == 2) return dispatch_bn<2, 2, 256>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);
   if (cg == 2) {
     if (g.block_n == 256) return dispatch_bn<2, 1, 256>(ta, tb, tc, tp, kp, grid, g, stream, tail_ws);

@@ -222,6 +222,16 @@ __device__ __forceinline__ void tma_load_2d_pair_hint(void* smem_dst, const void
       "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c_inner), "r"(c_outer), "l"(policy)
       : "memory");
 }
+// 2-CTA TMA load multicast to the CTAs of `mask` (same smem offset in each); each
+// destination's bytes are counted on its pair leader's mbarrier.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* smem_dst, const void* tmap, uint64_t* bar,
+                                                    int32_t c_inner, int32_t c_outer, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c_inner), "r"(c_outer), "h"(mask)
+      : "memory");
+}
 // L2 eviction-priority policy for TMA loads: 1 evict_first, 2 evict_last, 3 evict_normal
 __device__ __forceinline__ uint64_t l2_policy(int kind) {
   uint64_t pol = 0;
