@@ -86,6 +86,7 @@ struct KParams {
   int trace_rank;
   int hint_a, hint_b;                 // L2 policy of the A / B TMA loads (l2_policy kinds)
   int ksnake;                         // odd waves walk K backwards (L2 reuse across waves)
+  int chunks_per_rank;                // AG flags per source rank (trace payload in rank slots)
   // Grouped (MoE) mode, ag_moe.py:120-142: work item -> (slot, pid_n), slot record
   // {expert, first gathered row, rows, seg_start | seg_end << 16}; B is the stacked
   // [E * moe_n, K] expert weights.  Tiles acquire-wait the arrival counters of the
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      uint32_t ready_mask = 0;  // AllGather chunks already observed as arrived
+      uint64_t ready_mask = 0;  // AllGather chunks already observed as arrived
       const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
       for (int work = cluster_id; work < p.total_work; work += num_clusters) {
         int step, kb0, kb1, slot;
@@ -429,10 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const unsigned long long tw0 = p.trace ? globaltimer_ns() : 0;
             bool waited = false;
             for (int sr = s0; sr <= s1; ++sr) {
-              if (ready_mask & (1u << sr)) continue;
+              if (ready_mask & (1ull << sr)) continue;
               wait_geq_sys(p.src_flags + sr, p.src_target, p.timeout_ns, p.err,
                            0x1000000ull | static_cast<unsigned long long>(sr));
-              ready_mask |= 1u << sr;
+              ready_mask |= 1ull << sr;
               waited = true;
             }
             if (waited) {
@@ -458,18 +459,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const unsigned long long tw0 = p.trace ? globaltimer_ns() : 0;
             bool this_wait = false;
             for (int c = c_beg; c <= c_end; ++c) {
-              if (ready_mask & (1u << c)) continue;
+              if (ready_mask & (1ull << c)) continue;
               wait_geq_sys(p.chunk_flags + c, p.epoch, p.timeout_ns, p.err,
                            0x1000000ull | static_cast<unsigned long long>(c));
-              ready_mask |= 1u << c;
+              ready_mask |= 1ull << c;
               waited = true;
               this_wait = true;
             }
-            // wait(arrival, rank_beg, num_slots) as in the reference trace
-            if (this_wait)
+            // wait(arrival, rank_beg, num_slots) as in the reference trace (rank slots)
+            if (this_wait) {
+              const int cpr = p.chunks_per_rank > 0 ? p.chunks_per_rank : 1;
               trace_rec(p, 1, pid_m * p.num_pid_n * NPAIR + pid_n, tw0, globaltimer_ns(),
-                        (static_cast<unsigned long long>(c_beg) << 32) |
-                            static_cast<unsigned>(c_end - c_beg + 1));
+                        (static_cast<unsigned long long>(c_beg / cpr) << 32) |
+                            static_cast<unsigned>(c_end / cpr - c_beg / cpr + 1));
+            }
           }
           // generic-proxy acquire -> async-proxy (TMA) reads of the same bytes
           if (waited) fence_proxy_async_global();
@@ -1226,8 +1229,8 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     return fail(TF_ERR_INVALID, "GEMM dimension exceeds int32");
   if (g.epilogue == 1 && (g.world < 1 || g.world > kMaxWorld || g.rows_per_rank <= 0))
     return fail(TF_ERR_INVALID, "scatter epilogue needs 1 <= world <= TF_MAX_WORLD");
-  if (g.chunk_flags && (g.wait_on_b ? g.n : g.m) / g.rows_per_chunk + 1 > 32)
-    return fail(TF_ERR_CONFIG, "AllGather wait supports at most 32 chunks");
+  if (g.chunk_flags && ((g.wait_on_b ? g.n : g.m) + g.rows_per_chunk - 1) / g.rows_per_chunk > 64)
+    return fail(TF_ERR_CONFIG, "AllGather wait supports at most 64 chunks");
   if (g.group_m < 1) return fail(TF_ERR_CONFIG, "group_m must be >= 1");
 
   KParams kp{};
@@ -1278,6 +1281,7 @@ int launch_gemm(const GemmLaunch& g, cudaStream_t stream) {
     kp.hint_b = hb;
     const char* ks = getenv("TF_GEMM_KSNAKE");
     kp.ksnake = ks ? atoi(ks) : 0;
+    kp.chunks_per_rank = g.chunks_per_rank;
   }
   {
     std::lock_guard<std::mutex> lock(g_trace_mu);

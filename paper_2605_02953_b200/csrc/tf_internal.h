@@ -44,6 +44,7 @@ struct GemmLaunch {
   const uint64_t* chunk_flags = nullptr;
   uint64_t epoch = 0;
   int64_t rows_per_chunk = 0;
+  int chunks_per_rank = 1;           // flags per source rank (sub-chunked pulls)
   // ReduceScatter producer (scatter epilogue)
   int rank = 0, world = 1;
   int64_t rows_per_rank = 0;

@@ -25,6 +25,7 @@
 //   peer's next increment.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -399,8 +400,24 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     return tf::launch_gemm(g, static_cast<cudaStream_t>(stream));
   }
   const size_t chunk_bytes = static_cast<size_t>(mpr) * args->k * 2;
+  // Each peer chunk is pulled as `sub` row slices with their own flags, so the first
+  // wave of tiles waits for the first slice of a chunk, not the whole chunk (a TP8
+  // chunk of config 2 is 16.8 MB: ~22 us at 770 GB/s).  Slices are whole 128-row
+  // blocks; at most 64 flags per parity.
+  constexpr int kMaxSub = 4;
+  int sub = 1;
+  for (int c = kMaxSub; c > 1; c /= 2)
+    if (mpr % (128 * c) == 0 && w * c <= 64) { sub = c; break; }
+  if (const char* e = getenv("TF_AG_SUBCHUNKS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= kMaxSub && mpr % v == 0 && w * v <= 64) sub = v;
+  }
+  const int fstride = w * kMaxSub;  // flags per call parity
+  const int64_t rows_sub = mpr / sub;
+  const size_t sub_bytes = chunk_bytes / sub;
+  const int nflags = w * sub;
   const std::string key = "ag:" + std::to_string(args->m) + "x" + std::to_string(args->k);
-  tf::Workspace* ws = t->workspace(key, 2 * chunk_bytes * w, 2 * w, &rc);
+  tf::Workspace* ws = t->workspace(key, 2 * chunk_bytes * w, 2 * fstride, &rc);
   if (!ws) return rc;
   auto s = static_cast<cudaStream_t>(stream);
   auto cs = comm_stream ? static_cast<cudaStream_t>(comm_stream) : s;
@@ -412,8 +429,10 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     const int64_t lda = args->lda ? args->lda : args->k;
     TF_CUDA_TRY(cudaMemcpy2DAsync(own + rank * chunk_bytes, args->k * 2, args->a, lda * 2,
                                   args->k * 2, mpr, cudaMemcpyDefault, s));
-    rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + rank, e, s);
-    if (rc) return rc;
+    for (int j = 0; j < sub; ++j) {
+      rc = tf::stream_signal_set(t, rank, ws->sig_base + par * fstride + rank * sub + j, e, s);
+      if (rc) return rc;
+    }
     rc = tf::team_barrier_arrive(t, rank, s);
     if (rc) return rc;
   }
@@ -428,19 +447,23 @@ int tf_ag_gemm(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     if (rc) return rc;
     for (int i = 1; i < w; ++i) {
       const int src = (rank + i) % w;  // pull order of ag_gemm.py:64-69
-      TF_CUDA_TRY(cudaMemcpyAsync(own + src * chunk_bytes,
-                                  t->pes[src].base + buf_off + src * chunk_bytes, chunk_bytes,
-                                  cudaMemcpyDefault, cs));
-      rc = tf::stream_signal_set(t, rank, ws->sig_base + par * w + src, e, cs);
-      if (rc) return rc;
+      for (int j = 0; j < sub; ++j) {
+        const size_t off = src * chunk_bytes + j * sub_bytes;
+        TF_CUDA_TRY(cudaMemcpyAsync(own + off, t->pes[src].base + buf_off + off, sub_bytes,
+                                    cudaMemcpyDefault, cs));
+        rc = tf::stream_signal_set(t, rank, ws->sig_base + par * fstride + src * sub + j, e, cs);
+        if (rc) return rc;
+      }
     }
+    (void)nflags;
     tf::GemmLaunch g = tf::base_launch(args);
     g.a = own;
     g.lda = args->k;
     g.num_sms = tf::gemm_grid(args);
-    g.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
+    g.chunk_flags = t->pes[rank].sig + ws->sig_base + par * fstride;
     g.epoch = e;
-    g.rows_per_chunk = mpr;
+    g.rows_per_chunk = rows_sub;
+    g.chunks_per_rank = sub;
     g.trace_rank = rank;
     g.err = t->err_word(rank);
     g.timeout_ns = t->timeout_ns;
