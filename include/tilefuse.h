@@ -183,6 +183,8 @@ typedef struct tf_gemm_args {
   int32_t fuse_scatter;/* gemm_rs only; 1 = epilogue stores into owners' slots */
   int32_t reduce_order;/* TF_REDUCE_* */
   const int32_t* tile_map; /* optional device [ceil(m/block_m)] table; NULL = identity */
+  int32_t nnodes;      /* gemm_rs unfused: nodes of the topology (0/1 = one node) */
+  int32_t ring_links;  /* gemm_rs unfused: 1 = assume_full_mesh_links=False (ring order in a node) */
 } tf_gemm_args;
 
 int tf_gemm(const tf_gemm_args* args, void* stream);

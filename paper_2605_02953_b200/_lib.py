@@ -34,6 +34,7 @@ class GemmArgs(C.Structure):
         ("out_dtype", i32), ("block_m", i32), ("block_n", i32), ("block_k", i32),
         ("group_m", i32), ("num_gemm_sms", i32), ("num_comm_sms", i32), ("swizzle", i32),
         ("fuse_scatter", i32), ("reduce_order", i32), ("tile_map", vp),
+        ("nnodes", i32), ("ring_links", i32),
     ]
 
 

@@ -937,7 +937,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int r1 = min(row0 + 128, p.m) - 1;
             const int o0 = static_cast<int>(row0 / p.rows_per_rank);
             const int o1 = static_cast<int>(r1 / p.rows_per_rank);
-            for (int o = o0; o <= o1; ++o) red_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
+            for (int o = o0; o <= o1; ++o) {
+              if (p.trace) {
+                // traced: the fetch-add's old value records which bump this was (the
+                // reference's atomic_add signal event, gemm_rs.py:155-161)
+                const unsigned long long t0 = globaltimer_ns();  // <= the add's visibility
+                const unsigned long long old = atom_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
+                trace_push(p.trace, p.trace_cap, 4, p.trace_rank, row0 / 128, t0, globaltimer_ns(),
+                           (static_cast<unsigned long long>(o) << 32) | static_cast<unsigned>(old + 1));
+              } else {
+                red_add_release_sys(p.peer_counts[o] + row0 / 128, 1);
+              }
+            }
           }
         }
       }
@@ -1149,6 +1160,17 @@ std::mutex g_trace_mu;
 std::map<int, TraceBuf> g_trace;
 
 }  // namespace
+
+int trace_buffer(int device, unsigned long long** buf) {
+  std::lock_guard<std::mutex> lock(g_trace_mu);
+  auto it = g_trace.find(device);
+  if (it == g_trace.end() || !it->second.buf) {
+    *buf = nullptr;
+    return 0;
+  }
+  *buf = it->second.buf;
+  return static_cast<int>(it->second.cap);
+}
 
 int num_sms_of_current_device() {
   int dev = 0, n = 0;

@@ -75,5 +75,7 @@ struct GemmLaunch {
 int launch_gemm(const GemmLaunch& g, cudaStream_t stream);
 void layer_release_team(const tf_team* t);
 int num_sms_of_current_device();
+// device trace ring of `device` (tf_trace_enable) and its capacity, or 0 / nullptr
+int trace_buffer(int device, unsigned long long** buf);
 
 }  // namespace tf

@@ -47,18 +47,26 @@ struct ReduceSrc {
 // sources in `order` in fp32 with 16-byte vector loads.
 template <bool IN_F32>
 __global__ void __launch_bounds__(256) rs_reduce_kernel(
-    ReduceSrc srcs, long long src_ld, int world, int order_ring, int owner, void* out,
+    ReduceSrc srcs, long long src_ld, int world, int nnodes, int intra_ring, int inter_ring, int owner, void* out,
     long long out_ld, int out_f32, int out_vec, long long rows, long long n, long long row0_global,
     const uint64_t* counters, unsigned long long expected, int first_tile, int ntiles,
-    int col_chunks, unsigned long long timeout_ns, unsigned long long* err) {
+    int col_chunks, unsigned long long timeout_ns, unsigned long long* err,
+    unsigned long long* trace, int trace_cap) {
   const int items = ntiles * col_chunks;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int t = item / col_chunks;
     const int cc = item - t * col_chunks;
     const int pid_m = first_tile + t;
     if (counters) {
-      if (threadIdx.x == 0)
+      if (threadIdx.x == 0) {
         wait_geq_sys(counters + pid_m, expected, timeout_ns, err, 0x4000000ull | pid_m);
+        if (trace) {  // the row block's "segment ready" moment, seen by its owner
+          const unsigned long long now = globaltimer_ns();
+          trace_push(trace, trace_cap, 5, owner, pid_m, now, now,
+                     (static_cast<unsigned long long>(owner) << 32) |
+                         static_cast<unsigned>(ld_relaxed_sys(counters + pid_m)));
+        }
+      }
       __syncthreads();
     }
     // rows of this owner covered by global row tile pid_m
@@ -72,37 +80,50 @@ __global__ void __launch_bounds__(256) rs_reduce_kernel(
     for (long long v = threadIdx.x; v < total; v += blockDim.x) {
       const long long r = g0 - row0_global + v / vec_per_row;
       const long long c = c0 + (v % vec_per_row) * 8;
-      float acc[8];
+      // The reference's summation tree (gemm_rs.py:199-319): node partials are left
+      // folds over the node's ranks in the intra-node order (reduce_visit_order, or the
+      // neighbour ring when links are not a full mesh), then a left fold of the node
+      // partials in the inter-node order.  One node: a flat fold.
+      float acc[8], part[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = 0.f;
       const bool full = c + 8 <= n;
-      for (int i = 0; i < world; ++i) {
-        const int s = order_ring ? (owner + 1 + i) % world : i;
-        if constexpr (IN_F32) {
-          const float* p = static_cast<const float*>(srcs.src[s]) + r * src_ld + c;
-          if (full) {
-            const float4 x0 = *reinterpret_cast<const float4*>(p);
-            const float4 x1 = *reinterpret_cast<const float4*>(p + 4);
-            acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
-            acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
-          } else {
-            for (int j = 0; j < 8 && c + j < n; ++j) acc[j] += p[j];
-          }
-        } else {
-          const uint16_t* p = static_cast<const uint16_t*>(srcs.src[s]) + r * src_ld + c;
-          if (full) {
-            const uint4 x = *reinterpret_cast<const uint4*>(p);
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+      const int lws = world / nnodes;
+      const int onode = owner / lws, olocal = owner % lws;
+      for (int a = 0; a < nnodes; ++a) {
+        const int nd = inter_ring ? (onode + 1 + a) % nnodes : a;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              acc[2 * j] += __uint_as_float(w[j] << 16);
-              acc[2 * j + 1] += __uint_as_float(w[j] & 0xFFFF0000u);
+        for (int j = 0; j < 8; ++j) part[j] = 0.f;
+        for (int b = 0; b < lws; ++b) {
+          const int s = nd * lws + (intra_ring ? (olocal + 1 + b) % lws : b);
+          if constexpr (IN_F32) {
+            const float* p = static_cast<const float*>(srcs.src[s]) + r * src_ld + c;
+            if (full) {
+              const float4 x0 = *reinterpret_cast<const float4*>(p);
+              const float4 x1 = *reinterpret_cast<const float4*>(p + 4);
+              part[0] += x0.x; part[1] += x0.y; part[2] += x0.z; part[3] += x0.w;
+              part[4] += x1.x; part[5] += x1.y; part[6] += x1.z; part[7] += x1.w;
+            } else {
+              for (int j = 0; j < 8 && c + j < n; ++j) part[j] += p[j];
             }
           } else {
-            for (int j = 0; j < 8 && c + j < n; ++j)
-              acc[j] += __uint_as_float(static_cast<uint32_t>(p[j]) << 16);
+            const uint16_t* p = static_cast<const uint16_t*>(srcs.src[s]) + r * src_ld + c;
+            if (full) {
+              const uint4 x = *reinterpret_cast<const uint4*>(p);
+              const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                part[2 * j] += __uint_as_float(w[j] << 16);
+                part[2 * j + 1] += __uint_as_float(w[j] & 0xFFFF0000u);
+              }
+            } else {
+              for (int j = 0; j < 8 && c + j < n; ++j)
+                part[j] += __uint_as_float(static_cast<uint32_t>(p[j]) << 16);
+            }
           }
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += part[j];
       }
       if (out_f32) {
         float* o = static_cast<float*>(out) + r * out_ld + c;
@@ -537,16 +558,26 @@ int tf_gemm_rs(tf_team* t, int rank, const tf_gemm_args* args, int phase, void* 
     const uint64_t* cnt = t->pes[rank].sig + ws->sig_base;
     const int out_vec = ((static_cast<int64_t>(ldc) * esz) % 16 == 0) &&
                         (reinterpret_cast<uintptr_t>(args->c) % 16 == 0);
+    // summation tree: fused = one flat fold over the world (_fused_reducer); unfused =
+    // the hierarchical reducer with the neighbour ring inside a node when the links are
+    // not a full mesh (_hier_reducer / _scatter_ring)
+    const int ring = args->reduce_order == TF_REDUCE_RING;
+    const int nn = (!fused && args->nnodes > 1 && w % args->nnodes == 0) ? args->nnodes : 1;
+    const int intra = (!fused && args->ring_links && w / nn > 1) ? 1 : ring;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned long long* tr = nullptr;
+    const int tcap = tf::trace_buffer(dev, &tr);
     if (f32)
       tf::rs_reduce_kernel<true><<<grid, 256, 0, rs>>>(
-          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 1, out_vec, mpr, n,
+          srcs, ld, w, nn, intra, ring, rank, args->c, ldc, 1, out_vec, mpr, n,
           rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
-          t->timeout_ns, t->err_word(rank));
+          t->timeout_ns, t->err_word(rank), tr, tcap);
     else
       tf::rs_reduce_kernel<false><<<grid, 256, 0, rs>>>(
-          srcs, ld, w, args->reduce_order == TF_REDUCE_RING, rank, args->c, ldc, 0, out_vec, mpr, n,
+          srcs, ld, w, nn, intra, ring, rank, args->c, ldc, 0, out_vec, mpr, n,
           rank * mpr, cnt, expected, static_cast<int>(first_tile), ntiles, col_chunks,
-          t->timeout_ns, t->err_word(rank));
+          t->timeout_ns, t->err_word(rank), tr, tcap);
     TF_CUDA_TRY(cudaGetLastError());
     // owner resets its counters once consumed (gemm_rs.py:168-174)
     TF_CUDA_TRY(cudaMemsetAsync(t->pes[rank].sig + ws->sig_base, 0, num_pid_m * sizeof(uint64_t), rs));

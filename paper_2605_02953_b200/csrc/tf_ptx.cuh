@@ -345,6 +345,22 @@ __device__ __forceinline__ bool wait_eq_sys(const uint64_t* p, uint64_t want, ui
   return true;
 }
 
+// Device trace record (tf_trace_enable ring: [count, pad x3][cap][4] u64):
+// kind|rank|cta|tile, t_start, t_end, payload (%globaltimer ns).
+__device__ __forceinline__ void trace_push(unsigned long long* ring, int cap, unsigned kind, int rank,
+                                           int tile, unsigned long long t0, unsigned long long t1,
+                                           unsigned long long payload) {
+  if (!ring) return;
+  const unsigned long long i = atomicAdd(ring, 1ull);
+  if (i >= static_cast<unsigned long long>(cap)) return;
+  unsigned long long* e = ring + 4 + i * 4;
+  e[0] = (static_cast<unsigned long long>(kind) << 56) | (static_cast<unsigned long long>(rank & 0xFF) << 48) |
+         (static_cast<unsigned long long>(blockIdx.x & 0xFFFF) << 32) | static_cast<unsigned>(tile);
+  e[1] = t0;
+  e[2] = t1;
+  e[3] = payload;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(lo), "f"(hi));

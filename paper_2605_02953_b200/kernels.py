@@ -158,6 +158,17 @@ def tile_map_tensor(m: int, rank: int, world: int, nnodes: int, mode: str, devic
     return torch.from_numpy(host).to(device)
 
 
+def _tile_map_or_none(m: int, rank: int, world: int, nnodes: int, mode: str, device, block_m: int):
+    """The swizzle only orders tiles (results do not depend on it): when the hardware
+    tile is too coarse for the node ranges of a multi-node topology (e.g. 16 rows on
+    2 nodes with 128-row tiles) the identity order is used."""
+    from .errors import ProtocolError
+    try:
+        return tile_map_tensor(m, rank, world, nnodes, mode, device, block_m)
+    except ProtocolError:
+        return None
+
+
 def tile_map_host(m: int, rank: int, world: int, nnodes: int, block_m: int, mode: str) -> np.ndarray:
     tiles = (m + block_m - 1) // block_m
     buf = (C.c_int32 * max(tiles, 1))()
@@ -268,7 +279,7 @@ def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     for r in range(world):
         dev = devices[r]
         out = torch.empty((m, n_per_rank), dtype=odt, device=f"cuda:{dev}")
-        tm = (tile_map_tensor(m, r, world, topo.nnodes, "ag_gemm", f"cuda:{dev}", ctx.hw_block_m)
+        tm = (_tile_map_or_none(m, r, world, topo.nnodes, "ag_gemm", f"cuda:{dev}", ctx.hw_block_m)
               if ctx.swizzle else None)
         a = pa.tensors[r]
         args[r] = _args(a, pb.tensors[r], out, m, n_per_rank, kp, out_dtype=odt,
@@ -291,8 +302,11 @@ def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
             assume_full_mesh_links: bool = True) -> WorkloadRun:
     """Per rank r: rows r of sum_w(input_w @ weight_w.T), shape [M_per_rank, N].
 
-    `assume_full_mesh_links` is accepted for API parity: NVSwitch gives every
-    GPU full bandwidth to every peer, so the ring fallback is never needed."""
+    The unfused reduction follows the reference's summation tree
+    (gemm_rs.py:199-319): per node a fold in reduce_visit_order -- or, with
+    `assume_full_mesh_links=False`, the neighbour-ring order of _scatter_ring --
+    then a fold of the node partials.  On NVSwitch every peer is one hop, so the
+    data still moves as one pull per peer; only the arithmetic order changes."""
     topo = ctx.topology
     world = topo.world_size
     if len(input_shards) != world or len(weight_shards) != world:
@@ -323,13 +337,15 @@ def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
     for r in range(world):
         dev = devices[r]
         out = torch.empty((mpr, n), dtype=odt, device=f"cuda:{dev}")
-        tm = (tile_map_tensor(m, r, world, topo.nnodes, "gemm_rs", f"cuda:{dev}", ctx.hw_block_m)
+        tm = (_tile_map_or_none(m, r, world, topo.nnodes, "gemm_rs", f"cuda:{dev}", ctx.hw_block_m)
               if ctx.swizzle else None)
         args[r] = _args(px.tensors[r], pw.tensors[r], out, m, n, kp, out_dtype=odt,
                         block_n=ctx.hw_block_n, group_m=ctx.group_m,
                         num_gemm_sms=ctx.num_gemm_sms, num_comm_sms=ctx.num_comm_sms,
                         swizzle=ctx.swizzle, tile_map=tm, fuse_scatter=ctx.fuse_scatter,
                         reduce_order=ctx.reduce_order, block_m=ctx.hw_block_m)
+        args[r].nnodes = int(topo.nnodes)
+        args[r].ring_links = 0 if assume_full_mesh_links else 1
         outs.append(out)
         keep.append(tm)
     if mpr > 0 and n > 0:

@@ -9,7 +9,9 @@ waits on both chunks, gather order starts at the local chunk) can be checked
 against the real kernels, and `export_chrome_trace` writes the same JSON.
 
 Kinds: "wait" (name wait_chunks: slot = first chunk, num_slots), "compute"
-(name gemm_tile: MMA issue window of a tile), "store" (name epilogue).
+(name gemm_tile: MMA issue window of a tile), "store" (name epilogue), "signal"
+(name atomic_add: a GEMM-RS producer bumped owner `pe`'s row-block counter `slot`
+to `value`; name segment_ready: owner `pe` saw counter `slot` complete).
 Times are seconds relative to the first event.
 """
 
@@ -23,7 +25,8 @@ import numpy as np
 
 from . import _lib
 
-_KINDS = {1: ("wait", "wait_chunks"), 2: ("compute", "gemm_tile"), 3: ("store", "epilogue")}
+_KINDS = {1: ("wait", "wait_chunks"), 2: ("compute", "gemm_tile"), 3: ("store", "epilogue"),
+          4: ("signal", "atomic_add"), 5: ("signal", "segment_ready")}
 
 
 @dataclass(frozen=True)
@@ -71,6 +74,10 @@ def collect(device: int = 0, capacity: int = 1 << 20) -> Trace:
         tile = int(w0) & 0xFFFFFFFF
         if kind == "wait":
             payload = {"name": name, "tile": tile, "slot": int(pl) >> 32, "num_slots": int(pl) & 0xFFFFFFFF}
+        elif kind == "signal":
+            # RS row-block counter: bump by producer `rank` (value = count after it), or the
+            # owner observing it complete (gemm_rs.py:155-161 atomic_add / segment_ready)
+            payload = {"name": name, "slot": tile, "pe": int(pl) >> 32, "value": int(pl) & 0xFFFFFFFF}
         else:
             payload = {"name": name, "tile": tile, "pid_m": int(pl) >> 32, "pid_n": int(pl) & 0xFFFFFFFF}
         events.append(TraceEvent(rank, f"cta{cta}", cta, kind, (int(ts) - t0) * 1e-9,

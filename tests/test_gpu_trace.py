@@ -27,14 +27,24 @@ def _ctx(world, **kw):
 
 
 def _traced(fn):
+    """Run fn with device tracing on every GPU (ranks may sit on different devices)
+    and merge the rings."""
     from paper_2605_02953_b200 import trace as T
-    T.enable(0)
+    devs = range(torch.cuda.device_count())
+    for d in devs:
+        T.enable(d)
     try:
         out = fn()
-        torch.cuda.synchronize()
-        return out, T.collect(0)
+        for d in devs:
+            torch.cuda.synchronize(d)
+        events = []
+        for d in devs:
+            events += T.collect(d).events
+        events.sort(key=lambda e: (e.t_start, e.rank, e.worker_id))
+        return out, T.Trace(events)
     finally:
-        T.disable(0)
+        for d in devs:
+            T.disable(d)
 
 
 def test_straddling_tiles_wait_on_both_chunks():
@@ -83,3 +93,36 @@ def test_compute_events_cover_every_tile_and_chrome_schema(tmp_path):
     T.export_chrome_trace(tr, path)
     events = json.loads(path.read_text())
     assert events and {"name", "cat", "ph", "ts", "dur", "pid", "tid", "args"} <= set(events[0])
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_gemm_rs_counter_protocol_fires_on_fourth_tile(fuse):
+    """ovs tests/test_kernels.py:164-191 on the real kernels: 2 row tiles x 2 column
+    tiles feed each owner row block (world 2, 128-row blocks, block_n 128); the
+    counter reaches exactly 4 through bumps 1, 2, 3, 4, and the owner's reduce sees
+    the block ready no earlier than the 4th bump (%globaltimer)."""
+    from oracle import collectives as O
+    from paper_2605_02953_b200.kernels import gemm_rs
+    rng = np.random.default_rng(6)
+    world = 2
+    m, n, k = world * 256, 256, 64
+    inp = [rng.integers(-8, 8, (m, k)) for _ in range(world)]
+    w = [rng.integers(-8, 8, (n, k)) for _ in range(world)]
+    run, tr = _traced(lambda: gemm_rs(inp, w, _ctx(world, fuse_scatter=fuse, num_gemm_sms=4)))
+    for got, want in zip(run.outputs, O.ref_reduce_scatter(inp, w)):
+        assert np.array_equal(got, want)
+    sig = tr.by_kind("signal")
+    bumps, ready = {}, {}
+    for e in sig:
+        key = (e.payload["pe"], e.payload["slot"])
+        if e.payload["name"] == "atomic_add":
+            bumps.setdefault(key, []).append((e.t_start, e.payload["value"]))
+        else:
+            ready.setdefault(key, []).append((e.t_start, e.payload["value"]))
+    blocks = {(r, b) for r in range(world) for b in range(r * 2, r * 2 + 2)}
+    assert set(bumps) == blocks and set(ready) == blocks
+    for key, hist in bumps.items():
+        assert sorted(v for _, v in hist) == [1, 2, 3, 4], key
+        fourth = max(t for t, v in hist if v == 4)
+        assert all(t >= fourth for t, _ in ready[key]), key
+        assert all(v == 4 for _, v in ready[key]), key
