@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--only-layer", action="store_true")
     p.add_argument("--only-attn", action="store_true")
     p.add_argument("--only-agmoe", action="store_true")
+    p.add_argument("--only-moe", action="store_true")
     return p.parse_args()
 
 
@@ -302,8 +303,7 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
             if i >= warmup:
                 flush.zero_()
                 ev[i - warmup][0].record(stream)
-            idx, w = M.moe_route(logits, MOE_K, stream=stream)
-            recv = ep.dispatch(x, idx)
+            recv, idx, w = ep.route_dispatch(x, logits)  # top-k fused into the dispatch launch
             if i >= warmup:
                 ev[i - warmup][1].record(stream)
             if i == 0:
@@ -874,6 +874,13 @@ def main_ours(args):
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
         print(json.dumps(bench_ag_moe(0, 1, 0, args.steps, args.warmup, flush, torch.cuda.Stream(), False,
                                       load_peaks()[0])), flush=True)
+        return
+    if args.only_moe:  # probe: config 4 dispatch/combine only
+        torch.cuda.set_device(0)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda:0")
+        team = Team(1, [0], heap_bytes=2 * MOE_T * MOE_K * MOE_H * 2 + (64 << 20), signal_slots=4096)
+        print(json.dumps(bench_moe(team, 0, 1, 0, args.steps, args.warmup, flush, torch.cuda.Stream(), False,
+                                   load_peaks()[0])), flush=True)
         return
     if args.only_layer:  # probe: config 5 only
         torch.cuda.set_device(0)

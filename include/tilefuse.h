@@ -323,12 +323,17 @@ typedef struct tf_moe_args {
   int32_t* sorted_pos;    /* [T, k] device: from tf_moe_count */
   int32_t* dest_row;      /* [T, k] device: receive row of (t, j) on its owner (filled by dispatch) */
   int64_t* recv_rows;     /* [1] device: rows received by this rank (filled by dispatch) */
+  const float* logits;    /* optional [T, E] fp32 router logits: dispatch computes the top-k
+                             itself (ties -> lower expert) into topk_idx / topk_w */
 } tf_moe_args;
 
 /* Device pointers of this rank's receive buffer [max_recv, H] bf16 and expert
  * output buffer [max_recv, H] bf16 inside the symmetric heap. */
 int tf_moe_buffers(tf_team* t, int rank, const tf_moe_args* a, void** recv, void** expert_out);
-/* Dispatch (EP all-to-all):
+/* Dispatch (EP all-to-all).  When the caller passes PRE|MAIN in one call (one
+ * rank per GPU), both run as ONE persistent launch (routing, counts, count
+ * exchange, layout and scatter, with a grid-wide wait in between); PRE and MAIN
+ * called separately (several ranks sharing a GPU) are one launch each.
  *   PRE  = routing counts + send order of this rank (as tf_moe_count, into
  *          a->sorted_pos), count row pushed to every peer's matrix + flag;
  *   MAIN = wait for all rows, copy the full matrix to a->counts, compute

@@ -42,7 +42,7 @@ class MoeArgs(C.Structure):
     _fields_ = [
         ("tokens", i64), ("hidden", i64), ("k", i32), ("n_experts", i32), ("max_recv", i64),
         ("x", vp), ("topk_idx", vp), ("topk_w", vp), ("out", vp), ("counts", vp),
-        ("sorted_pos", vp), ("dest_row", vp), ("recv_rows", vp),
+        ("sorted_pos", vp), ("dest_row", vp), ("recv_rows", vp), ("logits", vp),
     ]
 
 

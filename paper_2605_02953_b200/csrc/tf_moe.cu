@@ -56,18 +56,15 @@ __device__ __forceinline__ float key2f(uint32_t k) {
 // ties); a round is two warp reductions on the integer pipe (`redux.sync`: max
 // key, then min expert id among lanes holding it), so picks are identical to a
 // stable sort by (-logit, expert id).
+// Lane j < k returns slot j's (expert, weight) of the token whose logits are `row`.
 template <int VPL>  // logits per lane (E <= 32 * VPL)
-__global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, int E, int k,
-                            int32_t* __restrict__ idx, float* __restrict__ w) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (t >= tokens) return;
-  const float* row = logits + t * E;
+__device__ __forceinline__ void topk_warp(const float* __restrict__ row, int E, int k, int lane,
+                                          int& out_idx, float& out_w) {
   uint32_t key[VPL];
 #pragma unroll
   for (int c = 0; c < VPL; ++c) {  // coalesced: lane + 32c
     const int e = lane + 32 * c;
-    key[c] = e < E ? f2key(__ldg(row + e)) : 0u;
+    key[c] = e < E ? f2key(row[e]) : 0u;
   }
   auto lane_best = [&](uint32_t& bk, uint32_t& bi) {
     bk = key[0];
@@ -95,9 +92,22 @@ __global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, in
     z += ez;
     if (lane == r) { my_val = ez; my_idx = static_cast<int>(wi); }
   }
+  out_idx = my_idx;
+  out_w = my_val / z;
+}
+
+template <int VPL>
+__global__ void topk_kernel(const float* __restrict__ logits, int64_t tokens, int E, int k,
+                            int32_t* __restrict__ idx, float* __restrict__ w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= tokens) return;
+  int my_idx;
+  float my_w;
+  topk_warp<VPL>(logits + t * E, E, k, lane, my_idx, my_w);
   if (lane < k) {
     idx[t * k + lane] = my_idx;
-    w[t * k + lane] = my_val / z;
+    w[t * k + lane] = my_w;
   }
 }
 
@@ -530,6 +540,373 @@ __global__ void release_kernel(PeerSig flags, int world, int rank, uint64_t epoc
   }
 }
 
+// ---------------------------------------------------------------- fused dispatch
+// One persistent launch per rank replaces topk + count + push + wait + layout +
+// scatter + release: CTA c owns tokens [c*tpc, (c+1)*tpc).
+//   PRE   (top-k of its tokens when logits are given) -> stable per-expert ranks of
+//         its (token, slot) entries in token order -> chunk histogram published
+//         with a release flag -> grid-wide wait -> totals, expert bases and this
+//         chunk's offsets (same arithmetic as count_fused_kernel, so send positions
+//         are bit-identical) -> CTA 0 pushes the count row to every peer's matrix.
+//   MAIN  wait for every source's count row -> destination segment bases
+//         (layout_kernel's arithmetic) -> double-buffered scatter of its own tokens
+//         (bulk copy in, bulk stores to local rows, 16-byte P2P stores to peers) ->
+//         the last CTA to finish releases "source `rank` delivered" on every owner.
+// The first row pieces are already loading while PRE runs (x does not depend on
+// the routing).  All CTAs must be co-resident (grid <= SMs x occupancy).
+constexpr int kFdWarps = 12;
+constexpr int kFdBuf = 8192;            // bytes per row piece buffer (two per warp)
+constexpr int kFdEntCap = 1024;         // (token, slot) entries per CTA
+constexpr int kFdDoneSlot = 1023;       // gflags[1023]: CTAs done scattering (grid <= 1023)
+
+struct FusedDispatch {
+  const uint4* x;
+  const float* logits;                  // nullptr: routing given in idx
+  int64_t tokens, vec_per_row, max_recv;
+  int k, E, world, rank, tpc, mode;     // mode: bit 0 PRE, bit 1 MAIN
+  int32_t* idx;
+  float* w;
+  int32_t* sorted_pos;
+  int32_t* dest_row;
+  int32_t* ebase;                       // [E] expert bases of the send order
+  int32_t* seg_base;                    // [E]
+  int32_t* counts_out;                  // [world][E]
+  int64_t* recv_rows;
+  int32_t* mat;                         // this rank's [world][E] count matrix
+  PeerPtrs mats, recv;
+  PeerSig count_flags, deliver_flags;
+  const uint64_t* own_count_flags;      // [world] on this rank
+  unsigned long long epoch;             // MoE call epoch
+  int32_t* chunk_hist;                  // [grid][E]
+  unsigned long long* gflags;           // [grid] barrier flags, then the done counter
+  unsigned long long gepoch;
+  unsigned long long* err;
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const unsigned long long* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// chunk histograms are stored with the expert stride rounded up to 4 (16-byte rows)
+__host__ __device__ __forceinline__ int fd_stride(int E) { return (E + 3) & ~3; }
+
+// wc [nw][E] and the cross-chunk partial sums [2][4 * blockDim] share one region
+__host__ __device__ __forceinline__ int fd_wc_ints(int E) {
+  return kFdWarps * E > 8 * 32 * kFdWarps ? kFdWarps * E : 8 * 32 * kFdWarps;
+}
+
+size_t fused_dispatch_smem(int E) {
+  return static_cast<size_t>(2) * kFdWarps * kFdBuf +
+         (static_cast<size_t>(fd_wc_ints(E)) + 4 * static_cast<size_t>(E) + 2 * kFdEntCap) * 4;
+}
+
+template <int VPL>  // VPL 0: routing given
+__global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const FusedDispatch p) {
+  extern __shared__ __align__(128) uint8_t fsm_raw[];
+  __shared__ uint64_t bars[2 * kFdWarps];
+  __shared__ uint4* sdst[kFdWarps][16];
+  __shared__ int32_t last_tot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kFdWarps;
+  const int E = p.E, k = p.k, G = gridDim.x, c = blockIdx.x;
+  uint8_t* bufs = fsm_raw;                                     // [nw][2][kFdBuf]
+  int32_t* wc = reinterpret_cast<int32_t*>(fsm_raw + 2 * nw * kFdBuf);  // [nw][E]
+  int32_t* cnt = wc + fd_wc_ints(E);                           // [E]
+  int32_t* tot = cnt + E;                                      // [E]
+  int32_t* off = tot + E;                                      // [E]
+  int32_t* seg = off + E;                                      // [E]
+  int32_t* idx_s = seg + E;                                    // [kFdEntCap]
+  int32_t* pos_s = idx_s + kFdEntCap;                          // [kFdEntCap] rank inside the expert's send segment
+  int32_t* part = wc;                                          // [2][4 * blockDim] cross-chunk partial sums (after wc)
+  const int Ep = fd_stride(E);
+  const int64_t t0 = static_cast<int64_t>(c) * p.tpc;
+  const int64_t t_end = t0 + p.tpc < p.tokens ? t0 + p.tpc : p.tokens;
+  const int nt = t_end > t0 ? static_cast<int>(t_end - t0) : 0;
+  const int ent = nt * k;
+  const int epr = E / p.world;
+  constexpr int64_t kPiece = kFdBuf / 16;
+  const int64_t npieces = (p.vec_per_row + kPiece - 1) / kPiece;
+  const int ntasks = static_cast<int>(nt * npieces);
+  if (lane == 0) {
+    mbar_init(&bars[2 * warp], 1);
+    mbar_init(&bars[2 * warp + 1], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  auto piece_bytes = [&](int ti) {
+    const int64_t v0 = (ti % npieces) * kPiece;
+    return static_cast<uint32_t>((min(v0 + kPiece, p.vec_per_row) - v0) * 16);
+  };
+  auto issue_load = [&](int ti, int b) {  // lane 0 only
+    const int64_t t = t0 + ti / npieces, v0 = (ti % npieces) * kPiece;
+    const uint32_t bytes = piece_bytes(ti);
+    mbar_arrive_expect_tx(&bars[2 * warp + b], bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(bufs + (2 * warp + b) * kFdBuf)),
+        "l"(p.x + t * p.vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bars[2 * warp + b]))
+        : "memory");
+  };
+  if ((p.mode & 2) && lane == 0 && warp < ntasks) issue_load(warp, 0);  // prefetch under PRE
+  uint32_t ph1 = 0;  // parity of buffer 1's barrier
+
+  if (p.mode & 1) {
+    // ---- routing of this CTA's tokens
+    if constexpr (VPL > 0) {
+      // this warp's tokens tt = warp + j*nw: their logits rows come in with one bulk
+      // copy each (one DRAM latency per round, not per token) into the warp's second
+      // row buffer, which the scatter does not use before its second task
+      const uint32_t rb = static_cast<uint32_t>(E) * 4;
+      const bool bulk = (rb % 16) == 0 && (reinterpret_cast<uintptr_t>(p.logits) % 16) == 0;
+      const int per_round = bulk ? static_cast<int>(kFdBuf / rb) : 1;
+      const float* lbuf = reinterpret_cast<const float*>(bufs + (2 * warp + 1) * kFdBuf);
+      for (int j0 = 0; warp + j0 * nw < nt; j0 += per_round) {
+        const int nr = min(per_round, (nt - warp + nw - 1) / nw - j0);
+        if (bulk) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&bars[2 * warp + 1], rb * nr);
+            for (int j = 0; j < nr; ++j)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      smem_u32(lbuf) + j * rb),
+                  "l"(p.logits + (t0 + warp + (j0 + j) * nw) * E), "r"(rb), "r"(smem_u32(&bars[2 * warp + 1]))
+                  : "memory");
+          }
+          mbar_wait(&bars[2 * warp + 1], ph1);
+          ph1 ^= 1;
+        }
+        for (int j = 0; j < nr; ++j) {
+          const int tt = warp + (j0 + j) * nw;
+          int my_idx;
+          float my_w;
+          topk_warp<VPL>(bulk ? lbuf + j * E : p.logits + (t0 + tt) * E, E, k, lane, my_idx, my_w);
+          if (lane < k) {
+            idx_s[tt * k + lane] = my_idx;
+            p.idx[(t0 + tt) * k + lane] = my_idx;
+            p.w[(t0 + tt) * k + lane] = my_w;
+          }
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int i = tid; i < ent; i += blockDim.x) idx_s[i] = p.idx[t0 * k + i];
+    }
+    for (int x = tid; x < E; x += blockDim.x) cnt[x] = 0;
+    // ---- stable ranks: entries in token order, blockDim at a time
+    for (int base = 0; base < ent; base += blockDim.x) {
+      for (int i = tid; i < nw * E; i += blockDim.x) wc[i] = 0;
+      __syncthreads();
+      const int i = base + tid;
+      int e = i < ent ? idx_s[i] : -1;
+      if (e >= E || e < -1) {
+        if (p.err) atomicCAS(p.err, 0ull, 0x5300000ull | static_cast<unsigned>(i & 0xFFFFF));
+        e = -1;
+      }
+      const unsigned same = __match_any_sync(0xffffffffu, e);
+      const int in_warp = __popc(same & ((1u << lane) - 1));
+      if (e >= 0 && in_warp == 0) wc[warp * E + e] = __popc(same);
+      __syncthreads();
+      for (int x = tid; x < E; x += blockDim.x) {
+        int32_t run = cnt[x];
+#pragma unroll
+        for (int ww = 0; ww < nw; ++ww) {
+          const int32_t v = wc[ww * E + x];
+          wc[ww * E + x] = run;
+          run += v;
+        }
+        cnt[x] = run;
+      }
+      __syncthreads();
+      if (i < ent) pos_s[i] = e >= 0 ? wc[warp * E + e] + in_warp : -1;
+      __syncthreads();
+    }
+    __syncthreads();
+    // ---- publish the chunk histogram, wait for every chunk
+    for (int x = tid; x < Ep; x += blockDim.x) p.chunk_hist[static_cast<int64_t>(c) * Ep + x] = x < E ? cnt[x] : 0;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
+    }
+    for (int x = tid; x < G; x += blockDim.x) {
+      if (ld_acquire_gpu(p.gflags + x) >= p.gepoch) continue;
+      const uint64_t ts = globaltimer_ns();
+      while (ld_acquire_gpu(p.gflags + x) < p.gepoch) {
+        if (globaltimer_ns() - ts > p.timeout_ns) {
+          if (p.err) atomicCAS(p.err, 0ull, 0x5400000ull | static_cast<unsigned>(x));
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- totals and this chunk's offsets: thread = (4-expert quad, chunk group), one
+    // 16-byte load per chunk, all chunk groups' loads independent
+    {
+      const int quads = Ep / 4;
+      const int groups = max(1, static_cast<int>(blockDim.x) / quads);
+      int4* part_t = reinterpret_cast<int4*>(part);
+      int4* part_o = reinterpret_cast<int4*>(part + 4 * blockDim.x);
+      for (int i = tid; i < quads * groups; i += blockDim.x) {
+        const int q = i % quads, g = i / quads;
+        int4 t = make_int4(0, 0, 0, 0), o = make_int4(0, 0, 0, 0);
+        const int4* col = reinterpret_cast<const int4*>(p.chunk_hist) + q;
+#pragma unroll 16
+        for (int cc = g; cc < G; cc += groups) {
+          const int4 v = __ldcg(col + static_cast<int64_t>(cc) * quads);
+          t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+          if (cc < c) { o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w; }
+        }
+        part_t[g * quads + q] = t;
+        part_o[g * quads + q] = o;
+      }
+      __syncthreads();
+      for (int x = tid; x < E; x += blockDim.x) {
+        int32_t t = 0, o = 0;
+        for (int g = 0; g < groups; ++g) {
+          t += part[4 * (g * quads) + x];
+          o += part[4 * blockDim.x + 4 * (g * quads) + x];
+        }
+        tot[x] = t;
+        off[x] = o;
+        cnt[x] = t;  // this rank's count row (tot becomes the expert bases below)
+      }
+    }
+    __syncthreads();
+    block_exclusive_scan(tot, E);  // ends with __syncthreads
+    if (c == 0)
+      for (int x = tid; x < E; x += blockDim.x) {
+        p.ebase[x] = tot[x];
+        p.mat[static_cast<int64_t>(p.rank) * E + x] = cnt[x];
+      }
+    for (int i = tid; i < ent; i += blockDim.x) {
+      if (pos_s[i] < 0) continue;
+      const int e = idx_s[i];
+      pos_s[i] += off[e];
+      p.sorted_pos[t0 * k + i] = tot[e] + pos_s[i];
+    }
+    if (c == 0 && p.world > 1) {  // count row -> every peer's matrix, then its flag
+      for (int q = 0; q < p.world; ++q) {
+        int32_t* dst = static_cast<int32_t*>(p.mats.p[q]) + static_cast<int64_t>(p.rank) * E;
+        for (int x = tid; x < E; x += blockDim.x) dst[x] = cnt[x];
+      }
+      __syncthreads();
+      if (tid < p.world) {
+        fence_sys();
+        st_release_sys(p.count_flags.p[tid] + p.rank, p.epoch);
+      }
+    }
+    __syncthreads();
+  } else {
+    // MAIN only: the PRE launch left idx / sorted_pos / ebase in global memory
+    for (int x = tid; x < E; x += blockDim.x) tot[x] = __ldcg(p.ebase + x);
+    __syncthreads();
+    for (int i = tid; i < ent; i += blockDim.x) {
+      const int e = __ldcg(p.idx + t0 * k + i);
+      idx_s[i] = e;
+      pos_s[i] = (e >= 0 && e < E) ? __ldcg(p.sorted_pos + t0 * k + i) - tot[e] : -1;
+    }
+    __syncthreads();
+  }
+  if (!(p.mode & 2)) return;
+
+  // ---- destination segment bases (layout_kernel's arithmetic)
+  if (p.world > 1) {
+    if (tid < p.world)
+      wait_geq_sys(p.own_count_flags + tid, p.epoch, p.timeout_ns, p.err, 0x5000000ull | tid);
+    __syncthreads();
+  }
+  for (int x = tid; x < E; x += blockDim.x) {
+    int32_t t = 0, below = 0;
+    for (int s = 0; s < p.world; ++s) {
+      // own row: from smem when PRE ran in this launch (CTA 0 may not have stored it yet)
+      const int32_t v = (s == p.rank && (p.mode & 1)) ? cnt[x] : __ldcg(p.mat + s * E + x);
+      t += v;
+      below += s < p.rank ? v : 0;
+    }
+    seg[x] = t;
+    off[x] = below;  // rows of lower source ranks for the same expert
+  }
+  __syncthreads();
+  if (tid == 0) last_tot = seg[(p.rank + 1) * epr - 1];
+  block_exclusive_scan(seg, E);
+  for (int x = tid; x < E; x += blockDim.x) {
+    const int owner_first = (x / epr) * epr;
+    off[x] += seg[x] - seg[owner_first];
+  }
+  __syncthreads();
+  if (c == 0) {
+    if (tid == 0)
+      *p.recv_rows = static_cast<int64_t>(seg[(p.rank + 1) * epr - 1]) + last_tot - seg[p.rank * epr];
+    for (int x = tid; x < E; x += blockDim.x) p.seg_base[x] = off[x];
+    for (int i = tid; i < p.world * E; i += blockDim.x)
+      p.counts_out[i] = (i / E == p.rank && (p.mode & 1)) ? cnt[i % E] : __ldcg(p.mat + i);
+  }
+
+  // ---- scatter this CTA's tokens
+  uint32_t phases = ph1 << 1;  // buffer 1's barrier may have been used for the logits
+  const int64_t vpr = p.vec_per_row;
+  int ti = warp;
+  for (int b = 0; ti < ntasks; ti += nw, b ^= 1) {
+    const int tt = static_cast<int>(ti / npieces);
+    const int64_t v0 = (ti % npieces) * kPiece;
+    const uint32_t bytes = piece_bytes(ti);
+    uint4* my_dst = nullptr;
+    int my_remote = 0;
+    if (lane < k) {
+      const int slot = tt * k + lane;
+      const int e = idx_s[slot];
+      if (pos_s[slot] >= 0) {
+        const int64_t row = static_cast<int64_t>(off[e]) + pos_s[slot];
+        if (v0 == 0) p.dest_row[t0 * k + slot] = static_cast<int32_t>(row);
+        if (row < p.max_recv) my_dst = static_cast<uint4*>(p.recv.p[e / epr]) + row * vpr + v0;
+        else if (p.err) atomicCAS(p.err, 0ull, 0x5000000ull | 0xFFFFFFull);
+        my_remote = (e / epr) != p.rank;
+      }
+    }
+    if (lane < k) sdst[warp][lane] = my_dst;
+    __syncwarp();
+    const unsigned remote = __ballot_sync(0xffffffffu, my_remote != 0 && my_dst != nullptr);
+    mbar_wait(&bars[2 * warp + b], (phases >> b) & 1);
+    phases ^= 1u << b;
+    uint8_t* buf = bufs + (2 * warp + b) * kFdBuf;
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (ti + nw < ntasks) issue_load(ti + nw, b ^ 1);
+      for (int j = 0; j < k; ++j)
+        if (sdst[warp][j] != nullptr && !((remote >> j) & 1))
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[warp][j]),
+                       "r"(smem_u32(buf)), "r"(bytes)
+                       : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (int j = 0; j < k; ++j) {
+      if (!((remote >> j) & 1)) continue;
+      uint4* d = sdst[warp][j];
+      const uint4* sb = reinterpret_cast<const uint4*>(buf);
+      for (int v = lane; v < static_cast<int>(bytes / 16); v += 32) d[v] = sb[v];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores performed
+  if (p.world > 1) {
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async_global();
+      fence_sys();
+      unsigned long long* done = p.gflags + kFdDoneSlot;
+      const unsigned long long old = atomicAdd(done, 1ull);
+      if (old == static_cast<unsigned long long>(G - 1)) {  // last CTA: every row of this rank landed
+        fence_sys();
+        *done = 0;  // the next launch on this device is stream-ordered after this one
+        for (int q = 0; q < p.world; ++q) st_release_sys(p.deliver_flags.p[q] + p.rank, p.epoch);
+      }
+    }
+  }
+}
+
 // warp per token; hidden in 256-element chunks (8 bf16 = 16 bytes per lane)
 __global__ void __launch_bounds__(256) combine_kernel(
     int64_t tokens, int64_t vec_per_row, int k, int E, int world,
@@ -737,6 +1114,84 @@ int check_moe(tf_team* t, int rank, const tf_moe_args* a) {
   return TF_OK;
 }
 
+
+// Fused dispatch launch (mode 1 PRE, 2 MAIN, 3 both).  Returns TF_ERR_CONFIG (no
+// launch) when the shape does not fit the fused kernel; the caller then runs the
+// multi-kernel path.
+int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
+  *launched = false;
+  static const bool enabled = [] {
+    const char* e = getenv("TF_MOE_FUSED");
+    return !e || atoi(e) != 0;
+  }();
+  if (!enabled || p.E > 1024) return TF_OK;
+  int dev = 0;
+  TF_CUDA_TRY(cudaGetDevice(&dev));
+  const size_t smem = fused_dispatch_smem(p.E);
+  if (smem > 225 * 1024) return TF_OK;
+  const int vpl = !p.logits ? 0 : p.E <= 64 ? 2 : p.E <= 256 ? 8 : 32;
+  const void* fn = vpl == 0 ? reinterpret_cast<const void*>(dispatch_fused_kernel<0>)
+                 : vpl == 2 ? reinterpret_cast<const void*>(dispatch_fused_kernel<2>)
+                 : vpl == 8 ? reinterpret_cast<const void*>(dispatch_fused_kernel<8>)
+                            : reinterpret_cast<const void*>(dispatch_fused_kernel<32>);
+  static std::mutex mu;
+  static std::map<int, unsigned long long*> flag_bufs;
+  static std::map<int, unsigned long long> epochs;
+  static std::map<std::pair<int, const void*>, int> occ;
+  unsigned long long* flags = nullptr;
+  unsigned long long ge = 0;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = flag_bufs.find(dev);
+    if (it == flag_bufs.end()) {
+      TF_CUDA_TRY(cudaMalloc(&flags, 1024 * sizeof(unsigned long long)));
+      TF_CUDA_TRY(cudaMemset(flags, 0, 1024 * sizeof(unsigned long long)));
+      flag_bufs[dev] = flags;
+    } else {
+      flags = it->second;
+    }
+    auto key = std::make_pair(dev, fn);
+    auto oi = occ.find(key);
+    if (oi == occ.end()) {
+      TF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+      TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kFdWarps, smem));
+      occ[key] = per_sm;
+    } else {
+      per_sm = oi->second;
+    }
+    if (p.mode & 1) ge = ++epochs[dev];
+  }
+  if (per_sm < 1) return TF_OK;
+  const int64_t cap = std::min<int64_t>(static_cast<int64_t>(num_sms_of_current_device()) * per_sm, kFdDoneSlot);
+  const int64_t T = p.tokens;
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>(cap, T));
+  const int64_t tpc = T > 0 ? (T + G - 1) / G : 1;
+  G = T > 0 ? (T + tpc - 1) / tpc : 1;
+  if (tpc * p.k > kFdEntCap) return TF_OK;
+  p.tpc = static_cast<int>(tpc);
+  p.gflags = flags;
+  p.gepoch = ge;
+  // the chunk histogram scratch [G][E] (G <= 1023, E <= 1024): one 4 MB buffer per device
+  void* hist = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    static std::map<int, void*> hist_bufs;
+    auto it = hist_bufs.find(dev);
+    if (it == hist_bufs.end()) {
+      TF_CUDA_TRY(cudaMalloc(&hist, static_cast<size_t>(kFdDoneSlot) * fd_stride(1024) * 4));
+      hist_bufs[dev] = hist;
+    } else {
+      hist = it->second;
+    }
+  }
+  p.chunk_hist = static_cast<int32_t*>(hist);
+  void* args[] = {&p};
+  TF_CUDA_TRY(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(G)), dim3(32 * kFdWarps), args, smem, s));
+  *launched = true;
+  return TF_OK;
+}
+
 int grid_for(int64_t warps) {
   int64_t blocks = (warps * 32 + 255) / 256;
   const int cap = num_sms_of_current_device() * 8;
@@ -803,7 +1258,52 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
   const int dev = t->pes[rank].device;
   int32_t* ebase = reinterpret_cast<int32_t*>(t->pes[rank].base + m.ebase_off);
   int32_t* seg_base = reinterpret_cast<int32_t*>(t->pes[rank].base + m.seg_off);
-  if (phase & TF_PHASE_PRE) {
+  if (a->logits && (!a->topk_idx || !a->topk_w))
+    return fail(TF_ERR_INVALID, "routing from logits needs topk_idx and topk_w outputs");
+  const int fmode = ((phase & TF_PHASE_PRE) ? 1 : 0) | ((phase & TF_PHASE_MAIN) ? 2 : 0);
+  bool fused = false;
+  if (fmode) {
+    // one launch per phase group (PRE+MAIN in one when the caller drives both)
+    tf::FusedDispatch p{};
+    p.x = static_cast<const uint4*>(a->x);
+    p.logits = a->logits;
+    p.tokens = a->tokens;
+    p.vec_per_row = a->hidden / 8;
+    p.max_recv = a->max_recv;
+    p.k = a->k;
+    p.E = E;
+    p.world = w;
+    p.rank = rank;
+    p.mode = fmode;
+    p.idx = const_cast<int32_t*>(a->topk_idx);
+    p.w = const_cast<float*>(a->topk_w);
+    p.sorted_pos = a->sorted_pos;
+    p.dest_row = a->dest_row;
+    p.ebase = ebase;
+    p.seg_base = seg_base;
+    p.counts_out = a->counts;
+    p.recv_rows = a->recv_rows;
+    p.mat = reinterpret_cast<int32_t*>(t->pes[rank].base + m.mat_off);
+    for (int q = 0; q < w; ++q) {
+      p.mats.p[q] = t->pes[q].base + m.mat_off;
+      p.recv.p[q] = t->pes[q].base + m.recv_off;
+      p.count_flags.p[q] = t->pes[q].sig + sig;
+      p.deliver_flags.p[q] = t->pes[q].sig + sig + w;
+    }
+    p.own_count_flags = t->pes[rank].sig + sig;
+    p.epoch = m.ws->epoch[rank] + ((fmode & 1) ? 1 : 0);
+    p.err = t->err_word(rank);
+    p.timeout_ns = t->timeout_ns;
+    rc = tf::launch_fused_dispatch(p, s, &fused);
+    if (rc) return rc;
+    if (fused && (fmode & 1)) m.ws->epoch[rank] = p.epoch;
+  }
+  if ((phase & TF_PHASE_PRE) && !fused) {
+    if (a->logits) {
+      rc = tf_moe_topk(a->logits, a->tokens, E, a->k, const_cast<int32_t*>(a->topk_idx),
+                       const_cast<float*>(a->topk_w), stream);
+      if (rc) return rc;
+    }
     const uint64_t e = ++m.ws->epoch[rank];
     // count into this rank's own row of its local matrix, then push the row to all peers
     int32_t* own_row = reinterpret_cast<int32_t*>(t->pes[rank].base + m.mat_off) +
@@ -821,7 +1321,7 @@ int tf_moe_dispatch(tf_team* t, int rank, const tf_moe_args* a, int phase, void*
     if (w > 1) tf::push_counts_kernel<<<1, 256, 0, s>>>(own_row, E, mats, flags, w, rank, e);
     TF_CUDA_TRY(cudaGetLastError());
   }
-  if (phase & TF_PHASE_MAIN) {
+  if ((phase & TF_PHASE_MAIN) && !fused) {
     const uint64_t e = m.ws->epoch[rank];
     if (w > 1)
       tf::wait_flags_kernel<<<1, 32 * ((w + 31) / 32), 0, s>>>(t->pes[rank].sig + sig, w, e,

@@ -89,7 +89,7 @@ class ExpertParallelMoE:
             self.state[r] = st
 
     # -------------------------------------------------------------- helpers
-    def _fill(self, r, x, idx, w=None, out=None):
+    def _fill(self, r, x, idx, w=None, out=None, logits=None):
         st = self.state[r]
         a = st["args"]
         t = idx.shape[0]
@@ -97,6 +97,7 @@ class ExpertParallelMoE:
             raise ValueError(f"{t} tokens exceed max_tokens={self.max_tokens}")
         if idx.dtype != torch.int32 or idx.shape[1] != self.k:
             raise ValueError("topk_idx must be int32 [T, k]")
+        a.logits = logits.data_ptr() if logits is not None else None
         a.tokens = t
         a.x = x.data_ptr() if x is not None else None
         a.topk_idx = idx.data_ptr()
@@ -114,9 +115,18 @@ class ExpertParallelMoE:
             return {(t.rank or 0): (x, idx)}
         return {r: (x[r], idx[r]) for r in range(t.world)}
 
+    def _phases(self):
+        """PRE and MAIN are one call (one launch for the dispatch) when every rank
+        has its own GPU; ranks sharing a GPU need every PRE enqueued before any
+        MAIN waits on it."""
+        t = self.team
+        if t.rank is not None or t.world == 1 or t.distinct_devices:
+            return (_lib.PHASE_PRE | _lib.PHASE_MAIN, _lib.PHASE_POST)
+        return (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST)
+
     def _drive(self, fn, per_rank):
         t = self.team
-        for phase in (_lib.PHASE_PRE, _lib.PHASE_MAIN, _lib.PHASE_POST):
+        for phase in self._phases():
             for r, a in per_rank.items():
                 with torch.cuda.device(t.devices[r]):
                     s = torch.cuda.current_stream(t.devices[r])
@@ -139,6 +149,29 @@ class ExpertParallelMoE:
         if isinstance(topk_idx, torch.Tensor):
             return self.state[next(iter(per))]["recv"]
         return [self.state[r]["recv"] for r in per]
+
+    def route_dispatch(self, x, logits):
+        """Top-k routing (as moe_route: ties -> lower expert) fused into the
+        dispatch launch.  Returns (recv, topk_idx, topk_w), per local rank as
+        lists for a local team with several ranks."""
+        items = self._ranks_args(x, logits)
+        per, keep, res = {}, {}, {}
+        for r, (xx, lg) in items.items():
+            if xx.dtype != torch.bfloat16 or xx.shape[1] != self.H or not xx.is_contiguous():
+                raise ValueError("x must be a contiguous bf16 [T, hidden] tensor")
+            if lg.dtype != torch.float32 or lg.dim() != 2 or lg.shape[0] != xx.shape[0] or lg.shape[1] != self.E:
+                raise ValueError(f"logits must be float32 [T, {self.E}]")
+            lg = lg.contiguous()
+            idx = torch.empty((lg.shape[0], self.k), dtype=torch.int32, device=lg.device)
+            w = torch.empty((lg.shape[0], self.k), dtype=torch.float32, device=lg.device)
+            keep[r] = (xx, lg, idx, w)
+            per[r] = self._fill(r, xx, idx, w, None, logits=lg)
+            res[r] = (self.state[r]["recv"], idx, w)
+        self._keep = keep
+        self._drive("tf_moe_dispatch", per)
+        if isinstance(logits, torch.Tensor):
+            return res[next(iter(per))]
+        return [res[r] for r in per]
 
     def _r(self, r):
         if r is not None:

@@ -103,6 +103,47 @@ def test_dispatch_combine_vs_oracle(world, e, k, t, h):
         assert OC.compare(outs[r].float().cpu().numpy(), want[r]) <= TOL_BF16
 
 
+@pytest.mark.parametrize("world,e,k,t,h", [(1, 256, 8, 4096, 256), (1, 60, 4, 300, 64), (2, 8, 2, 37, 64),
+                                           (8, 256, 8, 200, 128), (1, 1024, 16, 33, 64),
+                                           (1, 64, 8, 40000, 16)])
+def test_route_dispatch_fused(world, e, k, t, h):
+    """Top-k fused into the dispatch launch: the same (idx, w) as moe_route and the
+    oracle's layout.  (1, 64, 8, 40000) exceeds the fused kernel's per-CTA entry
+    budget and runs the multi-kernel path."""
+    M = _m()
+    rng = np.random.default_rng(world * 7 + e + t)
+    team = _team(world)
+    ep = M.ExpertParallelMoE(team, e, h, k, max_tokens=t)
+    xs = [torch.from_numpy(rng.standard_normal((t, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+          for _ in range(world)]
+    lg = [torch.from_numpy(rng.standard_normal((t, e)).astype(np.float32)).cuda() for _ in range(world)]
+    lg[0][0, :4] = 7.0  # ties -> lower expert id
+    if world == 1:
+        res = [ep.route_dispatch(xs[0], lg[0])]
+    else:
+        res = ep.route_dispatch(xs, lg)
+    torch.cuda.synchronize()
+    team.check()
+    idx_np = []
+    for r in range(world):
+        ridx, rw = OM.topk_route(lg[r].cpu().numpy(), k)
+        assert np.array_equal(res[r][1].cpu().numpy(), ridx)
+        assert np.allclose(res[r][2].cpu().numpy(), rw, rtol=1e-5, atol=1e-6)
+        idx_np.append(ridx.astype(np.int32))
+    counts, recv_src, recv_tok, slot_row = OM.dispatch_layout_fast(idx_np, e, world)
+    x_np = [x.float().cpu().numpy() for x in xs]
+    for r in range(world):
+        assert np.array_equal(ep.counts(r).cpu().numpy(), counts)
+        n = ep.recv_rows(r)
+        assert n == len(recv_src[r])
+        src, tok = recv_src[r], recv_tok[r]
+        got = res[r][0][:n].float().cpu().numpy()
+        for s_ in range(world):
+            sel = src == s_
+            assert np.array_equal(got[sel], x_np[s_][tok[sel]])
+        assert np.array_equal(ep.dest_rows(r).cpu().numpy(), slot_row[r])
+
+
 def test_dispatch_repeated_calls_epochs():
     M = _m()
     world, e, k, t, h = 4, 16, 2, 40, 64

@@ -50,6 +50,7 @@ def main():
     res = {}
     res["route"] = timed(lambda: M.moe_route(logits, K))
     res["dispatch"] = timed(lambda: ep.dispatch(x, idx))
+    res["route_dispatch"] = timed(lambda: ep.route_dispatch(x, logits))
     res["combine"] = timed(lambda: ep.combine(idx, w))
     res["fill_470MB"] = timed(lambda: big.zero_())
     res["bcast_copy_x8"] = timed(lambda: out.copy_(x.unsqueeze(1).expand(T, K, H)))
