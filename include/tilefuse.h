@@ -434,6 +434,13 @@ int tf_trace_enable(int device, int64_t capacity);
 int tf_trace_disable(int device);
 int tf_trace_read(int device, uint64_t* host, int64_t capacity, int64_t* count);
 
+/* ------------------------------------------------------------------ device topology
+ * Die (L2 partition) of every SM of `device`, measured once per process by
+ * first-touch load latency (no reference counterpart: it feeds the persistent
+ * GEMM's die-ranked tile order, TF_GEMM_DIE).  out[smid] = 0 / 1 for smid <
+ * *n_sms; *n_sms = 0 when no two-die structure was found. */
+int tf_sm_die_map(int device, uint8_t* out, int cap, int* n_sms);
+
 #ifdef __cplusplus
 }
 #endif

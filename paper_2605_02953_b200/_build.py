@@ -21,7 +21,7 @@ PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtilefuse.so"
-SOURCES = ["tf_team.cu", "tf_ops.cu", "tf_gemm.cu", "tf_moe.cu", "tf_attn.cu", "tf_mega.cu", "tf_layer.cu", "tf_prep.cu", "tf_agmoe.cu", "tf_nvls.cu", "tf_swizzle.cpp"]
+SOURCES = ["tf_team.cu", "tf_ops.cu", "tf_gemm.cu", "tf_moe.cu", "tf_attn.cu", "tf_mega.cu", "tf_layer.cu", "tf_prep.cu", "tf_agmoe.cu", "tf_nvls.cu", "tf_topo.cu", "tf_swizzle.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

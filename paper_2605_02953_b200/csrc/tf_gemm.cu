@@ -45,6 +45,7 @@ __device__ __forceinline__ uint32_t desc_lo_k(uint32_t addr) { return ((addr & 0
 
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
 constexpr bool kDefaultMulticast = false;  // 4-CTA multicast clusters (TF_GEMM_MC overrides)
+constexpr int kDefaultDieMode = 1;         // die-ranked cluster ids (TF_GEMM_DIE overrides)
 #ifndef TF_GEMM_LAG
 #define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
 #endif
@@ -106,6 +107,14 @@ struct KParams {
   int n_experts;
   long long row_bytes;
   uint64_t* own_flags;
+  // die-ranked cluster ids (TF_GEMM_DIE): sm_die[%smid] in {0,1}; die_ctr = this
+  // launch's self-resetting counter (die-0 arrivals low word, die-1 high word).
+  // die_mode 1: clusters on die 0 take the first positions of every wave; 2: also
+  // reorder each full wave so its tiles in the lower half of the group's rows come
+  // first (die 0 then works on those rows, die 1 on the upper half: A is not shared)
+  const uint8_t* sm_die;
+  unsigned long long* die_ctr;
+  int die_mode;
 };
 
 // CG = CTAs per tile (1, or 2 = CTA pair with tcgen05 cta_group::2).
@@ -184,11 +193,40 @@ __device__ __forceinline__ int block_row(int h, uint32_t cta_rank) {
   return (h * CG + static_cast<int>(cta_rank)) * 128;
 }
 
+// die_mode 2: position o of a full wave of W steps -> step.  The wave's steps in
+// order, those in the lower half of their group's rows first (stable), so die 0
+// (positions [0, n0)) gets the lower rows and die 1 the upper rows of the wave.
+__device__ __forceinline__ int wave_step(const KParams& p, int work, int W) {
+  const int base = work - work % W;
+  if (base + W > p.tail_base) return work;  // partial last wave: plain order
+  const int per_group = p.group_m * p.num_pid_n;
+  const int g = base / per_group;
+  if ((base + W - 1) / per_group != g) return work;  // wave straddles two groups: plain order
+  const int rows = min(p.num_pid_m - g * p.group_m, p.group_m);
+  const int hr = (rows + 1) / 2;  // rows [0, hr) of the group are the "lower" half
+  if (hr == rows) return work;
+  // group-local steps are column-major: s = col * rows + row
+  auto nlow_below = [&](int x) { return (x / rows) * hr + min(x % rows, hr); };
+  const int a = base - g * per_group;
+  const int la = nlow_below(a), nlow = nlow_below(a + W) - la;
+  const int o = work - base;
+  int s;
+  if (o < nlow) {
+    const int t = la + o;
+    s = (t / hr) * rows + t % hr;
+  } else {
+    const int hu = rows - hr;
+    const int t = (a - la) + (o - nlow);  // upper-half index
+    s = (t / hu) * rows + hr + t % hu;
+  }
+  return g * per_group + s;
+}
+
 // Work item -> (tile step, k-block range, partial slot or -1).
 __device__ __forceinline__ void decode_work(const KParams& p, int work, int& step, int& kb0,
-                                            int& kb1, int& slot) {
+                                            int& kb1, int& slot, int W = 0) {
   if (work < p.tail_base) {
-    step = work;
+    step = (p.die_mode == 2 && W > 0) ? wave_step(p, work, W) : work;
     kb0 = 0;
     kb1 = p.num_kb;
     slot = -1;
@@ -379,8 +417,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int pair = static_cast<int>(cta_rank >> 1); // which pair of the cluster
   const bool leader = prank == 0;
   constexpr int kCluster = CG * NPAIR;
-  const int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / kCluster;
   const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / kCluster;
+  int* vcid_slot = reinterpret_cast<int*>(tmem_slot + 2);  // spare word after the TMEM slot
+  if (NPAIR == 1 && !GROUPED && p.die_mode && threadIdx.x == 0 && leader) {
+    // die-ranked cluster id: die-0 clusters count up from 0, die-1 clusters down from
+    // num_clusters - 1 (a bijection whatever the arrival order); the last arrival
+    // resets the counter for the next launch that uses this slot
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int d = p.sm_die[smid & 255] & 1;
+    const unsigned long long old = atomicAdd(p.die_ctr, d ? (1ull << 32) : 1ull);
+    const int lo = static_cast<int>(old & 0xFFFFFFFFull), hi = static_cast<int>(old >> 32);
+    if (lo + hi + 1 == num_clusters) atomicExch(p.die_ctr, 0ull);
+    const int v = d ? num_clusters - 1 - hi : lo;
+    *vcid_slot = v;  // the pair's second CTA reads it after the cluster barrier below
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S::kStages; ++s) {
@@ -408,6 +459,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / kCluster;
+  if (NPAIR == 1 && !GROUPED && p.die_mode) {
+    if (leader) {
+      cluster_id = *vcid_slot;
+    } else {
+      uint32_t v;
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(mapa_shared(smem_u32(vcid_slot), 0)) : "memory");
+      cluster_id = static_cast<int>(v);
+    }
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -418,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
       for (int work = cluster_id; work < p.total_work; work += num_clusters) {
         int step, kb0, kb1, slot;
-        decode_work(p, work, step, kb0, kb1, slot);
+        decode_work(p, work, step, kb0, kb1, slot, num_clusters);
         const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
         const int pid_m = geo.pid_m, pid_n = geo.pid_n;
         const int tile_m0 = geo.row0;
@@ -554,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
         int step, kb0, kb1, slot;
-        decode_work(p, work, step, kb0, kb1, slot);
+        decode_work(p, work, step, kb0, kb1, slot, num_clusters);
         const uint32_t tph = local & 1;
         const int nkb = kb1 - kb0;
         const bool lagged = nkb >= 2 * L + 1;
@@ -615,7 +676,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int local = 0;
       for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
         int step, kb0, kb1, slot;
-        decode_work(p, work, step, kb0, kb1, slot);
+        decode_work(p, work, step, kb0, kb1, slot, num_clusters);
         const int acc = local % ACC;
         const uint32_t acc_phase = (local / ACC) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -674,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int local = 0;
     for (int work = cluster_id; work < p.total_work; work += num_clusters, ++local) {
       int step, kb0, kb1, slot;
-      decode_work(p, work, step, kb0, kb1, slot);
+      decode_work(p, work, step, kb0, kb1, slot, num_clusters);
       const TileGeo geo = tile_geo<GROUPED, S::kTileM, BN, NPAIR>(p, step, pair);
       const int pid_m = geo.pid_m, pid_n = geo.pid_n;
       const int acc = local % ACC;
@@ -1093,6 +1154,23 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     const int cap = max_clusters[dev] * CG * NPAIR + kp.comm_ctas;
     if (grid > cap) grid = cap;
   }
+  KParams kd = kp;
+  if (NPAIR == 1 && !GROUPED) {
+    // die-ranked cluster ids (tf_topo.cu); TF_GEMM_DIE = 0 off, 1 ranked, 2 ranked + row split
+    static const int die_env = [] {
+      const char* e = getenv("TF_GEMM_DIE");
+      return e ? atoi(e) : kDefaultDieMode;
+    }();
+    if (die_env > 0) {
+      unsigned long long* slot = nullptr;
+      const uint8_t* tab = sm_die_table(dev, &slot);
+      if (tab) {
+        kd.sm_die = tab;
+        kd.die_ctr = slot;
+        kd.die_mode = die_env;
+      }
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1105,7 +1183,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tp, kp));
+  TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tp, kd));
   if (kp.split_s > 1) {
     const int tail_tiles = (kp.total_work - kp.tail_base) / kp.split_s * NPAIR;
     tail_fixup_kernel<S::kTileM, BN, OUT_F32, NPAIR>

@@ -77,5 +77,9 @@ void layer_release_team(const tf_team* t);
 int num_sms_of_current_device();
 // device trace ring of `device` (tf_trace_enable) and its capacity, or 0 / nullptr
 int trace_buffer(int device, unsigned long long** buf);
+// SM -> die table (tf_topo.cu): device [256] die ids by %smid plus a per-launch counter
+// slot (a ring of kDieCtrSlots self-resetting counters), or nullptr without two dies
+constexpr int kDieCtrSlots = 64;
+const uint8_t* sm_die_table(int dev, unsigned long long** ctr_slot);
 
 }  // namespace tf

@@ -44,3 +44,27 @@ for j in sorted(starts):
           f"first {min(s) * 1e6:8.1f} us")
 end = max(e.t_end for e in ev)
 print(f"kernel span {end * 1e6:.1f} us")
+
+# per-CTA tile transitions: gap between consecutive MMA windows, and how long after a
+# tile's MMA window its epilogue finished (drain tail)
+comp = defaultdict(list)
+epi = defaultdict(list)
+for e in tr.events:
+    if e.kind == "compute":
+        comp[e.worker_id].append(e)
+    elif e.kind == "store":
+        epi[e.worker_id].append(e)
+gaps, tails, edur = [], [], []
+for cta, es in comp.items():
+    es.sort(key=lambda e: e.t_start)
+    for a, b in zip(es, es[1:]):
+        gaps.append(b.t_start - a.t_end)
+    ep = sorted(epi.get(cta, []), key=lambda e: e.t_start)
+    for c, s in zip(es, ep):
+        tails.append(s.t_end - c.t_end)
+        edur.append(s.t_end - s.t_start)
+if gaps:
+    print(f"MMA gap between tiles: mean {statistics.mean(gaps) * 1e6:.2f} us, max {max(gaps) * 1e6:.2f} us")
+if tails:
+    print(f"epilogue end after MMA end: mean {statistics.mean(tails) * 1e6:.2f} us; epilogue event mean {statistics.mean(edur) * 1e6:.2f} us "
+          f"({len(edur)} events from {len(epi)} CTAs)")
