@@ -46,6 +46,10 @@ __device__ __forceinline__ uint32_t desc_lo_k(uint32_t addr) { return ((addr & 0
 constexpr int BK = 64;                 // 64 bf16 = 128 B = one swizzle atom row
 constexpr bool kDefaultMulticast = false;  // 4-CTA multicast clusters (TF_GEMM_MC overrides)
 constexpr int kDefaultDieMode = 1;         // die-ranked cluster ids (TF_GEMM_DIE overrides)
+#ifndef TF_GEMM_EARLY_RELEASE
+#define TF_GEMM_EARLY_RELEASE 1
+#endif
+constexpr bool kEarlyRelease = TF_GEMM_EARLY_RELEASE;  // epilogue frees TMEM before its stores
 #ifndef TF_GEMM_LAG
 #define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
 #endif
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kCluster = CG * NPAIR;
   const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / kCluster;
   int* vcid_slot = reinterpret_cast<int*>(tmem_slot + 2);  // spare word after the TMEM slot
-  if (NPAIR == 1 && !GROUPED && p.die_mode && threadIdx.x == 0 && leader) {
+  if (!GROUPED && p.die_mode && threadIdx.x == 0 && cta_rank == 0) {
     // die-ranked cluster id: die-0 clusters count up from 0, die-1 clusters down from
     // num_clusters - 1 (a bijection whatever the arrival order); the last arrival
     // resets the counter for the next launch that uses this slot
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lo = static_cast<int>(old & 0xFFFFFFFFull), hi = static_cast<int>(old >> 32);
     if (lo + hi + 1 == num_clusters) atomicExch(p.die_ctr, 0ull);
     const int v = d ? num_clusters - 1 - hi : lo;
-    *vcid_slot = v;  // the pair's second CTA reads it after the cluster barrier below
+    *vcid_slot = v;  // the cluster's other CTAs read it after the cluster barrier below
   }
 
   if (threadIdx.x == 0) {
@@ -460,8 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / kCluster;
-  if (NPAIR == 1 && !GROUPED && p.die_mode) {
-    if (leader) {
+  if (!GROUPED && p.die_mode) {
+    if (cta_rank == 0) {
       cluster_id = *vcid_slot;
     } else {
       uint32_t v;
@@ -794,6 +798,53 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (MH == 2 || h == MH - 1) arrive_empty(h);
         }
         continue;
+      }
+      if constexpr (EPI == 0 && !OUT_F32 && !GROUPED && BN == 256) {
+        if (p.tma_store && kEarlyRelease) {
+          // Early release: the half's 256 fp32 columns come out of TMEM as packed bf16 in
+          // registers (128 regs per thread), TMEM is handed back to the MMA warp at once,
+          // and only then are the registers staged through swizzled smem and TMA-stored
+          // -- the store traffic overlaps the next tile's MMAs instead of stalling them
+#pragma unroll 1
+          for (int h = 0; h < MH; ++h) {
+            if (MH == 2 || h == 0) wait_full(h);
+            const int wrow0 = geo.row0 + block_row<CG>(h, prank) + quarter * 32;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                   acc * S::kAccCols + h * BN;
+            uint32_t pk[BN / 2];
+#pragma unroll
+            for (int cc = 0; cc < BN; cc += 64) {
+              uint32_t v[64];
+              tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+              tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                pk[cc / 2 + j] = pack_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            }
+            if (MH == 2 || h == MH - 1) arrive_empty(h);  // TMEM free: the next tile may start
+#pragma unroll
+            for (int cc = 0; cc < BN; cc += 64) {
+              uint8_t* buf = epi_buf + epi_slot * S::kEpiBuf;
+              // the store issued from this buffer two rounds ago must have read it
+              if (lane == 0) tma_store_wait_read<1>();
+              __syncwarp();
+              uint8_t* my_row = buf + lane * 128;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(my_row + ((j ^ (lane & 7)) << 4)) =
+                    make_uint4(pk[cc / 2 + 4 * j], pk[cc / 2 + 4 * j + 1], pk[cc / 2 + 4 * j + 2],
+                               pk[cc / 2 + 4 * j + 3]);
+              fence_proxy_async_shared();
+              __syncwarp();
+              if (lane == 0 && wrow0 < p.m && pid_n * BN + cc < p.n && !p.dbg_skip_store)
+                tma_store_2d(&tmap_c, buf, pid_n * BN + cc, wrow0);
+              if (lane == 0) tma_store_commit();
+              epi_slot ^= 1;
+            }
+          }
+          continue;
+        }
       }
       if (EPI == 0 && p.tma_store) {
         // 32-row x 128-byte boxes: TMEM -> regs -> swizzled smem -> cp.async.bulk.tensor
@@ -1155,7 +1206,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     if (grid > cap) grid = cap;
   }
   KParams kd = kp;
-  if (NPAIR == 1 && !GROUPED) {
+  if (!GROUPED) {
     // die-ranked cluster ids (tf_topo.cu); TF_GEMM_DIE = 0 off, 1 ranked, 2 ranked + row split
     static const int die_env = [] {
       const char* e = getenv("TF_GEMM_DIE");

@@ -96,6 +96,34 @@ def test_core_gemm_persistent_grid_and_tile_map_order_irrelevant():
             assert torch.equal(out, base)
 
 
+def test_sm_die_map_and_die_ranked_grid():
+    """tf_sm_die_map: every SM in one of two L2 partitions (B200: two dies); the
+    die-ranked cluster ids (default TF_GEMM_DIE=1) give bit-identical results for
+    full waves, partial waves and repeated launches (self-resetting counter slots)."""
+    import ctypes as C
+    from paper_2605_02953_b200 import _lib
+    out = (C.c_uint8 * 256)()
+    n = C.c_int()
+    _lib.call("tf_sm_die_map", 0, out, 256, C.byref(n))
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    dies = np.frombuffer(out, np.uint8)[: n.value]
+    if n.value:
+        assert n.value == nsm
+        assert set(dies.tolist()) == {0, 1} and min((dies == 0).sum(), (dies == 1).sum()) >= nsm // 4
+    K = _k()
+    rng = np.random.default_rng(5)
+    m, n_, k = 4096, 2304, 512
+    a = _bf16(rng, (m, k)).cuda()
+    b = _bf16(rng, (n_, k)).cuda()
+    want = a.float() @ b.float().T
+    for sms in (148, 100, 7):
+        for _ in range(3):
+            out = K.gemm(a, b, num_sms=sms, block_m=512, group_m=8)
+            torch.cuda.synchronize()
+            assert torch.equal(out, K.gemm(a, b, num_sms=sms, block_m=512, group_m=8))
+            assert (out.float() - want).abs().max().item() <= 2e-2 * want.abs().max().item()
+
+
 @pytest.mark.parametrize("bm", [128, 256, 512])
 @pytest.mark.parametrize("case", range(12))
 def test_ag_gemm_exact_vs_reference_fixture(case, bm):
