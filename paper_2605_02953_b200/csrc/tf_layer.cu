@@ -78,6 +78,8 @@ struct LayerParams {
   int num_maps;
   int num_sms, max_tiles;
   int fixed_rank;            // IPC: this process's rank; local team: -1 (rank = cta / num_sms)
+  const uint8_t* sm_die;     // die-ranked queues (one rank per launch): SM -> die table
+  unsigned long long* die_ctr;  // and this launch's self-resetting counter, or nullptr
   int world;
   uint64_t flag_base;
   unsigned long long epoch;
@@ -170,8 +172,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-__device__ __forceinline__ unsigned long long* trace_at(const LayerParams& p, int idx) {
-  return p.trace + (static_cast<long long>(blockIdx.x) * p.slots + idx) * 4;
+// trace rows are per queue (the CTA's queue index `q`, die-ranked or blockIdx)
+__device__ __forceinline__ unsigned long long* trace_at(const LayerParams& p, int q, int idx) {
+  return p.trace + (static_cast<long long>(q) * p.slots + idx) * 4;
 }
 
 __device__ __forceinline__ void tma_load_3d_l(void* smem_dst, const void* tmap, uint64_t* bar,
@@ -286,7 +289,20 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = p.fixed_rank >= 0 ? p.fixed_rank : static_cast<int>(blockIdx.x) / p.num_sms;
-  const int sm = static_cast<int>(blockIdx.x) % p.num_sms;
+  int sm = static_cast<int>(blockIdx.x) % p.num_sms;
+  int* qslot = reinterpret_cast<int*>(bars + 27);
+  if (p.die_ctr && threadIdx.x == 0) {
+    // one rank per launch: take the queue by die rank (die-0 CTAs count up from 0, die-1
+    // CTAs down from num_sms - 1), so a wave of round-robin queues gives each die a
+    // compact block of the grouped GEMM raster (tf_topo.cu; same scheme as tf_gemm.cu)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int d = p.sm_die[smid & 255] & 1;
+    const unsigned long long old = atomicAdd(p.die_ctr, d ? (1ull << 32) : 1ull);
+    const int lo = static_cast<int>(old & 0xFFFFFFFFull), hi = static_cast<int>(old >> 32);
+    if (lo + hi + 1 == p.num_sms) atomicExch(p.die_ctr, 0ull);
+    *qslot = d ? p.num_sms - 1 - hi : lo;
+  }
   const CUtensorMap* maps = p.maps + (p.fixed_rank >= 0 ? 0 : rank) * p.num_maps;
   uint8_t* my_base = p.base[rank];
 
@@ -316,6 +332,8 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (p.die_ctr) sm = *qslot;
+  const int qrow = p.fixed_rank >= 0 ? sm : rank * p.num_sms + sm;  // this CTA's trace row
   const int n_tasks = p.counts[sm];
   int last_cls = -1;
 
@@ -337,7 +355,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
       const bool waited = __any_sync(0xffffffffu, wait_deps(p, r, rank, 1, lane, 32));
       __syncwarp();
       if (p.trace && lane == 0) {
-        unsigned long long* tr = trace_at(p, idx);
+        unsigned long long* tr = trace_at(p, qrow, idx);
         tr[0] = t_fetch;
         tr[1] = globaltimer_ns();
       }
@@ -738,7 +756,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         wait_deps(p, r, rank, npe, et, gthreads);
         named_bar(gbar, gthreads);
         if (p.trace && et == 0) {
-          unsigned long long* tr = trace_at(p, idx);
+          unsigned long long* tr = trace_at(p, qrow, idx);
           tr[0] = t_fetch;
           tr[1] = globaltimer_ns();
         }
@@ -951,7 +969,7 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         else
           release_flag(p, rank, r, rank);
         if (p.trace) {
-          unsigned long long* tr = trace_at(p, idx);
+          unsigned long long* tr = trace_at(p, qrow, idx);
           tr[2] = globaltimer_ns();
           tr[3] = (static_cast<unsigned long long>(r.task_id) << 32) | static_cast<unsigned>(r.tile);
         }
@@ -1102,6 +1120,20 @@ extern "C" int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args
   }
   p.trace = reinterpret_cast<unsigned long long*>(a->trace);
   p.slots = a->trace_slots;
+  if (grid == a->num_sms) {  // one rank's queues per launch: rank them by die (TF_LAYER_DIE=0 off)
+    static const bool die_on = [] {
+      const char* e = getenv("TF_LAYER_DIE");
+      return !e || atoi(e) != 0;
+    }();
+    int cur = 0;
+    cudaGetDevice(&cur);
+    unsigned long long* slot = nullptr;
+    const uint8_t* tab = die_on ? tf::sm_die_table(cur, &slot) : nullptr;
+    if (tab) {
+      p.sm_die = tab;
+      p.die_ctr = slot;
+    }
+  }
   static uint64_t attr_done = 0;
   int dev = 0;
   cudaGetDevice(&dev);
