@@ -582,6 +582,7 @@ struct FusedDispatch {
   unsigned long long gepoch;
   unsigned long long* err;
   unsigned long long timeout_ns;
+  int dbg;                              // timing experiments only (TF_MOE_FD_DEBUG): 1 no scatter, 2 no grid wait
 };
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const unsigned long long* p) {
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
   const int epr = E / p.world;
   constexpr int64_t kPiece = kFdBuf / 16;
   const int64_t npieces = (p.vec_per_row + kPiece - 1) / kPiece;
-  const int ntasks = static_cast<int>(nt * npieces);
+  const int ntasks = (p.dbg & 1) ? 0 : static_cast<int>(nt * npieces);
   if (lane == 0) {
     mbar_init(&bars[2 * warp], 1);
     mbar_init(&bars[2 * warp + 1], 1);
@@ -731,7 +732,7 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       __threadfence();
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
     }
-    for (int x = tid; x < G; x += blockDim.x) {
+    for (int x = tid; x < G && !(p.dbg & 2); x += blockDim.x) {
       if (ld_acquire_gpu(p.gflags + x) >= p.gepoch) continue;
       const uint64_t ts = globaltimer_ns();
       while (ld_acquire_gpu(p.gflags + x) < p.gepoch) {
@@ -1186,6 +1187,11 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     }
   }
   p.chunk_hist = static_cast<int32_t*>(hist);
+  static const int dbg = [] {
+    const char* e = getenv("TF_MOE_FD_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   void* args[] = {&p};
   TF_CUDA_TRY(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(G)), dim3(32 * kFdWarps), args, smem, s));
   *launched = true;
