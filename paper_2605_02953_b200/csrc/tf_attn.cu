@@ -803,6 +803,264 @@ __global__ void __maxnreg__(168)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair, S double-buffered
+// A cluster of two CTAs runs ONE 128-query tile per CTA (256 rows per pair) with
+// cta_group::2 MMAs issued by the leader: S(j) = Q K_j^T is one M=256 MMA whose B
+// operand (128 keys) is split 64/64 across the two CTAs' shared memory, O += P(j) V_j
+// one M=256 TS-MMA (P from each CTA's TMEM, V's 128 dims split 64/64).  With one
+// query tile per CTA, TMEM holds TWO S buffers next to O (S0 [0,128), S1 [128,256),
+// O [256,384)), so the tensor pipe computes S(j+1) while the softmax works on S(j):
+// the single-CTA kernel's chain softmax(j) -> PV(j) -> S(j+1) -> softmax(j+1) is
+// broken, and each CTA stages half of every K and V tile (shared-memory traffic per
+// key tile 96 KB vs 128 KB for the same work).  MMA order per key tile j:
+//   PV(j) (needs P(j)), then S(j+2) into P(j)'s buffer -- the in-order tensor pipe
+//   reads P(j) before S(j+2) overwrites it.
+// O rescale (lazy, rare): softmax(j) first waits for PV(j-1) (pv_bar parity; PV(j+1)
+// cannot complete before softmax(j) ends, so the parity wait cannot alias).
+struct AttnPair2Smem {
+  static constexpr int kQ = 2 * kHalf;        // this CTA's Q tile, 32 KB
+  static constexpr int kSlot = 16384;         // half a K tile (64 keys x 128 dims) or half a V tile (128 keys x 64 dims)
+  static constexpr int kSlots = 11;
+  static constexpr int kBars = 512;  // 33 barrier words + the TMEM slot
+  static constexpr int kXchg = 2 * 2 * 128 * 4;  // row-max halves [j & 1][half][row]
+  static constexpr int kTotal = 1024 + kQ + kSlots * kSlot + kBars + kXchg;
+};
+constexpr int kAttnPair2Threads = 320;        // TMA, MMA, 8 softmax warps (2 per TMEM lane quarter)
+
+__global__ void __maxnreg__(255)
+    ag_attn_fwd_pair2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                             const __grid_constant__ CUtensorMap tv, const __grid_constant__ AttnParams p) {
+  using S = AttnPair2Smem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sq = smem;
+  uint8_t* sring = sq + S::kQ;                      // K0 V0 K1 V1 ... halves
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sring + S::kSlots * S::kSlot);
+  uint64_t* q_full = bars;                          // leader: both CTAs' Q bytes
+  uint64_t* r_full = bars + 1;                      // [kSlots] leader: both halves of a K or V tile
+  uint64_t* r_empty = bars + 13;                    // [kSlots] each CTA (multicast commits)
+  uint64_t* s_full = bars + 25;                     // [2] each CTA: S(j) in buffer j & 1
+  uint64_t* p_full = bars + 27;                     // [2] leader: 8 softmax warps x 2 CTAs
+  uint64_t* pv_bar = bars + 29;                     // [2] each CTA: PV(j) complete, by j & 1
+  uint64_t* o_ready = bars + 31;                    // each CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int q0 = (blockIdx.x >> 1) * 2 * kQT + static_cast<int>(cta) * kQT;  // this CTA's tile
+  const int h = blockIdx.y;
+  const int g = h / (p.hq / p.hkv);
+  const int n = p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < S::kSlots; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 16);
+      mbar_init(&pv_bar[i], 1);
+    }
+    mbar_init(o_ready, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * S::kQ);
+      tma_load_3d_pair(sq, &tq, q_full, 0, h, q0);
+      tma_load_3d_pair(sq + kHalf, &tq, q_full, 64, h, q0);
+      uint32_t ready = 0;
+      for (int c = 0; c < 2 * n; ++c) {  // K_j = 2j, V_j = 2j + 1
+        const int j = c >> 1, kv = c & 1;
+        const int kt = (p.start_tile + j) % n;     // gather order: own chunk first
+        const int chunk = kt / p.tiles_per_chunk;
+        if (!kv && p.chunk_flags && !(ready & (1u << chunk))) {
+          wait_geq_sys(p.chunk_flags + chunk, p.epoch, p.timeout_ns, p.err,
+                       0x1000000ull | static_cast<unsigned>(chunk));
+          fence_proxy_async_global();
+          ready |= 1u << chunk;
+        }
+        const int sl = c % S::kSlots;
+        mbar_wait(&r_empty[sl], ((c / S::kSlots) & 1) ^ 1);
+        ATTN_STAMP(j, 5 + kv);
+        uint8_t* dst = sring + sl * S::kSlot;
+        if (leader) mbar_arrive_expect_tx(&r_full[sl], 2 * S::kSlot);
+        if (!kv) {  // this CTA's 64 keys of K_j, all 128 dims (two 64-dim boxes)
+          const int row = kt * 128 + static_cast<int>(cta) * 64;
+          tma_load_3d_pair(dst, &tk, &r_full[sl], 0, g, row);
+          tma_load_3d_pair(dst + 8192, &tk, &r_full[sl], 64, g, row);
+        } else {    // all 128 keys of V_j, this CTA's 64 dims
+          tma_load_3d_pair(dst, &tv, &r_full[sl], static_cast<int>(cta) * 64, g, kt * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(2 * kQT, 128);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(2 * kQT, kD) | (1u << 16);  // B (V) MN-major
+      auto issue_s = [&](int j) {  // S(j) into buffer j & 1
+        const int c = 2 * j, sl = c % S::kSlots;
+        mbar_wait_spin(&r_full[sl], (c / S::kSlots) & 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sq);
+        const uint32_t kb = smem_u32(sring + sl * S::kSlot);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          umma_bf16_pair(tmem + (j & 1) * 128, umma_desc_k_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32),
+                         umma_desc_k_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32), idesc_s, kk != 0);
+        umma_commit_pair_mc(&s_full[j & 1], 0x3);
+        umma_commit_pair_mc(&r_empty[sl], 0x3);
+      };
+      mbar_wait_spin(q_full, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int j = 0; j < n; ++j) {
+        const int b = j & 1;
+        const int cv = 2 * j + 1, vs = cv % S::kSlots;
+        mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
+        ATTN_STAMP(j, 8);
+        mbar_wait_spin(&p_full[b], (j >> 1) & 1);
+        ATTN_STAMP(j, 2);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(sring + vs * S::kSlot);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts_pair(tmem + 256, tmem + b * 128 + kk * 8,
+                            umma_desc_mn_sw128(vb + kk * 2048, 16384), idesc_pv, (j | kk) != 0);
+        umma_commit_pair_mc(&pv_bar[b], 0x3);
+        umma_commit_pair_mc(&r_empty[vs], 0x3);
+        ATTN_STAMP(j, 3);
+        if (j + 2 < n) issue_s(j + 2);
+        ATTN_STAMP(j, 4);
+      }
+      umma_commit_pair_mc(o_ready, 0x3);
+    }
+    __syncwarp();
+  } else {
+    // two warps per TMEM lane quarter: `half` 0 takes keys / O columns [0,64), half 1
+    // [64,128) of the same 32 rows; the row max is combined through shared memory
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t t_o = tmem + lane_off + 256 + half * 64;
+    const uint32_t p_full_leader0 = mapa_shared(smem_u32(&p_full[0]), 0);
+    float* xmax = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + S::kBars);  // [2][2][128]
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1;
+      const uint32_t t_s = tmem + lane_off + b * 128;
+      SM_WAIT(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      if (threadIdx.x == 64) ATTN_STAMP(j, 0);
+      uint32_t sv[2][32];
+      tmem_ld_32x32b_x32(t_s + half * 64, sv[0]);
+      tmem_ld_32x32b_x32(t_s + half * 64 + 32, sv[1]);
+      tmem_ld_wait();
+      float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; i += 2)
+          mx[c] = fmax3(mx[c], __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+      float* xm = xmax + b * 256;
+      xm[half * 128 + row] = fmaxf(mx[0], mx[1]);
+      // both halves of these rows hold their S in registers now (P may overwrite S)
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const float mt = fmaxf(xm[row], xm[128 + row]) * p.scale_log2;
+      float alpha = 1.f;
+      if (mt > m + kLazyRescale) {
+        alpha = ex2(m - mt);
+        m = mt;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        // O must hold PV(j-1) before it is rescaled
+        mbar_wait_spin(&pv_bar[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[16];
+          tmem_ld_32x32b_x16(t_o + c * 16, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+          tmem_st_32x32b_x16(t_o + c * 16, ov);
+        }
+      }
+      uint64_t sum2 = f2pack(0.f, 0.f);
+      const uint64_t scale2 = f2pack(p.scale_log2, p.scale_log2), negm2 = f2pack(-m, -m);
+      uint32_t pk[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float a0, a1;
+          f2unpack(ffma2(f2pack(__uint_as_float(sv[c][2 * i]), __uint_as_float(sv[c][2 * i + 1])), scale2,
+                         negm2),
+                   a0, a1);
+          float p0, p1;
+          if (TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0) {
+            ex2_fma2(a0, a1, p0, p1);
+          } else {
+            p0 = ex2(a0);
+            p1 = ex2(a1);
+          }
+          sum2 = fadd2(sum2, f2pack(p0, p1));
+          pk[c * 16 + i] = pack_bf16x2(p0, p1);
+        }
+      float s0, s1;
+      f2unpack(sum2, s0, s1);
+      l = l * alpha + (s0 + s1);  // this half's keys; the halves are added at the end
+      tmem_st_32x32b_x32(t_s + half * 32, pk);  // P of keys [64 half, 64 half + 64) as bf16 pairs
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full_leader0 + b * 8);
+      if (threadIdx.x == 64) ATTN_STAMP(j, 1);
+      if (threadIdx.x == 192) ATTN_STAMP(j, 7);
+    }
+    mbar_wait_spin(o_ready, 0);
+    tc_fence_after();
+    float* lsum = xmax;  // reuse the exchange buffer: [half][row]
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    lsum[half * 128 + row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    const float inv = 1.f / (lsum[row] + lsum[128 + row]);
+    const int q = q0 + row;
+    uint16_t* dst = static_cast<uint16_t*>(p.out) + (static_cast<long long>(q) * p.hq + h) * kD + half * 64;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t ov[32];
+      tmem_ld_32x32b_x32(t_o + c * 32, ov);
+      tmem_ld_wait();
+      if (q < p.s_local) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          d4[i] = make_uint4(pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
+                             pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -918,7 +1176,9 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
     // 3.88 ms/rank: the pair's softmax warpgroups run in lockstep across two SMs), so
     // it is opt-in
     const char* pair_env = getenv("TF_ATTN_PAIR");
-    const bool pair = pair_env && atoi(pair_env) && sl % (4 * tf::kQT) == 0;
+    const int pair_mode = pair_env ? atoi(pair_env) : 0;
+    const bool pair2 = pair_mode == 2 && sl % (2 * tf::kQT) == 0;
+    const bool pair = (pair_mode == 1 && sl % (4 * tf::kQT) == 0) || pair2;
     // single-CTA kernel: K/V read over NVLink straight from each owner's chunk (no
     // staging copy; TF_ATTN_DIRECT=0 restores the copy-engine pull into this rank's
     // workspace); the pair variant keeps the pull
@@ -985,13 +1245,16 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
       TF_CUDA_TRY(cudaFuncSetAttribute(tf::ag_attn_fwd_pair_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        tf::AttnPairSmem::kTotal));
+      TF_CUDA_TRY(cudaFuncSetAttribute(tf::ag_attn_fwd_pair2_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tf::AttnPair2Smem::kTotal));
       attr_done |= 1ull << dev;
     }
     if (pair) {
       cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(static_cast<unsigned>(2 * sl / (4 * tf::kQT)), static_cast<unsigned>(a->hq));
-      cfg.blockDim = dim3(tf::kAttnThreads2);
-      cfg.dynamicSmemBytes = tf::AttnPairSmem::kTotal;
+      cfg.gridDim = dim3(static_cast<unsigned>(2 * sl / ((pair2 ? 2 : 4) * tf::kQT)), static_cast<unsigned>(a->hq));
+      cfg.blockDim = dim3(pair2 ? tf::kAttnPair2Threads : tf::kAttnThreads2);
+      cfg.dynamicSmemBytes = pair2 ? tf::AttnPair2Smem::kTotal : tf::AttnPairSmem::kTotal;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1000,7 +1263,8 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf::ag_attn_fwd_pair_kernel, tq, tk, tv, p));
+      if (pair2) TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf::ag_attn_fwd_pair2_kernel, tq, tk, tv, p));
+      else TF_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf::ag_attn_fwd_pair_kernel, tq, tk, tv, p));
     }
     dim3 grid(static_cast<unsigned>((sl + 2 * tf::kQT - 1) / (2 * tf::kQT)), static_cast<unsigned>(a->hq));
     if (!pair) tf::ag_attn_fwd_kernel<<<grid, tf::kAttnThreads2, tf::AttnSmem::kTotal, s>>>(tq, tk, tv, p);

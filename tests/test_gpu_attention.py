@@ -74,7 +74,9 @@ def test_ag_kv_scores_validation():
 @pytest.mark.parametrize("world,sl,hq,hkv", [(1, 128, 1, 1), (1, 256, 2, 1), (2, 128, 4, 2),
                                              (4, 256, 8, 1), (8, 128, 8, 8),
                                              (1, 512, 2, 1), (2, 512, 4, 2), (4, 1024, 8, 2)])
-@pytest.mark.parametrize("pair", ["0", "1"])  # TF_ATTN_PAIR=1: CTA-pair kernel when s_local % 512 == 0
+# TF_ATTN_PAIR=1: CTA-pair kernel, two query tiles per CTA (s_local % 512 == 0);
+# TF_ATTN_PAIR=2: CTA-pair kernel, one query tile per CTA and S double-buffered (s_local % 256 == 0)
+@pytest.mark.parametrize("pair", ["0", "1", "2"])
 def test_ag_kv_attention_vs_oracle(world, sl, hq, hkv, pair, monkeypatch):
     monkeypatch.setenv("TF_ATTN_PAIR", pair)
     from paper_2605_02953_b200.attention import ag_kv_attention
@@ -93,8 +95,10 @@ def test_ag_kv_attention_vs_oracle(world, sl, hq, hkv, pair, monkeypatch):
         assert OC.compare(got, want[r]) <= 2e-2, r
 
 
-def test_ag_kv_attention_peaked_scores_rescaling():
+@pytest.mark.parametrize("pair", ["0", "2"])
+def test_ag_kv_attention_peaked_scores_rescaling(pair, monkeypatch):
     """Large, growing logits force the online-softmax rescale path every tile."""
+    monkeypatch.setenv("TF_ATTN_PAIR", pair)
     from paper_2605_02953_b200.attention import ag_kv_attention
     rng = np.random.default_rng(11)
     world, sl, hq, hkv, d = 2, 256, 2, 1, 128
