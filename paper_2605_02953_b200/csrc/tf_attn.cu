@@ -772,7 +772,7 @@ __global__ void __maxnreg__(168)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full_leader);
+      if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader);
     }
     mbar_wait_spin(&o_ready[t], 0);
     tc_fence_after();
@@ -954,7 +954,7 @@ __global__ void __maxnreg__(255)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t t_o = tmem + lane_off + 256 + half * 64;
     const uint32_t p_full_leader0 = mapa_shared(smem_u32(&p_full[0]), 0);
-    float* xmax = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + S::kBars);  // [2][2][128]
+    float* xmax = reinterpret_cast<float*>(sring + S::kSlots * S::kSlot + S::kBars);  // [2][2][128]
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n; ++j) {
       const int b = j & 1;
@@ -1024,7 +1024,7 @@ __global__ void __maxnreg__(255)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full_leader0 + b * 8);
+      if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader0 + b * 8);
       if (threadIdx.x == 64) ATTN_STAMP(j, 1);
       if (threadIdx.x == 192) ATTN_STAMP(j, 7);
     }

@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     (static_cast<unsigned long long>(pid_m) << 32) | static_cast<unsigned>(pid_n));
         const int b = MH == 2 ? h : acc;
         if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + b * 8);
+          if constexpr (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + b * 8);
           else mbar_arrive(&tempty_bar[b]);
         }
       };

@@ -204,6 +204,13 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Relaxed remote arrive: one SYNCS instruction instead of the MEMBAR.GPU + ERRBAR that
+// .release.cluster costs.  For tcgen05 hand-offs only: the caller has already waited for
+// its TMEM accesses (tcgen05.wait::st / ::ld) and issued tcgen05.fence::before_thread_sync.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // 2-CTA TMA load: data lands in this CTA's smem, transaction bytes are counted on
 // the pair leader's mbarrier (peer bit of the barrier address cleared).
 __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tmap, uint64_t* bar,
