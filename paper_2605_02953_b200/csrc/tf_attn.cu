@@ -253,6 +253,36 @@ __device__ __forceinline__ void umma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, 
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// cta_group::2 forms of the warp-converged issue helpers (the leader CTA's MMA warp)
+__device__ __forceinline__ void umma_ss_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_pair_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -281,8 +311,12 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 __device__ long long g_attn_trace[512][20];
 #define ATTN_STAMP(j, e) \
   do { if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 512) g_attn_trace[j][e] = clock64(); } while (0)
+// cross-SM (globaltimer ns) stamps of the first CTA pair: slots 10 + 5 * cta + e
+#define ATTN_GSTAMP(j, e) \
+  do { if (blockIdx.x < 2 && blockIdx.y == 0 && (j) < 512) g_attn_trace[j][10 + 5 * blockIdx.x + (e)] = globaltimer_ns(); } while (0)
 #else
 #define ATTN_STAMP(j, e) do { } while (0)
+#define ATTN_GSTAMP(j, e) do { } while (0)
 #endif
 
 __global__ void __maxnreg__(168)
@@ -808,13 +842,14 @@ __global__ void __maxnreg__(168)
 // cta_group::2 MMAs issued by the leader: S(j) = Q K_j^T is one M=256 MMA whose B
 // operand (128 keys) is split 64/64 across the two CTAs' shared memory, O += P(j) V_j
 // one M=256 TS-MMA (P from each CTA's TMEM, V's 128 dims split 64/64).  With one
-// query tile per CTA, TMEM holds TWO S buffers next to O (S0 [0,128), S1 [128,256),
-// O [256,384)), so the tensor pipe computes S(j+1) while the softmax works on S(j):
+// query tile per CTA, TMEM holds THREE S buffers next to O (S0, S1, S2, O = 4 x 128
+// columns), so the tensor pipe computes S(j+1), S(j+2) while the softmax works on S(j):
 // the single-CTA kernel's chain softmax(j) -> PV(j) -> S(j+1) -> softmax(j+1) is
 // broken, and each CTA stages half of every K and V tile (shared-memory traffic per
 // key tile 96 KB vs 128 KB for the same work).  MMA order per key tile j:
-//   PV(j) (needs P(j)), then S(j+2) into P(j)'s buffer -- the in-order tensor pipe
-//   reads P(j) before S(j+2) overwrites it.
+//   PV(j) (needs P(j)), then S(j+3) into P(j)'s buffer -- the in-order tensor pipe
+//   reads P(j) before S(j+3) overwrites it.  The third buffer absorbs the cross-CTA
+//   hand-off latency (the leader's MMA needs both CTAs' P(j)).
 // O rescale (lazy, rare): softmax(j) first waits for PV(j-1) (pv_bar parity; PV(j+1)
 // cannot complete before softmax(j) ends, so the parity wait cannot alias).
 struct AttnPair2Smem {
@@ -826,6 +861,8 @@ struct AttnPair2Smem {
   static constexpr int kTotal = 1024 + kQ + kSlots * kSlot + kBars + kXchg;
 };
 constexpr int kAttnPair2Threads = 320;        // TMA, MMA, 8 softmax warps (2 per TMEM lane quarter)
+constexpr int kSBuf = 3;                      // S buffers in TMEM: S0 [0,128) S1 [128,256) S2 [256,384)
+constexpr int kOCol = 384;                    // O [384,512)
 
 __global__ void __maxnreg__(255)
     ag_attn_fwd_pair2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -840,11 +877,11 @@ __global__ void __maxnreg__(255)
   uint64_t* q_full = bars;                          // leader: both CTAs' Q bytes
   uint64_t* r_full = bars + 1;                      // [kSlots] leader: both halves of a K or V tile
   uint64_t* r_empty = bars + 13;                    // [kSlots] each CTA (multicast commits)
-  uint64_t* s_full = bars + 25;                     // [2] each CTA: S(j) in buffer j & 1
-  uint64_t* p_full = bars + 27;                     // [2] leader: 8 softmax warps x 2 CTAs
-  uint64_t* pv_bar = bars + 29;                     // [2] each CTA: PV(j) complete, by j & 1
-  uint64_t* o_ready = bars + 31;                    // each CTA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+  uint64_t* s_full = bars + 25;                     // [3] each CTA: S(j) in buffer j % 3
+  uint64_t* p_full = bars + 28;                     // [3] leader: 8 softmax warps x 2 CTAs
+  uint64_t* pv_bar = bars + 31;                     // [2] each CTA: PV(j) complete, by j & 1
+  uint64_t* o_ready = bars + 33;                    // each CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 34);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
@@ -860,11 +897,11 @@ __global__ void __maxnreg__(255)
       mbar_init(&r_full[i], 1);
       mbar_init(&r_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSBuf; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 16);
-      mbar_init(&pv_bar[i], 1);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(&pv_bar[i], 1);
     mbar_init(o_ready, 1);
     fence_barrier_init();
   }
@@ -893,6 +930,7 @@ __global__ void __maxnreg__(255)
         const int sl = c % S::kSlots;
         mbar_wait(&r_empty[sl], ((c / S::kSlots) & 1) ^ 1);
         ATTN_STAMP(j, 5 + kv);
+        if (!kv) ATTN_GSTAMP(j, 3);
         uint8_t* dst = sring + sl * S::kSlot;
         if (leader) mbar_arrive_expect_tx(&r_full[sl], 2 * S::kSlot);
         if (!kv) {  // this CTA's 64 keys of K_j, all 128 dims (two 64-dim boxes)
@@ -905,45 +943,55 @@ __global__ void __maxnreg__(255)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
+      // all 32 lanes run the loop (descriptor math stays on the uniform datapath: a low
+      // word plus compile-time deltas over a constant high word), elect.sync issues
       constexpr uint32_t idesc_s = umma_idesc_bf16(2 * kQT, 128);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(2 * kQT, kD) | (1u << 16);  // B (V) MN-major
-      auto issue_s = [&](int j) {  // S(j) into buffer j & 1
+      constexpr uint32_t kDescHi = (1024 >> 4) | (1u << (46 - 32)) | (2u << (61 - 32));
+      constexpr uint32_t kLoK = 1u << 16;                       // K-major SW128, LBO field 1
+      constexpr uint32_t kLoV = ((16384 >> 4) & 0x3FFF) << 16;  // MN-major V, LBO = 16 KB
+      auto mk = [](uint32_t lo) {
+        uint64_t d;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(kDescHi));
+        return d;
+      };
+      const uint32_t q_lo = ((smem_u32(sq) & 0x3FFFF) >> 4) | kLoK;
+      const uint32_t ring_lo = (smem_u32(sring) & 0x3FFFF) >> 4;
+      auto issue_s = [&](int j) {  // S(j) into buffer j % 3
         const int c = 2 * j, sl = c % S::kSlots;
-        mbar_wait_spin(&r_full[sl], (c / S::kSlots) & 1);
+        MMA_WAIT(&r_full[sl], (c / S::kSlots) & 1);
         tc_fence_after();
-        const uint32_t qa = smem_u32(sq);
-        const uint32_t kb = smem_u32(sring + sl * S::kSlot);
+        const uint32_t k_lo = (ring_lo + sl * (S::kSlot >> 4)) | kLoK;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
-          umma_bf16_pair(tmem + (j & 1) * 128, umma_desc_k_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32),
-                         umma_desc_k_sw128(kb + (kk >> 2) * 8192 + (kk & 3) * 32), idesc_s, kk != 0);
-        umma_commit_pair_mc(&s_full[j & 1], 0x3);
-        umma_commit_pair_mc(&r_empty[sl], 0x3);
+          umma_ss_pair_elect(tmem + (j % kSBuf) * 128, mk(q_lo + (kk >> 2) * (kHalf >> 4) + (kk & 3) * 2),
+                             mk(k_lo + (kk >> 2) * (8192 >> 4) + (kk & 3) * 2), idesc_s, kk != 0);
+        umma_commit_pair_mc_elect(&s_full[j % kSBuf], 0x3);
+        umma_commit_pair_mc_elect(&r_empty[sl], 0x3);
       };
-      mbar_wait_spin(q_full, 0);
-      issue_s(0);
-      if (n > 1) issue_s(1);
+      MMA_WAIT(q_full, 0);
+      for (int j = 0; j < kSBuf && j < n; ++j) issue_s(j);
       for (int j = 0; j < n; ++j) {
-        const int b = j & 1;
+        const int b = j % kSBuf;
         const int cv = 2 * j + 1, vs = cv % S::kSlots;
-        mbar_wait_spin(&r_full[vs], (cv / S::kSlots) & 1);
-        ATTN_STAMP(j, 8);
-        mbar_wait_spin(&p_full[b], (j >> 1) & 1);
-        ATTN_STAMP(j, 2);
+        MMA_WAIT(&r_full[vs], (cv / S::kSlots) & 1);
+        if (lane == 0) ATTN_STAMP(j, 8);
+        MMA_WAIT(&p_full[b], (j / kSBuf) & 1);
+        if (lane == 0) { ATTN_STAMP(j, 2); ATTN_GSTAMP(j, 2); }
         tc_fence_after();
-        const uint32_t vb = smem_u32(sring + vs * S::kSlot);
+        const uint32_t v_lo = (ring_lo + vs * (S::kSlot >> 4)) | kLoV;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts_pair(tmem + 256, tmem + b * 128 + kk * 8,
-                            umma_desc_mn_sw128(vb + kk * 2048, 16384), idesc_pv, (j | kk) != 0);
-        umma_commit_pair_mc(&pv_bar[b], 0x3);
-        umma_commit_pair_mc(&r_empty[vs], 0x3);
-        ATTN_STAMP(j, 3);
-        if (j + 2 < n) issue_s(j + 2);
-        ATTN_STAMP(j, 4);
+          umma_ts_pair_elect(tmem + kOCol, tmem + b * 128 + kk * 8, mk(v_lo + kk * (2048 >> 4)), idesc_pv,
+                             (j | kk) != 0);
+        umma_commit_pair_mc_elect(&pv_bar[j & 1], 0x3);
+        umma_commit_pair_mc_elect(&r_empty[vs], 0x3);
+        if (lane == 0) ATTN_STAMP(j, 3);
+        if (j + kSBuf < n) issue_s(j + kSBuf);
+        if (lane == 0) ATTN_STAMP(j, 4);
       }
-      umma_commit_pair_mc(o_ready, 0x3);
+      umma_commit_pair_mc_elect(o_ready, 0x3);
     }
     __syncwarp();
   } else {
@@ -952,16 +1000,16 @@ __global__ void __maxnreg__(255)
     const int quarter = warp & 3, half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t t_o = tmem + lane_off + 256 + half * 64;
+    const uint32_t t_o = tmem + lane_off + kOCol + half * 64;
     const uint32_t p_full_leader0 = mapa_shared(smem_u32(&p_full[0]), 0);
     float* xmax = reinterpret_cast<float*>(sring + S::kSlots * S::kSlot + S::kBars);  // [2][2][128]
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n; ++j) {
-      const int b = j & 1;
+      const int b = j % kSBuf;
       const uint32_t t_s = tmem + lane_off + b * 128;
-      SM_WAIT(&s_full[b], (j >> 1) & 1);
+      SM_WAIT(&s_full[b], (j / kSBuf) & 1);
       tc_fence_after();
-      if (threadIdx.x == 64) ATTN_STAMP(j, 0);
+      if (threadIdx.x == 64) { ATTN_STAMP(j, 0); ATTN_GSTAMP(j, 0); }
       uint32_t sv[2][32];
       tmem_ld_32x32b_x32(t_s + half * 64, sv[0]);
       tmem_ld_32x32b_x32(t_s + half * 64 + 32, sv[1]);
@@ -972,7 +1020,7 @@ __global__ void __maxnreg__(255)
 #pragma unroll
         for (int i = 0; i < 32; i += 2)
           mx[c] = fmax3(mx[c], __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
-      float* xm = xmax + b * 256;
+      float* xm = xmax + (j & 1) * 256;
       xm[half * 128 + row] = fmaxf(mx[0], mx[1]);
       // both halves of these rows hold their S in registers now (P may overwrite S)
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
@@ -1025,7 +1073,7 @@ __global__ void __maxnreg__(255)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(p_full_leader0 + b * 8);
-      if (threadIdx.x == 64) ATTN_STAMP(j, 1);
+      if (threadIdx.x == 64) { ATTN_STAMP(j, 1); ATTN_GSTAMP(j, 1); }
       if (threadIdx.x == 192) ATTN_STAMP(j, 7);
     }
     mbar_wait_spin(o_ready, 0);

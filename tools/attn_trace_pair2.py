@@ -27,3 +27,14 @@ mid = buf[20:240, :9]
 print("median period", np.median(np.diff(buf[20:241, 0])))
 for i, nme in enumerate(names):
     print(f"median {nme:9s} - smx_gotS: {np.median(mid[:, i] - mid[:, 0]):8.0f}")
+# cross-SM view (globaltimer ns): leader CTA slots 10.., peer CTA slots 15..
+g0, g1 = buf[:, 10:15], buf[:, 15:20]
+sel = slice(20, 240)
+print("ns, median over j in [20,240):")
+print("  leader gotS -> leader relP   ", np.median(g0[sel, 1] - g0[sel, 0]))
+print("  peer   gotS -> peer relP     ", np.median(g1[sel, 1] - g1[sel, 0]))
+print("  peer gotS - leader gotS      ", np.median(g1[sel, 0] - g0[sel, 0]))
+print("  leader MMA gotP - leader relP", np.median(g0[sel, 2] - g0[sel, 1]))
+print("  leader MMA gotP - peer relP  ", np.median(g0[sel, 2] - g1[sel, 1]))
+print("  peer K load(j) - leader K load(j)", np.median(g1[sel, 3] - g0[sel, 3]))
+print("  period (leader gotS)         ", np.median(np.diff(g0[20:241, 0])))
