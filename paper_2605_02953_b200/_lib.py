@@ -116,6 +116,7 @@ _SIGS = {
     "tf_trace_enable": (ci, [ci, i64]),
     "tf_trace_disable": (ci, [ci]),
     "tf_trace_read": (ci, [ci, vp, i64, C.POINTER(i64)]),
+    "tf_sm_die_map": (ci, [ci, vp, ci, C.POINTER(ci)]),
     "tf_moe_topk": (ci, [vp, i64, ci, ci, vp, vp, vp]),
     "tf_moe_count_scratch_bytes": (i64, [i64, ci]),
     "tf_moe_count": (ci, [vp, i64, ci, ci, vp, vp, vp, vp]),
