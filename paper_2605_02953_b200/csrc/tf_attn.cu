@@ -63,6 +63,7 @@ struct AttnParams {
   int direct, nchunks;
   const CUtensorMap* chunk_maps;
   const uint64_t* peer_flags[kMaxWorld];
+  const void* q;            // [s_local, hq, d] bf16 (the pair kernel stages Q rows into TMEM)
 };
 
 // Two 128-query tiles (A, B) per CTA share every K/V tile; each has its own
@@ -852,17 +853,23 @@ __global__ void __maxnreg__(168)
 //   hand-off latency (the leader's MMA needs both CTAs' P(j)).
 // O rescale (lazy, rare): softmax(j) first waits for PV(j-1) (pv_bar parity; PV(j+1)
 // cannot complete before softmax(j) ends, so the parity wait cannot alias).
+#ifndef TF_ATTN_Q_TMEM
+#define TF_ATTN_Q_TMEM 1  // Q staged in TMEM: QK^T as a TS-MMA, no Q reads from shared memory
+#endif
+constexpr bool kQInTmem = TF_ATTN_Q_TMEM;
 struct AttnPair2Smem {
-  static constexpr int kQ = 2 * kHalf;        // this CTA's Q tile, 32 KB
+  static constexpr int kQ = kQInTmem ? 0 : 2 * kHalf;  // this CTA's Q tile, 32 KB (smem variant)
   static constexpr int kSlot = 16384;         // half a K tile (64 keys x 128 dims) or half a V tile (128 keys x 64 dims)
-  static constexpr int kSlots = 11;
+  static constexpr int kSlots = kQInTmem ? 13 : 11;
   static constexpr int kBars = 512;  // 33 barrier words + the TMEM slot
   static constexpr int kXchg = 2 * 2 * 128 * 4;  // row-max halves [j & 1][half][row]
   static constexpr int kTotal = 1024 + kQ + kSlots * kSlot + kBars + kXchg;
 };
 constexpr int kAttnPair2Threads = 320;        // TMA, MMA, 8 softmax warps (2 per TMEM lane quarter)
-constexpr int kSBuf = 3;                      // S buffers in TMEM: S0 [0,128) S1 [128,256) S2 [256,384)
-constexpr int kOCol = 384;                    // O [384,512)
+// TMEM: three S buffers + O, or (Q in TMEM) two S buffers + O + Q (64 columns of bf16 pairs)
+constexpr int kSBuf = kQInTmem ? 2 : 3;
+constexpr int kOCol = kSBuf * 128;
+constexpr int kQCol = 384;
 
 __global__ void __maxnreg__(255)
     ag_attn_fwd_pair2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -876,12 +883,13 @@ __global__ void __maxnreg__(255)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sring + S::kSlots * S::kSlot);
   uint64_t* q_full = bars;                          // leader: both CTAs' Q bytes
   uint64_t* r_full = bars + 1;                      // [kSlots] leader: both halves of a K or V tile
-  uint64_t* r_empty = bars + 13;                    // [kSlots] each CTA (multicast commits)
-  uint64_t* s_full = bars + 25;                     // [3] each CTA: S(j) in buffer j % 3
-  uint64_t* p_full = bars + 28;                     // [3] leader: 8 softmax warps x 2 CTAs
-  uint64_t* pv_bar = bars + 31;                     // [2] each CTA: PV(j) complete, by j & 1
-  uint64_t* o_ready = bars + 33;                    // each CTA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 34);
+  uint64_t* r_empty = r_full + S::kSlots;           // [kSlots] each CTA (multicast commits)
+  uint64_t* s_full = r_empty + S::kSlots;           // [kSBuf] each CTA: S(j) in buffer j % kSBuf
+  uint64_t* p_full = s_full + kSBuf;                // [kSBuf] leader: 8 softmax warps x 2 CTAs
+  uint64_t* pv_bar = p_full + kSBuf;                // [2] each CTA: PV(j) complete, by j & 1
+  uint64_t* o_ready = pv_bar + 2;                   // each CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_ready + 1);
+  static_assert((1 + 2 * S::kSlots + 2 * kSBuf + 4) * 8 <= S::kBars, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
@@ -892,7 +900,7 @@ __global__ void __maxnreg__(255)
   const int n = p.n_tiles;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    mbar_init(q_full, kQInTmem ? 16 : 1);  // Q rows in TMEM: 8 softmax warps x 2 CTAs
     for (int i = 0; i < S::kSlots; ++i) {
       mbar_init(&r_full[i], 1);
       mbar_init(&r_empty[i], 1);
@@ -913,9 +921,11 @@ __global__ void __maxnreg__(255)
 
   if (warp == 0) {
     if (lane == 0) {
-      if (leader) mbar_arrive_expect_tx(q_full, 2 * S::kQ);
-      tma_load_3d_pair(sq, &tq, q_full, 0, h, q0);
-      tma_load_3d_pair(sq + kHalf, &tq, q_full, 64, h, q0);
+      if constexpr (!kQInTmem) {
+        if (leader) mbar_arrive_expect_tx(q_full, 2 * S::kQ);
+        tma_load_3d_pair(sq, &tq, q_full, 0, h, q0);
+        tma_load_3d_pair(sq + kHalf, &tq, q_full, 64, h, q0);
+      }
       uint32_t ready = 0;
       for (int c = 0; c < 2 * n; ++c) {  // K_j = 2j, V_j = 2j + 1
         const int j = c >> 1, kv = c & 1;
@@ -964,9 +974,14 @@ __global__ void __maxnreg__(255)
         tc_fence_after();
         const uint32_t k_lo = (ring_lo + sl * (S::kSlot >> 4)) | kLoK;
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          umma_ss_pair_elect(tmem + (j % kSBuf) * 128, mk(q_lo + (kk >> 2) * (kHalf >> 4) + (kk & 3) * 2),
-                             mk(k_lo + (kk >> 2) * (8192 >> 4) + (kk & 3) * 2), idesc_s, kk != 0);
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          if constexpr (kQInTmem)
+            umma_ts_pair_elect(tmem + (j % kSBuf) * 128, tmem + kQCol + kk * 8,
+                               mk(k_lo + (kk >> 2) * (8192 >> 4) + (kk & 3) * 2), idesc_s, kk != 0);
+          else
+            umma_ss_pair_elect(tmem + (j % kSBuf) * 128, mk(q_lo + (kk >> 2) * (kHalf >> 4) + (kk & 3) * 2),
+                               mk(k_lo + (kk >> 2) * (8192 >> 4) + (kk & 3) * 2), idesc_s, kk != 0);
+        }
         umma_commit_pair_mc_elect(&s_full[j % kSBuf], 0x3);
         umma_commit_pair_mc_elect(&r_empty[sl], 0x3);
       };
@@ -1003,6 +1018,31 @@ __global__ void __maxnreg__(255)
     const uint32_t t_o = tmem + lane_off + kOCol + half * 64;
     const uint32_t p_full_leader0 = mapa_shared(smem_u32(&p_full[0]), 0);
     float* xmax = reinterpret_cast<float*>(sring + S::kSlots * S::kSlot + S::kBars);  // [2][2][128]
+    if constexpr (kQInTmem) {
+      // this warp's 32 query rows x 64 dims of Q -> TMEM columns [kQCol + 32 half, +32)
+      const int q = q0 + row;
+      uint32_t qv[32];
+      if (q < p.s_local) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p.q) +
+                                                          (static_cast<long long>(q) * p.hq + h) * kD + half * 64);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 v = __ldg(src + i);
+          qv[4 * i] = v.x;
+          qv[4 * i + 1] = v.y;
+          qv[4 * i + 2] = v.z;
+          qv[4 * i + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) qv[i] = 0u;
+      }
+      tmem_st_32x32b_x32(tmem + lane_off + kQCol + half * 32, qv);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(q_full), 0));
+    }
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n; ++j) {
       const int b = j % kSBuf;
@@ -1270,6 +1310,7 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
     p.start_tile = rank * p.tiles_per_chunk;
     p.scale_log2 = a->scale * 1.4426950408889634f;
     p.out = a->out;
+    p.q = a->q;
     p.chunk_flags = t->pes[rank].sig + ws->sig_base + par * w;
     p.direct = direct ? 1 : 0;
     p.nchunks = w;

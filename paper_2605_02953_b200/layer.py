@@ -95,7 +95,7 @@ def plan_linear_bf16(io, config) -> MK.LayerPlan:
     # emission order = grouped raster (swizzle_2d, ovs/swizzle.py:76-88) so the tiles one
     # wave of round-robin queues runs share group_m A panels and ~grid/group_m B panels in
     # L2; tile ids stay row-major (the dependency contract)
-    gm = max(1, int(cfg.get("group_m", 8)))
+    gm = max(1, int(cfg.get("group_m", os.environ.get("TF_LAYER_GROUP_M", 8))))
     for step in range(tm_n * tn_n):
         grp, r = divmod(step, gm * tn_n)
         rows = min(tm_n - grp * gm, gm)

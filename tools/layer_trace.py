@@ -45,6 +45,23 @@ for lid, nm in enumerate(names):
         "mean_wait_us": round(float(np.mean(sel[:, 4] - sel[:, 3])) / 1e3, 2),
         "mean_task_us": round(float(np.mean(sel[:, 5] - sel[:, 4])) / 1e3, 2),
         "sum_task_ms_over_ctas": round(float(np.sum(sel[:, 5] - sel[:, 4])) / 1e6 / r.num_sms, 3)})
+# wave coherence of each layer: the k-th task of a layer in every CTA's queue belongs to
+# wave k of the round-robin queues; spread of their start (deps satisfied) times
+for lid, nm in enumerate(names):
+    sel = tr[tr[:, 1] == lid]
+    if not len(sel) or "linear" not in nm:
+        continue
+    waves = {}
+    for c in np.unique(sel[:, 0]):
+        rows = sel[sel[:, 0] == c]
+        rows = rows[np.argsort(rows[:, 3])]
+        for k, row in enumerate(rows):
+            waves.setdefault(k, []).append(row[4])
+    task = float(np.mean(sel[:, 5] - sel[:, 4]))
+    spreads = [(max(v) - min(v)) / task for k, v in sorted(waves.items()) if len(v) > 1]
+    rep.setdefault("wave_start_spread_tasks", {})[nm] = {
+        "median": round(float(np.median(spreads)), 2), "max": round(float(np.max(spreads)), 2),
+        "waves": len(spreads)}
 busy_end = np.array([tr[tr[:, 0] == c][:, 5].max() - t0 for c in range(r.num_sms)]) / 1e3
 rep["cta_finish_us"] = {"min": float(busy_end.min()), "median": float(np.median(busy_end)),
                         "max": float(busy_end.max())}
