@@ -63,6 +63,7 @@ constexpr int kKVSlots = 4;                   // P lives in TMEM (over its S buf
 constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag before O is rescaled
 constexpr int kLayerSmem = 1024 + kRegion + 512;
 constexpr int kCfgInts = 16;
+constexpr int kThrottleTasks = 64;
 constexpr int kIntPerTask = 30;
 
 enum { OP_RMSNORM = 1, OP_LINEAR = 2, OP_ATTENTION = 3, OP_ALLREDUCE_RES = 4 };
@@ -80,6 +81,11 @@ struct LayerParams {
   int fixed_rank;            // IPC: this process's rank; local team: -1 (rank = cta / num_sms)
   const uint8_t* sm_die;     // die-ranked queues (one rank per launch): SM -> die table
   unsigned long long* die_ctr;  // and this launch's self-resetting counter, or nullptr
+  // linear-tile wave throttle (TF_LAYER_THROTTLE): [ranks in launch][kThrottleTasks] tiles
+  // started per task, zeroed before the launch; a CTA starts its k-th tile of a linear
+  // task only once k * num_sms - num_sms / 2 tiles of it have started, so the round-robin
+  // waves stay within ~1.5 waves of each other and their operand panels stay in L2
+  unsigned* lin_started;
   int world;
   uint64_t flag_base;
   unsigned long long epoch;
@@ -342,6 +348,10 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
     int stage = 0;
     uint32_t phase = 0;
     int kv_it = 0, att_it = 0, ring_base = 0;
+    __shared__ int ord[kThrottleTasks];  // this queue's linear tiles started so far, per task
+    if (lane == 0)
+      for (int i = 0; i < kThrottleTasks; ++i) ord[i] = 0;
+    __syncwarp();
     for (int idx = 0; idx < n_tasks; ++idx) {
       Rec r;
       load_rec(p, idx, sm, r);
@@ -367,6 +377,25 @@ __global__ void __launch_bounds__(kLThreads, 1) layer_megakernel(const __grid_co
         const CUtensorMap* ma = maps + __ldg(cfg + 5);
         const CUtensorMap* mb = maps + __ldg(cfg + 6);
         if (lane == 0) {
+          if (p.lin_started && r.task_id < kThrottleTasks) {
+            const int kk = ord[r.task_id]++;
+            unsigned* ctr = p.lin_started + rank * kThrottleTasks + r.task_id;
+            const long long need = static_cast<long long>(kk) * p.num_sms - p.num_sms / 2;
+            if (need > 0) {
+              const unsigned long long t0 = globaltimer_ns();
+              while (true) {
+                unsigned v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                if (static_cast<long long>(v) >= need) break;
+                __nanosleep(64);
+                if (globaltimer_ns() - t0 > p.timeout_ns) {
+                  atomicCAS(reinterpret_cast<unsigned long long*>(p.err[rank]), 0ull, 0x7100000ull | r.task_id);
+                  break;
+                }
+              }
+            }
+            atomicAdd(ctr, 1u);
+          }
           if (waited) fence_proxy_async_global();
           for (int kb = 0; kb < k / 64; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -1120,6 +1149,32 @@ extern "C" int tf_layer_megakernel_run(tf_team* t, int rank, const tf_layer_args
   }
   p.trace = reinterpret_cast<unsigned long long*>(a->trace);
   p.slots = a->trace_slots;
+  {
+    static const bool thr_on = [] {
+      const char* e = getenv("TF_LAYER_THROTTLE");
+      return !e || atoi(e) != 0;
+    }();
+    if (thr_on) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      static std::mutex thr_mu;
+      static std::map<int, unsigned*> thr_bufs;
+      unsigned* buf = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(thr_mu);
+        auto it = thr_bufs.find(cur);
+        if (it == thr_bufs.end()) {
+          TF_CUDA_TRY(cudaMalloc(&buf, static_cast<size_t>(tf::kMaxWorld) * tf::kThrottleTasks * 4));
+          thr_bufs[cur] = buf;
+        } else {
+          buf = it->second;
+        }
+      }
+      TF_CUDA_TRY(cudaMemsetAsync(buf, 0, static_cast<size_t>(nranks) * tf::kThrottleTasks * 4,
+                                  static_cast<cudaStream_t>(stream)));
+      p.lin_started = buf;
+    }
+  }
   if (grid == a->num_sms) {  // one rank's queues per launch: rank them by die (TF_LAYER_DIE=0 off)
     static const bool die_on = [] {
       const char* e = getenv("TF_LAYER_DIE");
