@@ -50,6 +50,10 @@ constexpr int kDefaultDieMode = 1;         // die-ranked cluster ids (TF_GEMM_DI
 #define TF_GEMM_EARLY_RELEASE 1
 #endif
 constexpr bool kEarlyRelease = TF_GEMM_EARLY_RELEASE;  // epilogue frees TMEM before its stores
+#ifndef TF_GEMM_RELAXED_ARRIVE
+#define TF_GEMM_RELAXED_ARRIVE 1
+#endif
+constexpr bool kRelaxedArrive = TF_GEMM_RELAXED_ARRIVE;  // "accumulator free" without MEMBAR.GPU
 #ifndef TF_GEMM_LAG
 #define TF_GEMM_LAG 2                  // k-blocks the second M-half trails at tile edges
 #endif
@@ -762,7 +766,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     (static_cast<unsigned long long>(pid_m) << 32) | static_cast<unsigned>(pid_n));
         const int b = MH == 2 ? h : acc;
         if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_cluster_relaxed(tempty_leader + b * 8);
+          if constexpr (CG == 2) {
+            if constexpr (kRelaxedArrive) mbar_arrive_cluster_relaxed(tempty_leader + b * 8);
+            else mbar_arrive_cluster(tempty_leader + b * 8);
+          }
           else mbar_arrive(&tempty_bar[b]);
         }
       };
