@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kCluster = CG * NPAIR;
   const int num_clusters = (static_cast<int>(gridDim.x) - p.comm_ctas) / kCluster;
   int* vcid_slot = reinterpret_cast<int*>(tmem_slot + 2);  // spare word after the TMEM slot
-  if (!GROUPED && p.die_mode && threadIdx.x == 0 && cta_rank == 0) {
+  if (p.die_mode && threadIdx.x == 0 && cta_rank == 0) {
     // die-ranked cluster id: die-0 clusters count up from 0, die-1 clusters down from
     // num_clusters - 1 (a bijection whatever the arrival order); the last arrival
     // resets the counter for the next launch that uses this slot
@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   int cluster_id = (static_cast<int>(blockIdx.x) - p.comm_ctas) / kCluster;
-  if (!GROUPED && p.die_mode) {
+  if (p.die_mode) {
     if (cta_rank == 0) {
       cluster_id = *vcid_slot;
     } else {
@@ -1213,8 +1213,9 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
     if (grid > cap) grid = cap;
   }
   KParams kd = kp;
-  if (!GROUPED) {
+  {
     // die-ranked cluster ids (tf_topo.cu); TF_GEMM_DIE = 0 off, 1 ranked, 2 ranked + row split
+    // (the row split is for the grouped raster of plain GEMMs only)
     static const int die_env = [] {
       const char* e = getenv("TF_GEMM_DIE");
       return e ? atoi(e) : kDefaultDieMode;
@@ -1225,7 +1226,7 @@ int launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
       if (tab) {
         kd.sm_die = tab;
         kd.die_ctr = slot;
-        kd.die_mode = die_env;
+        kd.die_mode = GROUPED ? 1 : die_env;
       }
     }
   }
