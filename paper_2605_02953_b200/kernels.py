@@ -250,6 +250,28 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *,
 
 
 # ----------------------------------------------------------------- AllGather + GEMM
+# Teams (symmetric heaps + flags) of the drop-in entry points are cached per (op,
+# world, devices, heap size, slots), so repeated calls of the same shape reuse the
+# peer mappings and workspaces instead of rebuilding them (the reference builds a
+# heap per call, ag_gemm.py:35; here that is a one-time cost).  Epoch-valued flags make
+# back-to-back reuse safe.  TF_TEAM_CACHE=0 restores a fresh team per call.
+_TEAM_CACHE: "dict" = {}
+_TEAM_CACHE_MAX = 4
+
+
+def _cached_team(op, world, devices, heap_bytes, slots):
+    if os.environ.get("TF_TEAM_CACHE", "1") == "0":
+        return Team(world, devices, heap_bytes, slots)
+    key = (op, world, tuple(devices), int(heap_bytes), int(slots))
+    team = _TEAM_CACHE.pop(key, None)
+    if team is None:
+        team = Team(world, devices, heap_bytes, slots)
+        while len(_TEAM_CACHE) >= _TEAM_CACHE_MAX:  # evict the least recently used
+            _TEAM_CACHE.pop(next(iter(_TEAM_CACHE))).close()
+    _TEAM_CACHE[key] = team  # most recently used last
+    return team
+
+
 def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     """Per rank r: C_r = concat(a_0..a_{w-1}) @ b_r.T, shape [M, N_per_rank]."""
     topo = ctx.topology
@@ -273,7 +295,7 @@ def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     odt = _out_dtype(ctx.out_dtype, pa)
     kp = pa.kdim
     heap_bytes = 2 * m * kp * 2 + (1 << 20)
-    team = Team(world, devices, heap_bytes, 4 * world + 64)
+    team = _cached_team("ag_gemm", world, devices, heap_bytes, 4 * world + 64)
     heap = SymmetricHeap(topo, team=team)
     outs, args, keep = [], {}, []
     for r in range(world):
@@ -331,7 +353,7 @@ def gemm_rs(input_shards, weight_shards, ctx: WorkloadContext,
     ld = (n + 7) // 8 * 8
     heap_bytes = m * ld * esz + (1 << 20)
     num_pid_m = (m + BM - 1) // BM
-    team = Team(world, devices, heap_bytes, num_pid_m + 64)
+    team = _cached_team(f"gemm_rs:{bool(ctx.fuse_scatter)}", world, devices, heap_bytes, num_pid_m + 64)
     heap = SymmetricHeap(topo, team=team)
     outs, args, keep = [], {}, []
     for r in range(world):
@@ -498,7 +520,7 @@ def gemm_allreduce(a_shards, b_shards, ctx: WorkloadContext, use_multimem_st: bo
     esz = 4 if odt == torch.float32 else 2
     ld = (n + 7) // 8 * 8
     nblocks = (m + 127) // 128
-    team = Team(world, devices, 2 * m * ld * esz + (1 << 20), 2 * nblocks + 64)
+    team = Team(world, devices, 2 * m * ld * esz + (1 << 20), 2 * nblocks + 64)  # may bind an NVLS region
     if two_shot and team.distinct_devices and world > 1 and os.environ.get("TF_NVLS", "1") != "0":
         # two-shot through the switch (multimem.ld_reduce + multimem.st) when the
         # box exposes NVLS; otherwise the P2P owner-reduce + broadcast below
