@@ -26,6 +26,7 @@
 // O_B [384,512).  An opt-in CTA-pair variant (TF_ATTN_PAIR=1) splits K and V
 // across two CTAs with cta_group::2 MMAs.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -69,14 +70,26 @@ struct AttnParams {
 // Two 128-query tiles (A, B) per CTA share every K/V tile; each has its own
 // softmax warpgroup, S and O in TMEM, and P buffer in smem, so the tensor pipe
 // runs one tile's QK^T / PV while the other tile's softmax is on the ALUs.
+// TF_ATTN_SPLIT_ROWS=2 (opt-in): eight softmax warps per query tile, two per TMEM lane
+// quarter, each taking 64 of a row's 128 keys (the row max combined through shared
+// memory).  Measured slower than four warps per tile (3.89 vs 3.47 ms per rank).
+#ifndef TF_ATTN_SPLIT_ROWS
+#define TF_ATTN_SPLIT_ROWS 1  // 2 measured slower: 3.89 vs 3.47 ms per rank (same box)
+#endif
+constexpr int kRowSplit = TF_ATTN_SPLIT_ROWS;
 struct AttnSmem {
   static constexpr int kQ = 2 * kHalf;        // one Q tile, 32 KB
   static constexpr int kSlot = 2 * kHalf;     // one K or V tile (128 keys x 128 dims), 32 KB
   static constexpr int kSlots = 5;            // ring K0 V0 K1 V1 ...
   static constexpr int kBars = 256;
-  static constexpr int kTotal = 1024 + 2 * kQ + kSlots * kSlot + kBars;
+  // row-max halves, bf16 [j & 1][tile][half][row] (the same two values give every warp of a
+  // row the same max); reused as fp32 [tile][half][row] row sums at the end
+  static constexpr int kXchg = kRowSplit == 2 ? 2 * 2 * 2 * 128 * 2 : 0;
+  // no alignment slack in the split variant (dynamic smem starts 1 KB-aligned: checked)
+  static constexpr int kSlack = kRowSplit == 2 ? 0 : 1024;
+  static constexpr int kTotal = kSlack + 2 * kQ + kSlots * kSlot + kBars + kXchg;
 };
-constexpr int kAttnThreads2 = 320;            // TMA, MMA, 2 x 4 softmax warps
+constexpr int kAttnThreads2 = 64 + 2 * 4 * kRowSplit * 32;  // TMA, MMA, 2 tiles x 4 x split softmax warps
 constexpr float kLazyRescale = 8.0f;          // log2 units the running max may lag (FA4)
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
@@ -320,13 +333,16 @@ __device__ long long g_attn_trace[512][20];
 #define ATTN_GSTAMP(j, e) do { } while (0)
 #endif
 
-__global__ void __maxnreg__(168)
+__global__ void __launch_bounds__(kAttnThreads2, 1)
     ag_attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ AttnParams p) {
   using S = AttnSmem;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  if constexpr (S::kSlack == 0) {
+    if (smem != smem_raw) __trap();  // the layout above has no room to realign
+  }
   uint8_t* sq = smem;                               // Q_A, Q_B
   uint8_t* sring = sq + 2 * S::kQ;                  // 5 slots: K0 V0 K1 V1 ...
   uint64_t* bars = reinterpret_cast<uint64_t*>(sring + S::kSlots * S::kSlot);
@@ -356,7 +372,7 @@ __global__ void __maxnreg__(168)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_half[i], 4);
+      mbar_init(&p_half[i], 4 * kRowSplit);  // split: half-1 warps also report "O rescaled"
       mbar_init(&o_ready[i], 1);
     }
     fence_barrier_init();
@@ -473,6 +489,118 @@ __global__ void __maxnreg__(168)
       }
     }
     __syncwarp();
+  } else if constexpr (kRowSplit == 2) {
+    // two warps per TMEM lane quarter and tile: half h takes keys / O columns [64h, 64h+64)
+    const int t = (warp - 2) >> 3;                 // Q tile of this warp
+    const int half = ((warp - 2) >> 2) & 1;
+    if (t < nq) {
+      const int quarter = warp & 3;
+      const int row = quarter * 32 + lane;
+      const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+      const uint32_t t_s = tmem + lane_off + t * 128;
+      const uint32_t t_o = tmem + lane_off + 256 + t * 128 + half * 64;
+      // [j & 1][tile][half][row] bf16 row maxima, rounded up (both warps of a row then
+      // derive the same max from the same two values)
+      __nv_bfloat16* xm = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<uint8_t*>(bars) + S::kBars);
+      const uint32_t bar_id = 1 + t * 4 + quarter;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < n; ++j) {
+        SM_WAIT(&s_full[t], j & 1);
+        tc_fence_after();
+        uint32_t sv[2][32];
+        tmem_ld_32x32b_x32(t_s + half * 64, sv[0]);
+        tmem_ld_32x32b_x32(t_s + half * 64 + 32, sv[1]);
+        tmem_ld_wait();
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; i += 2)
+            mx[c] = fmax3(mx[c], __uint_as_float(sv[c][i]), __uint_as_float(sv[c][i + 1]));
+        __nv_bfloat16* x = xm + ((j & 1) * 2 + t) * 256;
+        x[half * 128 + row] = __float2bfloat16_ru(fmaxf(mx[0], mx[1]));
+        // both warps of these rows hold their S in registers from here on (P may overwrite S)
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float mt = fmaxf(__bfloat162float(x[row]), __bfloat162float(x[128 + row])) * p.scale_log2;
+        float alpha = 1.f;
+        if (mt > m + kLazyRescale) {
+          alpha = ex2(m - mt);
+          m = mt;
+        }
+        // O_t is stable (S_t(j) complete implies PV_t(j-1) complete): rescale this half
+        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[16];
+            tmem_ld_32x32b_x16(t_o + c * 16, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st_32x32b_x16(t_o + c * 16, ov);
+          }
+          tmem_st_wait();
+        }
+        if (half == 1) {  // "O rescaled" for the first PV half (keys 0-63 come from half 0)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_half[t]);
+        }
+        uint64_t sum2 = f2pack(0.f, 0.f);
+        const uint64_t scale2 = f2pack(p.scale_log2, p.scale_log2), negm2 = f2pack(-m, -m);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float a0, a1;
+            f2unpack(ffma2(f2pack(__uint_as_float(sv[c][2 * i]), __uint_as_float(sv[c][2 * i + 1])), scale2,
+                           negm2),
+                     a0, a1);
+            float p0, p1;
+            if (TF_EXP2_EMU_MASK >= 0 && (i & TF_EXP2_EMU_MASK) == 0) {
+              ex2_fma2(a0, a1, p0, p1);
+            } else {
+              p0 = ex2(a0);
+              p1 = ex2(a1);
+            }
+            sum2 = fadd2(sum2, f2pack(p0, p1));
+            sv[0][c * 16 + i] = pack_bf16x2(p0, p1);
+          }
+        tmem_st_32x32b_x32(t_s + half * 32, sv[0]);  // P keys [64 half, +64) as bf16 pairs
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(half == 0 ? &p_half[t] : &p_full[t]);
+        float s0, s1;
+        f2unpack(sum2, s0, s1);
+        l = l * alpha + (s0 + s1);
+      }
+      mbar_wait_spin(&o_ready[t], 0);
+      tc_fence_after();
+      // row sums through this tile's own exchange slots ([parity h][tile t] holds half h's
+      // 128 floats): the other tile's warps may still be in their loop
+      float* lsum = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + S::kBars);
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      lsum[(half * 2 + t) * 128 + row] = l;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      const float inv = 1.f / (lsum[t * 128 + row] + lsum[(2 + t) * 128 + row]);
+      const int q = q0 + t * kQT + row;
+      uint16_t* dst = static_cast<uint16_t*>(p.out) + (static_cast<long long>(q) * p.hq + h) * kD + half * 64;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ov[32];
+        tmem_ld_32x32b_x32(t_o + c * 32, ov);
+        tmem_ld_wait();
+        if (q < p.s_local) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            d4[i] = make_uint4(pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
+                               pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+        }
+      }
+    }
   } else {
     const int t = (warp - 2) >> 2;                 // Q tile of this warpgroup
     if (t < nq) {
@@ -1342,7 +1470,7 @@ extern "C" int tf_ag_kv_attention(tf_team* t, int rank, const tf_attn_fwd_args* 
     if (pair) {
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(static_cast<unsigned>(2 * sl / ((pair2 ? 2 : 4) * tf::kQT)), static_cast<unsigned>(a->hq));
-      cfg.blockDim = dim3(pair2 ? tf::kAttnPair2Threads : tf::kAttnThreads2);
+      cfg.blockDim = dim3(pair2 ? tf::kAttnPair2Threads : 320);
       cfg.dynamicSmemBytes = pair2 ? tf::AttnPair2Smem::kTotal : tf::AttnPairSmem::kTotal;
       cfg.stream = s;
       cudaLaunchAttribute attr[1];
