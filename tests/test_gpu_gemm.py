@@ -320,3 +320,26 @@ def test_float32_ag_gemm_fp32_accuracy(world, mpr, n, k):
         want = full @ b[r].astype(np.float64).T
         assert run.outputs[r].dtype == np.float32
         assert _norm_rel_err(run.outputs[r], want) <= 3e-5
+
+
+def test_drop_in_team_cache_reuse_is_exact():
+    """Repeated drop-in calls of one shape reuse a cached team (heap, flags, workspaces);
+    alternating fused / unfused GEMM-RS and interleaved AG-GEMM calls stay bit-exact."""
+    K = _k()
+    rng = np.random.default_rng(21)
+    world, mpr, n, k = 4, 128, 256, 192
+    for it in range(3):
+        a = [rng.integers(-8, 8, (mpr, k)).astype(np.int64) for _ in range(world)]
+        b = [rng.integers(-8, 8, (n, k)).astype(np.int64) for _ in range(world)]
+        run = K.ag_gemm(a, b, _ctx(world))
+        for got, want in zip(run.outputs, O.ref_allgather_gemm(a, b)):
+            assert np.array_equal(got, want), it
+        x = [rng.integers(-8, 8, (world * mpr, k)).astype(np.int64) for _ in range(world)]
+        w = [rng.integers(-8, 8, (n, k)).astype(np.int64) for _ in range(world)]
+        for fused in (True, False):
+            ctx = _ctx(world)
+            ctx.fuse_scatter = fused
+            run = K.gemm_rs(x, w, ctx)
+            for got, want in zip(run.outputs, O.ref_reduce_scatter(x, w)):
+                assert np.array_equal(got, want), (it, fused)
+    assert len(K._TEAM_CACHE) <= K._TEAM_CACHE_MAX
