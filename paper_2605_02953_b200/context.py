@@ -42,6 +42,9 @@ class WorkloadContext:
     seed: int = 0
     devices: list | None = None
     out_dtype: str | None = None
+    # B200 extension: how ag_gemm gathers -- "ce" (copy-engine pulls on a side stream,
+    # flags per row slice) or "sm" (num_comm_sms pull-engine CTAs inside the GEMM launch)
+    ag_pull: str = "ce"
 
     def __post_init__(self):
         if min(self.block_m, self.block_n, self.block_k, self.group_m) < 1:
@@ -53,6 +56,8 @@ class WorkloadContext:
                               f"{self.topology.num_sms} SMs per rank")
         if self.reduce_order not in REDUCE_ORDERS:
             raise ConfigError(f"reduce_order must be one of {REDUCE_ORDERS}")
+        if self.ag_pull not in ("ce", "sm"):
+            raise ConfigError("ag_pull must be 'ce' or 'sm'")
         if self.out_dtype not in (None, "bf16", "f32"):
             raise ConfigError("out_dtype must be None, 'bf16' or 'f32'")
         if self.devices is not None and len(self.devices) != self.topology.world_size:

@@ -294,6 +294,28 @@ def ag_gemm(a_shards, b_shards, ctx: WorkloadContext) -> WorkloadRun:
     _exact_bound_check(pa, pb, k)
     odt = _out_dtype(ctx.out_dtype, pa)
     kp = pa.kdim
+    if ctx.ag_pull == "sm" and m_per_rank > 0 and n_per_rank > 0:
+        # in-kernel gather: num_comm_sms pull-engine CTAs + the GEMM in one launch per rank
+        from .moe import _agmoe_heap_bytes
+        bm = 256 if ctx.hw_block_m >= 256 else 128
+        n_pad = max((n_per_rank + 7) // 8 * 8, 8)
+        team = _cached_team("ag_gemm_pull", world, devices, _agmoe_heap_bytes(m, kp, 1, world, bm), 4 * world + 64)
+        heap = SymmetricHeap(topo, team=team)
+        op = AllGatherGemm(team, m, kp, n_pad, out_dtype=odt, block_m=bm, block_n=ctx.hw_block_n,
+                           num_gemm_sms=ctx.num_gemm_sms, swizzle=ctx.swizzle,
+                           num_comm_sms=max(1, ctx.num_comm_sms))
+        wts = []
+        for r in range(world):
+            w = pb.tensors[r]
+            if n_pad != n_per_rank:
+                w = torch.cat([w, torch.zeros((n_pad - n_per_rank, kp), dtype=w.dtype, device=w.device)])
+            wts.append(w.contiguous())
+        outs = [torch.zeros((m, n_pad), dtype=odt, device=f"cuda:{devices[r]}") for r in range(world)]
+        op.forward([pa.tensors[r] for r in range(world)], wts, out=outs)
+        for d in sorted(set(devices)):
+            torch.cuda.synchronize(d)
+        team.check()
+        return WorkloadRun([_finish(o[:, :n_per_rank], pa) for o in outs], None, heap, {})
     heap_bytes = 2 * m * kp * 2 + (1 << 20)
     team = _cached_team("ag_gemm", world, devices, heap_bytes, 4 * world + 64)
     heap = SymmetricHeap(topo, team=team)
@@ -402,10 +424,25 @@ class AllGatherGemm:
 
     def __init__(self, team: Team, m: int, k: int, n_local: int, *, out_dtype=torch.bfloat16,
                  block_m: int = 512, block_n: int = 256, group_m: int = 8,
-                 num_gemm_sms: int = 0, swizzle: bool = True, nnodes: int = 1):
+                 num_gemm_sms: int = 0, swizzle: bool = True, nnodes: int = 1,
+                 num_comm_sms: int = 0):
         if k % 8:
             raise ValueError("K must be a multiple of 8")
         self.team, self.m, self.k, self.n = team, m, k, n_local
+        # num_comm_sms > 0: the gather runs INSIDE the GEMM launch -- that many pull-engine
+        # CTAs copy the peers' chunks ((rank+i)%w order) over NVLink into the workspace and
+        # release per-source arrival counters the GEMM tiles wait on (the reference's
+        # _pull_engine process, ag_gemm.py:55-69, as SM work).  This is the grouped
+        # AG-GEMM kernel with a single group (tf_ag_moe_group_gemm, E = 1).
+        self._pull = None
+        if num_comm_sms > 0:
+            from .moe import AgMoeGroupGemm
+            if m % team.world:
+                raise ValueError("M must divide across ranks")
+            self._pull = AgMoeGroupGemm(team, 1, n_local, k, m, block_m=256 if block_m >= 256 else 128,
+                                        block_n=block_n, num_gemm_sms=num_gemm_sms,
+                                        num_comm_sms=num_comm_sms, swizzle=swizzle, out_dtype=out_dtype)
+            self._routing = np.full((team.world, 1), m // team.world, dtype=np.int64)
         self.out_dtype = out_dtype
         self.block_m, self.block_n = block_m, block_n
         # a raster group must not span more than one gathered chunk: with the gather
@@ -426,6 +463,10 @@ class AllGatherGemm:
 
     def forward(self, a, b, out=None):
         t = self.team
+        if self._pull is not None:
+            if isinstance(b, torch.Tensor):
+                return self._pull(self._routing, a, b.unsqueeze(0), out=out)
+            return self._pull(self._routing, list(a), [x.unsqueeze(0) for x in b], out=out)
         if t.rank is not None or (t.world == 1 and isinstance(a, torch.Tensor)):
             r = t.rank or 0
             if out is None:

@@ -343,3 +343,41 @@ def test_drop_in_team_cache_reuse_is_exact():
             for got, want in zip(run.outputs, O.ref_reduce_scatter(x, w)):
                 assert np.array_equal(got, want), (it, fused)
     assert len(K._TEAM_CACHE) <= K._TEAM_CACHE_MAX
+
+
+@pytest.mark.parametrize("case", range(12))
+@pytest.mark.parametrize("comm", [1, 8])
+def test_ag_gemm_in_kernel_pull_exact_vs_reference_fixture(case, comm):
+    """ag_pull="sm": the gather runs inside the GEMM launch (pull-engine CTAs), bit-exact
+    with the reference's outputs on its fixtures."""
+    c = G.workloads()[case]
+    K = _k()
+    w = c["world"]
+    ctx = _ctx(w, ag_pull="sm", num_comm_sms=comm, block_m=256)
+    run = K.ag_gemm(list(c["ag_a"]), list(c["ag_b"]), ctx)
+    for r in range(w):
+        assert run.outputs[r].dtype == np.int64
+        assert np.array_equal(run.outputs[r], c["ag_c"][r]), (case, r)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_all_gather_gemm_in_kernel_pull_bf16(world):
+    """Persistent AllGatherGemm with num_comm_sms > 0 (in-kernel pulls) vs the fp32 reference."""
+    from paper_2605_02953_b200.kernels import AllGatherGemm
+    from paper_2605_02953_b200.shmem import Team
+    rng = np.random.default_rng(world)
+    m, k, n = 512 * world, 512, 768
+    team = Team(world, devices_for(world), heap_bytes=4 * m * k * 2 + (8 << 20), signal_slots=1024)
+    op = AllGatherGemm(team, m, k, n, num_comm_sms=4)
+    a = [_bf16(rng, (m // world, k)).cuda() for _ in range(world)]
+    b = [_bf16(rng, (n, k), k ** -0.5).cuda() for _ in range(world)]
+    for _ in range(2):  # second call: next epoch of the same workspace
+        outs = op.forward(a, b)
+        torch.cuda.synchronize()
+        team.check()
+        full = torch.cat(a).float()
+        for r in range(world):
+            want = full @ b[r].float().T
+            err = (outs[r].float() - want).abs().max().item() / want.abs().max().item()
+            assert err <= 2e-2, (r, err)
+    team.close()
