@@ -925,6 +925,7 @@ def main_ours(args):
     y = torch.empty(mpr, HIDDEN, dtype=torch.bfloat16, device=f"cuda:{dev}")
 
     heap = 2 * m * HIDDEN * 2 + m * ((HIDDEN + 7) // 8 * 8) * 2 + (64 << 20)
+    heap += 2 * m * HIDDEN * 2 + (16 << 20)  # in-kernel-pull AG variant (ag_sm_pull below)
     if not args.no_moe:  # EP receive + expert-output buffers (worst case: every token to one rank)
         heap += 2 * MOE_T * MOE_K * world * MOE_H * 2 + (8 << 20)
     if distributed:
@@ -1003,6 +1004,31 @@ def main_ours(args):
         torch.cuda.synchronize()
         clk = clocks.stop(t_clk0, t_clk1)
     team.check()
+    # AG-GEMM with the gather inside the GEMM launch (16 pull-engine CTAs; copy-engine
+    # pulls above): same flush/event protocol, reported beside the main line
+    ag_sm = None
+    try:
+        ag_pull = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, num_comm_sms=16)
+        h2 = torch.empty_like(h)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                ag_pull.forward(x, w1, h2)
+            torch.cuda.synchronize()
+            barrier()
+            evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(max(3, args.steps // 2))]
+            for e0, e1 in evp:
+                flush.zero_()
+                e0.record(stream)
+                ag_pull.forward(x, w1, h2)
+                e1.record(stream)
+            torch.cuda.synchronize()
+        team.check()
+        sm_ms = max_over_ranks([sum(a.elapsed_time(b) for a, b in evp) / len(evp)], dev, distributed)[0]
+        ag_sm = {"impl": "AllGatherGemm(num_comm_sms=16): gather by pull-engine CTAs inside the GEMM launch",
+                 "ms": round(sm_ms, 4), "tflops_per_rank": round(2.0 * m * f_tp * HIDDEN / (sm_ms * 1e-3) / 1e12, 2)}
+    except Exception as exc:  # noqa: BLE001
+        ag_sm = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     ag_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(n_events)]
     rs_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(n_events)]
     step_ms = sum(a + b for a, b in zip(ag_ms, rs_ms)) / n_events
@@ -1201,6 +1227,7 @@ def main_ours(args):
                 "speedup": round(cub_ms / step_ms, 4)},
             "overlap": overlap,
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "moe": moe, "ag_moe": agmoe, "attention": attn, "layer": layer,
+            "ag_sm_pull": ag_sm,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(line), flush=True)
