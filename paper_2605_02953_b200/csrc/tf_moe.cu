@@ -557,7 +557,13 @@ __global__ void release_kernel(PeerSig flags, int world, int rank, uint64_t epoc
 constexpr int kFdWarps = 12;
 constexpr int kFdBuf = 8192;            // bytes per row piece buffer (two per warp)
 constexpr int kFdEntCap = 1024;         // (token, slot) entries per CTA
-constexpr int kFdDoneSlot = 1023;       // gflags[1023]: CTAs done scattering (grid <= 1023)
+constexpr int kFdDoneSlot = 1023;
+constexpr int kFdMaxNb = 4;             // most row-piece buffers per warp
+constexpr int kFdReadyBase = 1024;      // gflags[1024 + c]: CTA c's destination rows are in dest_row
+constexpr int kFdTicket = 2048;         // gflags[2048]: next (token, piece) ticket of the launch
+constexpr int kFdRedBase = 2064;        // gflags[2064 + q]: column reducer q published
+constexpr int kFdFlagWords = 2368;
+constexpr int64_t kFdHistInts = 1023LL * 1024;  // chunk_hist [G][Ep]; then the prefixes, then the totals       // gflags[1023]: CTAs done scattering (grid <= 1023)
 
 struct FusedDispatch {
   const uint4* x;
@@ -583,6 +589,9 @@ struct FusedDispatch {
   unsigned long long* err;
   unsigned long long timeout_ns;
   int dbg;                              // timing experiments only (TF_MOE_FD_DEBUG): 1 no scatter, 2 no grid wait
+  int nb;                               // row piece buffers per warp (2..4), sharing the warp's 2 * kFdBuf bytes
+  int dyn;                              // 1: pieces handed out by a grid-wide ticket counter (PRE+MAIN launches)
+  int reduce;                           // 1: column-reducer CTAs publish the chunk prefixes (else every CTA sums)
 };
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const unsigned long long* p) {
@@ -607,13 +616,14 @@ size_t fused_dispatch_smem(int E) {
 template <int VPL>  // VPL 0: routing given
 __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const FusedDispatch p) {
   extern __shared__ __align__(128) uint8_t fsm_raw[];
-  __shared__ uint64_t bars[2 * kFdWarps];
+  __shared__ uint64_t bars[kFdMaxNb * kFdWarps];  // [warp][buffer]: row piece landed
+  __shared__ uint64_t rbars[kFdWarps];            // [warp]: logits rows landed (routing)
   __shared__ uint4* sdst[kFdWarps][16];
   __shared__ int32_t last_tot;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nw = kFdWarps;
   const int E = p.E, k = p.k, G = gridDim.x, c = blockIdx.x;
-  uint8_t* bufs = fsm_raw;                                     // [nw][2][kFdBuf]
+  uint8_t* bufs = fsm_raw;                                     // [nw][2 * kFdBuf]
   int32_t* wc = reinterpret_cast<int32_t*>(fsm_raw + 2 * nw * kFdBuf);  // [nw][E]
   int32_t* cnt = wc + fd_wc_ints(E);                           // [E]
   int32_t* tot = cnt + E;                                      // [E]
@@ -628,31 +638,58 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
   const int nt = t_end > t0 ? static_cast<int>(t_end - t0) : 0;
   const int ent = nt * k;
   const int epr = E / p.world;
-  constexpr int64_t kPiece = kFdBuf / 16;
-  const int64_t npieces = (p.vec_per_row + kPiece - 1) / kPiece;
+  // the warp's 2 * kFdBuf bytes hold NB row-piece buffers; rows split into equal
+  // 16-byte-multiple pieces that fit one buffer
+  // dynamic pieces: every launch that runs PRE and MAIN (gepoch is fresh) and scatters
+  const bool dyn = p.dyn && (p.mode & 3) == 3 && !(p.dbg & 1);
+  const int NB = dyn ? 2 : p.nb < 2 ? 2 : p.nb > kFdMaxNb ? kFdMaxNb : p.nb;
+  const uint32_t buf_bytes = (2u * kFdBuf / NB) & ~15u;
+  const int64_t npieces = (p.vec_per_row + buf_bytes / 16 - 1) / (buf_bytes / 16);
+  const int64_t kPiece = (p.vec_per_row + npieces - 1) / npieces;  // vectors per piece
   const int ntasks = (p.dbg & 1) ? 0 : static_cast<int>(nt * npieces);
+  uint8_t* wbuf = bufs + static_cast<size_t>(warp) * 2 * kFdBuf;
+  // TF_MOE_FD_DEBUG bit 3: every CTA prints its SM, phase clocks and %globaltimer at
+  // start / histogram published / counts released / exit (tools/moe_stamps.py)
+  const uint64_t g_start = (p.dbg & 8) ? globaltimer_ns() : 0;
+  uint64_t g_arrive = 0, g_release = 0;
+  const long long stamp_all0 = clock64();
+  long long stamp_all_mid = 0;
   if (lane == 0) {
-    mbar_init(&bars[2 * warp], 1);
-    mbar_init(&bars[2 * warp + 1], 1);
+    for (int b = 0; b < NB; ++b) mbar_init(&bars[kFdMaxNb * warp + b], 1);
+    mbar_init(&rbars[warp], 1);
     fence_barrier_init();
   }
   __syncwarp();
-  auto piece_bytes = [&](int ti) {
+  auto piece_bytes = [&](int64_t ti) {
     const int64_t v0 = (ti % npieces) * kPiece;
     return static_cast<uint32_t>((min(v0 + kPiece, p.vec_per_row) - v0) * 16);
   };
-  auto issue_load = [&](int ti, int b) {  // lane 0 only
-    const int64_t t = t0 + ti / npieces, v0 = (ti % npieces) * kPiece;
+  const int64_t dyn_total = p.tokens * npieces;  // tickets of the launch (dyn)
+  auto issue_load = [&](int64_t ti, int b) {  // lane 0 only; ti: CTA-local task, or a global ticket (dyn)
+    const int64_t t = (dyn ? 0 : t0) + ti / npieces, v0 = (ti % npieces) * kPiece;
     const uint32_t bytes = piece_bytes(ti);
-    mbar_arrive_expect_tx(&bars[2 * warp + b], bytes);
+    mbar_arrive_expect_tx(&bars[kFdMaxNb * warp + b], bytes);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(bufs + (2 * warp + b) * kFdBuf)),
-        "l"(p.x + t * p.vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bars[2 * warp + b]))
+            smem_u32(wbuf + b * buf_bytes)),
+        "l"(p.x + t * p.vec_per_row + v0), "r"(bytes), "r"(smem_u32(&bars[kFdMaxNb * warp + b]))
         : "memory");
   };
-  if ((p.mode & 2) && lane == 0 && warp < ntasks) issue_load(warp, 0);  // prefetch under PRE
-  uint32_t ph1 = 0;  // parity of buffer 1's barrier
+  // buffer 0 (the first buffer_bytes <= kFdBuf of the warp's region) loads under PRE;
+  // the routing below stages logits in the region's second half
+  int64_t cur = 0;  // dyn: this warp's current ticket (drawn before PRE, its row loads under PRE)
+  if (dyn) {
+    if (lane == 0) {
+      cur = static_cast<int64_t>(atomicAdd(p.gflags + kFdTicket, 1ull));
+      if (cur < dyn_total) issue_load(cur, 0);
+      // every warp draws exactly one ticket past the end; the last such draw resets the
+      // counter for the next launch (stream-ordered after this one)
+      else if (cur == dyn_total + static_cast<int64_t>(G) * nw - 1) p.gflags[kFdTicket] = 0;
+    }
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+  } else if ((p.mode & 2) && lane == 0 && warp < ntasks) {
+    issue_load(warp, 0);
+  }
 
   if (p.mode & 1) {
     // ---- routing of this CTA's tokens
@@ -663,21 +700,22 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       const uint32_t rb = static_cast<uint32_t>(E) * 4;
       const bool bulk = (rb % 16) == 0 && (reinterpret_cast<uintptr_t>(p.logits) % 16) == 0;
       const int per_round = bulk ? static_cast<int>(kFdBuf / rb) : 1;
-      const float* lbuf = reinterpret_cast<const float*>(bufs + (2 * warp + 1) * kFdBuf);
+      const float* lbuf = reinterpret_cast<const float*>(wbuf + kFdBuf);
+      uint32_t rph = 0;
       for (int j0 = 0; warp + j0 * nw < nt; j0 += per_round) {
         const int nr = min(per_round, (nt - warp + nw - 1) / nw - j0);
         if (bulk) {
           if (lane == 0) {
-            mbar_arrive_expect_tx(&bars[2 * warp + 1], rb * nr);
+            mbar_arrive_expect_tx(&rbars[warp], rb * nr);
             for (int j = 0; j < nr; ++j)
               asm volatile(
                   "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                       smem_u32(lbuf) + j * rb),
-                  "l"(p.logits + (t0 + warp + (j0 + j) * nw) * E), "r"(rb), "r"(smem_u32(&bars[2 * warp + 1]))
+                  "l"(p.logits + (t0 + warp + (j0 + j) * nw) * E), "r"(rb), "r"(smem_u32(&rbars[warp]))
                   : "memory");
           }
-          mbar_wait(&bars[2 * warp + 1], ph1);
-          ph1 ^= 1;
+          mbar_wait(&rbars[warp], rph);
+          rph ^= 1;
         }
         for (int j = 0; j < nr; ++j) {
           const int tt = warp + (j0 + j) * nw;
@@ -725,24 +763,81 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       __syncthreads();
     }
     __syncthreads();
-    // ---- publish the chunk histogram, wait for every chunk
+    // ---- publish the chunk histogram
     for (int x = tid; x < Ep; x += blockDim.x) p.chunk_hist[static_cast<int64_t>(c) * Ep + x] = x < E ? cnt[x] : 0;
     __syncthreads();
     if (tid == 0) {
+      if (p.dbg & 8) g_arrive = globaltimer_ns();
       __threadfence();
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
     }
-    for (int x = tid; x < G && !(p.dbg & 2); x += blockDim.x) {
-      if (ld_acquire_gpu(p.gflags + x) >= p.gepoch) continue;
-      const uint64_t ts = globaltimer_ns();
-      while (ld_acquire_gpu(p.gflags + x) < p.gepoch) {
-        if (globaltimer_ns() - ts > p.timeout_ns) {
-          if (p.err) atomicCAS(p.err, 0ull, 0x5400000ull | static_cast<unsigned>(x));
-          break;
+    auto wait_flags = [&](const unsigned long long* f, int n, unsigned long long code) {
+      for (int x = tid; x < n; x += blockDim.x) {
+        if (ld_acquire_gpu(f + x) >= p.gepoch) continue;
+        const uint64_t ts = globaltimer_ns();
+        while (ld_acquire_gpu(f + x) < p.gepoch) {
+          if (globaltimer_ns() - ts > p.timeout_ns) {
+            if (p.err) atomicCAS(p.err, 0ull, code | static_cast<unsigned>(x));
+            break;
+          }
         }
       }
-    }
+    };
+    const int Q = Ep / 4;
+    if (p.reduce && G <= static_cast<int>(blockDim.x) && Q <= G && !(p.dbg & 2)) {
+      // ---- column reducers: CTA q < Q owns experts [4q, 4q + 4): waits for every chunk,
+      // scans its column over the chunks (one int4 per thread) and publishes every
+      // chunk's exclusive prefix and the totals; the other CTAs read one prefix row.
+      int32_t* pfx = p.chunk_hist + kFdHistInts;  // [G][Ep]
+      int32_t* totg = pfx + kFdHistInts;          // [Ep]
+      if (c < Q) {
+        __shared__ int4 wsum[kFdWarps];
+        wait_flags(p.gflags, G, 0x5400000ull);
+        __syncthreads();
+        const int4 v = tid < G ? __ldcg(reinterpret_cast<const int4*>(p.chunk_hist) + static_cast<int64_t>(tid) * Q + c)
+                               : make_int4(0, 0, 0, 0);
+        int4 inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int ax = __shfl_up_sync(0xffffffffu, inc.x, o), ay = __shfl_up_sync(0xffffffffu, inc.y, o);
+          const int az = __shfl_up_sync(0xffffffffu, inc.z, o), aw = __shfl_up_sync(0xffffffffu, inc.w, o);
+          if (lane >= o) { inc.x += ax; inc.y += ay; inc.z += az; inc.w += aw; }
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        int4 below = make_int4(0, 0, 0, 0);
+        for (int ww = 0; ww < warp; ++ww) {
+          const int4 u = wsum[ww];
+          below.x += u.x; below.y += u.y; below.z += u.z; below.w += u.w;
+        }
+        if (tid < G) {
+          const int4 ex = make_int4(below.x + inc.x - v.x, below.y + inc.y - v.y, below.z + inc.z - v.z,
+                                    below.w + inc.w - v.w);
+          reinterpret_cast<int4*>(pfx)[static_cast<int64_t>(tid) * Q + c] = ex;
+          if (tid == G - 1)
+            reinterpret_cast<int4*>(totg)[c] = make_int4(ex.x + v.x, ex.y + v.y, ex.z + v.z, ex.w + v.w);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + kFdRedBase + c), "l"(p.gepoch)
+                       : "memory");
+        }
+      }
+      wait_flags(p.gflags + kFdRedBase, Q, 0x5600000ull);
+      __syncthreads();
+      if ((p.dbg & 8) && tid == 0) g_release = globaltimer_ns();
+      for (int x = tid; x < E; x += blockDim.x) {
+        const int32_t t = __ldcg(totg + x);
+        off[x] = __ldcg(pfx + static_cast<int64_t>(c) * Ep + x);
+        tot[x] = t;
+        cnt[x] = t;  // this rank's count row (tot becomes the expert bases below)
+      }
+    } else {
+    // ---- every CTA waits for every chunk and sums the columns itself
+    if (!(p.dbg & 2)) wait_flags(p.gflags, G, 0x5400000ull);
     __syncthreads();
+    if ((p.dbg & 8) && tid == 0) g_release = globaltimer_ns();
     // ---- totals and this chunk's offsets: thread = (4-expert quad, chunk group), one
     // 16-byte load per chunk, all chunk groups' loads independent
     {
@@ -774,6 +869,7 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
         off[x] = o;
         cnt[x] = t;  // this rank's count row (tot becomes the expert bases below)
       }
+    }
     }
     __syncthreads();
     block_exclusive_scan(tot, E);  // ends with __syncthreads
@@ -846,11 +942,89 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       p.counts_out[i] = (i / E == p.rank && (p.mode & 1)) ? cnt[i % E] : __ldcg(p.mat + i);
   }
 
-  // ---- scatter this CTA's tokens
-  uint32_t phases = ph1 << 1;  // buffer 1's barrier may have been used for the logits
+  stamp_all_mid = clock64();
+  if (dyn) {
+    // ---- dynamic scatter: publish this CTA's destination rows, then every warp takes
+    // (token, piece) tickets from the grid-wide counter until they run out, so SMs that
+    // drain their stores faster take more pieces.  A ticket's row load only needs the
+    // token; its stores wait for the owner CTA's "rows published" flag.
+    for (int i = tid; i < ent; i += blockDim.x)
+      if (pos_s[i] >= 0) p.dest_row[t0 * k + i] = off[idx_s[i]] + pos_s[i];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + kFdReadyBase + c), "l"(p.gepoch) : "memory");
+    }
+    uint32_t phases = 0;
+    const int64_t vpr = p.vec_per_row;
+    int b = 0;
+    while (cur < dyn_total) {
+      int64_t nxt = 0;
+      if (lane == 0) {
+        nxt = static_cast<int64_t>(atomicAdd(p.gflags + kFdTicket, 1ull));
+        if (nxt == dyn_total + static_cast<int64_t>(G) * nw - 1) p.gflags[kFdTicket] = 0;  // last draw of the launch
+      }
+      nxt = __shfl_sync(0xffffffffu, nxt, 0);
+      const int64_t t = cur / npieces;
+      const int64_t v0 = (cur % npieces) * kPiece;
+      const uint32_t bytes = piece_bytes(cur);
+      uint4* my_dst = nullptr;
+      int my_remote = 0;
+      if (lane < k) {
+        const unsigned long long* rf = p.gflags + kFdReadyBase + t / p.tpc;
+        if (ld_acquire_gpu(rf) < p.gepoch) {
+          const uint64_t ts = globaltimer_ns();
+          while (ld_acquire_gpu(rf) < p.gepoch)
+            if (globaltimer_ns() - ts > p.timeout_ns) {
+              if (p.err) atomicCAS(p.err, 0ull, 0x5500000ull | static_cast<unsigned>(t / p.tpc));
+              break;
+            }
+        }
+        const int e = __ldcg(p.idx + t * k + lane);
+        if (e >= 0 && e < E) {
+          const int64_t row = __ldcg(p.dest_row + t * k + lane);
+          if (row < p.max_recv) my_dst = static_cast<uint4*>(p.recv.p[e / epr]) + row * vpr + v0;
+          else if (p.err) atomicCAS(p.err, 0ull, 0x5000000ull | 0xFFFFFFull);
+          my_remote = (e / epr) != p.rank;
+        }
+      }
+      if (lane < k) sdst[warp][lane] = my_dst;
+      __syncwarp();
+      const unsigned remote = __ballot_sync(0xffffffffu, my_remote != 0 && my_dst != nullptr);
+      mbar_wait(&bars[kFdMaxNb * warp + b], (phases >> b) & 1);
+      phases ^= 1u << b;
+      uint8_t* buf = wbuf + b * buf_bytes;
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // buffer b ^ 1 free
+        if (nxt < dyn_total) issue_load(nxt, b ^ 1);
+        for (int j = 0; j < k; ++j)
+          if (sdst[warp][j] != nullptr && !((remote >> j) & 1))
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[warp][j]),
+                         "r"(smem_u32(buf)), "r"(bytes)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      for (int j = 0; j < k; ++j) {
+        if (!((remote >> j) & 1)) continue;
+        uint4* d = sdst[warp][j];
+        const uint4* sb = reinterpret_cast<const uint4*>(buf);
+        for (int v = lane; v < static_cast<int>(bytes / 16); v += 32) d[v] = sb[v];
+      }
+      __syncwarp();
+      cur = nxt;
+      b ^= 1;
+    }
+  } else {
+  // ---- scatter this CTA's tokens: task j of this warp is piece (warp + j * nw),
+  // buffer j % NB; the load of task j + NB - 1 goes out once task j - 1's stores
+  // have read their buffer, so NB - 1 loads are in flight under the stores
+  if (lane == 0)
+    for (int b = 1; b < NB - 1; ++b)
+      if (warp + b * nw < ntasks) issue_load(warp + b * nw, b);
+  uint32_t phases = 0;
   const int64_t vpr = p.vec_per_row;
-  int ti = warp;
-  for (int b = 0; ti < ntasks; ti += nw, b ^= 1) {
+  int b = 0;
+  for (int ti = warp; ti < ntasks; ti += nw, b = (b + 1 == NB) ? 0 : b + 1) {
     const int tt = static_cast<int>(ti / npieces);
     const int64_t v0 = (ti % npieces) * kPiece;
     const uint32_t bytes = piece_bytes(ti);
@@ -870,12 +1044,10 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
     if (lane < k) sdst[warp][lane] = my_dst;
     __syncwarp();
     const unsigned remote = __ballot_sync(0xffffffffu, my_remote != 0 && my_dst != nullptr);
-    mbar_wait(&bars[2 * warp + b], (phases >> b) & 1);
+    mbar_wait(&bars[kFdMaxNb * warp + b], (phases >> b) & 1);
     phases ^= 1u << b;
-    uint8_t* buf = bufs + (2 * warp + b) * kFdBuf;
+    uint8_t* buf = wbuf + b * buf_bytes;
     if (lane == 0) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      if (ti + nw < ntasks) issue_load(ti + nw, b ^ 1);
       for (int j = 0; j < k; ++j)
         if (sdst[warp][j] != nullptr && !((remote >> j) & 1))
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[warp][j]),
@@ -889,9 +1061,21 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       const uint4* sb = reinterpret_cast<const uint4*>(buf);
       for (int v = lane; v < static_cast<int>(bytes / 16); v += 32) d[v] = sb[v];
     }
-    __syncwarp();
+    __syncwarp();  // the lanes' remote stores have read the buffer
+    if (lane == 0 && ti + (NB - 1) * nw < ntasks) {
+      // refill buffer (b + NB - 1) % NB, last used by the previous task: its stores
+      // are the second most recent bulk group
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      issue_load(ti + (NB - 1) * nw, b == 0 ? NB - 1 : b - 1);
+    }
   }
+  }  // static scatter
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores performed
+  if ((p.dbg & 8) && tid == 0)
+    printf("fdsm cta %d sm %u pre_layout %lld scatter %lld clk t %llu %llu %llu %llu\n", c, smid_u32(),
+           stamp_all_mid - stamp_all0, clock64() - stamp_all_mid, static_cast<unsigned long long>(g_start),
+           static_cast<unsigned long long>(g_arrive), static_cast<unsigned long long>(g_release),
+           static_cast<unsigned long long>(globaltimer_ns()));
   if (p.world > 1) {
     __syncthreads();
     if (tid == 0) {
@@ -1146,8 +1330,8 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = flag_bufs.find(dev);
     if (it == flag_bufs.end()) {
-      TF_CUDA_TRY(cudaMalloc(&flags, 1024 * sizeof(unsigned long long)));
-      TF_CUDA_TRY(cudaMemset(flags, 0, 1024 * sizeof(unsigned long long)));
+      TF_CUDA_TRY(cudaMalloc(&flags, kFdFlagWords * sizeof(unsigned long long)));
+      TF_CUDA_TRY(cudaMemset(flags, 0, kFdFlagWords * sizeof(unsigned long long)));
       flag_bufs[dev] = flags;
     } else {
       flags = it->second;
@@ -1155,7 +1339,13 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     auto key = std::make_pair(dev, fn);
     auto oi = occ.find(key);
     if (oi == occ.end()) {
-      TF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+      cudaFuncAttributes fa{};
+      TF_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+      int optin = 0;
+      TF_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      const int dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
+      if (dyn_max < static_cast<int>(smem)) return TF_OK;  // multi-kernel path
+      TF_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
       TF_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kFdWarps, smem));
       occ[key] = per_sm;
     } else {
@@ -1180,7 +1370,7 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     static std::map<int, void*> hist_bufs;
     auto it = hist_bufs.find(dev);
     if (it == hist_bufs.end()) {
-      TF_CUDA_TRY(cudaMalloc(&hist, static_cast<size_t>(kFdDoneSlot) * fd_stride(1024) * 4));
+      TF_CUDA_TRY(cudaMalloc(&hist, (2 * static_cast<size_t>(kFdHistInts) + 1024) * 4));
       hist_bufs[dev] = hist;
     } else {
       hist = it->second;
@@ -1192,6 +1382,21 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     return e ? atoi(e) : 0;
   }();
   p.dbg = dbg;
+  static const int nb = [] {
+    const char* e = getenv("TF_MOE_FD_NB");
+    return e ? atoi(e) : 2;
+  }();
+  p.nb = nb;
+  static const int dyn = [] {
+    const char* e = getenv("TF_MOE_FD_DYN");
+    return e ? atoi(e) : 1;
+  }();
+  p.dyn = dyn;
+  static const int reduce = [] {  // measured neutral (profiles/r02_moe_dispatch_s3.txt): opt-in
+    const char* e = getenv("TF_MOE_FD_REDUCE");
+    return e ? atoi(e) : 0;
+  }();
+  p.reduce = reduce;
   void* args[] = {&p};
   TF_CUDA_TRY(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(G)), dim3(32 * kFdWarps), args, smem, s));
   *launched = true;
