@@ -592,6 +592,7 @@ struct FusedDispatch {
   int nb;                               // row piece buffers per warp (2..4), sharing the warp's 2 * kFdBuf bytes
   int dyn;                              // 1: pieces handed out by a grid-wide ticket counter (PRE+MAIN launches)
   int reduce;                           // 1: column-reducer CTAs publish the chunk prefixes (else every CTA sums)
+  int lhist;                            // 1: every CTA counts every entry of p.idx (no histogram exchange)
 };
 
 __device__ __forceinline__ uint64_t ld_acquire_gpu(const unsigned long long* p) {
@@ -763,14 +764,6 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       __syncthreads();
     }
     __syncthreads();
-    // ---- publish the chunk histogram
-    for (int x = tid; x < Ep; x += blockDim.x) p.chunk_hist[static_cast<int64_t>(c) * Ep + x] = x < E ? cnt[x] : 0;
-    __syncthreads();
-    if (tid == 0) {
-      if (p.dbg & 8) g_arrive = globaltimer_ns();
-      __threadfence();
-      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
-    }
     auto wait_flags = [&](const unsigned long long* f, int n, unsigned long long code) {
       for (int x = tid; x < n; x += blockDim.x) {
         if (ld_acquire_gpu(f + x) >= p.gepoch) continue;
@@ -783,6 +776,57 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
         }
       }
     };
+    if (p.lhist) {
+      // ---- every CTA counts every entry itself (the routing is in p.idx: the input, or
+      // published by each CTA's routing behind its arrival flag): totals, and the
+      // entries of the chunks below this one -- no histogram exchange
+      if (VPL > 0) {
+        if (tid == 0) {
+          if (p.dbg & 8) g_arrive = globaltimer_ns();
+          __threadfence();
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
+        }
+        if (!(p.dbg & 2)) wait_flags(p.gflags, G, 0x5400000ull);
+        __syncthreads();
+      }
+      int32_t* hrest = wc;  // entries of this and higher chunks
+      int32_t* hbelow = wc + E;
+      for (int x = tid; x < 2 * E; x += blockDim.x) wc[x] = 0;
+      __syncthreads();
+      const int64_t nent = p.tokens * k, below_end = t0 * k;
+      auto count = [&](int e, int64_t i) {  // one shared-memory atomic per entry
+        if (e >= 0 && e < E) atomicAdd(i < below_end ? &hbelow[e] : &hrest[e], 1);
+      };
+      if ((reinterpret_cast<uintptr_t>(p.idx) & 15) == 0) {
+        const int4* idx4 = reinterpret_cast<const int4*>(p.idx);
+        for (int64_t q = tid; q < nent / 4; q += blockDim.x) {
+          const int4 v = __ldcg(idx4 + q);
+          count(v.x, 4 * q);
+          count(v.y, 4 * q + 1);
+          count(v.z, 4 * q + 2);
+          count(v.w, 4 * q + 3);
+        }
+        for (int64_t i = (nent / 4) * 4 + tid; i < nent; i += blockDim.x) count(__ldcg(p.idx + i), i);
+      } else {
+        for (int64_t i = tid; i < nent; i += blockDim.x) count(__ldcg(p.idx + i), i);
+      }
+      __syncthreads();
+      if ((p.dbg & 8) && tid == 0) g_release = globaltimer_ns();
+      for (int x = tid; x < E; x += blockDim.x) {
+        const int32_t t = hrest[x] + hbelow[x];
+        tot[x] = t;
+        off[x] = hbelow[x];
+        cnt[x] = t;  // this rank's count row (tot becomes the expert bases below)
+      }
+    } else {
+    // ---- publish the chunk histogram
+    for (int x = tid; x < Ep; x += blockDim.x) p.chunk_hist[static_cast<int64_t>(c) * Ep + x] = x < E ? cnt[x] : 0;
+    __syncthreads();
+    if (tid == 0) {
+      if (p.dbg & 8) g_arrive = globaltimer_ns();
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.gflags + c), "l"(p.gepoch) : "memory");
+    }
     const int Q = Ep / 4;
     if (p.reduce && G <= static_cast<int>(blockDim.x) && Q <= G && !(p.dbg & 2)) {
       // ---- column reducers: CTA q < Q owns experts [4q, 4q + 4): waits for every chunk,
@@ -871,6 +915,7 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       }
     }
     }
+    }  // histogram exchange
     __syncthreads();
     block_exclusive_scan(tot, E);  // ends with __syncthreads
     if (c == 0)
@@ -1397,6 +1442,14 @@ int launch_fused_dispatch(FusedDispatch p, cudaStream_t s, bool* launched) {
     return e ? atoi(e) : 0;
   }();
   p.reduce = reduce;
+  // local counting: measured 104.4 vs 109.5 us with the routing given, 117.8-118.8 vs
+  // 115.6-116.7 us when the launch routes (profiles/r02_moe_dispatch_s3.txt), so by
+  // default only for given routing (TF_MOE_FD_LHIST: 0 never, 1 given routing, 2 always)
+  static const int lhist = [] {
+    const char* e = getenv("TF_MOE_FD_LHIST");
+    return e ? atoi(e) : 1;
+  }();
+  p.lhist = lhist == 2 || (lhist == 1 && !p.logits);
   void* args[] = {&p};
   TF_CUDA_TRY(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(G)), dim3(32 * kFdWarps), args, smem, s));
   *launched = true;
