@@ -314,10 +314,23 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
             if i >= warmup:
                 ev[i - warmup][2].record(stream)
         torch.cuda.synchronize()
+        # the same dispatch with the routing given (ExpertParallelMoE.dispatch(x, topk_idx),
+        # the reference's split of routing and dispatch): no top-k, no grid-wide barrier
+        evg = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        idx_given = idx.clone()
+        for i in range(warmup + steps):
+            if i >= warmup:
+                flush.zero_()
+                evg[i - warmup][0].record(stream)
+            ep.dispatch(x, idx_given)
+            if i >= warmup:
+                evg[i - warmup][1].record(stream)
+        torch.cuda.synchronize()
     team.check()
     d_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
     c_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
-    d_ms, c_ms = max_over_ranks([d_ms, c_ms], dev, distributed)
+    g_ms = sum(e[0].elapsed_time(e[1]) for e in evg) / steps
+    d_ms, c_ms, g_ms = max_over_ranks([d_ms, c_ms, g_ms], dev, distributed)
     rows = MOE_T * MOE_K
     row_b = MOE_H * 2
     moved = rows * row_b  # token rows delivered by dispatch (and pulled back by combine), per rank
@@ -328,6 +341,7 @@ def bench_moe(team, dev, world, rank, steps, warmup, flush, stream, distributed,
         "workload": f"EP={world}: {MOE_E} experts, top-{MOE_K}, hidden {MOE_H}, {MOE_T} tokens/rank, "
                     "bf16, routing from N(0,1) logits (device top-k); expert compute excluded",
         "dispatch_ms": round(d_ms, 4), "combine_ms": round(c_ms, 4),
+        "dispatch_given_routing_ms": round(g_ms, 4),
         "gbps": round(world * 2 * moved / ((d_ms + c_ms) * 1e-3) / 1e9, 2),
         "unit": "GB/s (routed token bytes moved by dispatch + combine, all ranks)",
         "nvlink_bytes_per_rank_per_phase": remote,
