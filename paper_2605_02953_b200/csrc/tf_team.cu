@@ -406,6 +406,14 @@ int tf_team_check(tf_team* t) {
         return fail(TF_ERR_TIMEOUT, "device spin timed out on PE " + std::to_string(p) +
                                         ": scoreboard task slot " + std::to_string(w & 0xFFFFFF) +
                                         " (task = slot / max_tiles_per_op)");
+      if (kind == 5 && (w & 0xFFFFFF) == 0xFFFFFF)
+        return fail(TF_ERR_INVALID, "MoE receive buffer overflow on PE " + std::to_string(p) +
+                                        ": a destination row >= max_recv (raise max_recv / capacity_factor); "
+                                        "rows past it were not delivered");
+      if (kind == 5 && ((w >> 20) & 0xF) == 3)
+        return fail(TF_ERR_INVALID, "MoE routing index out of range on PE " + std::to_string(p) +
+                                        " at (token, slot) entry " + std::to_string(w & 0xFFFFF) +
+                                        " of a CTA's slice (expert ids must be in [-1, n_experts))");
       const char* what = kind == 1 ? "AllGather chunk flag" : kind == 2 ? "signal wait"
                        : kind == 3 ? "barrier_all" : kind == 4 ? "reduce-scatter tile counter"
                        : kind == 5 ? "moe dispatch flag" : "device wait";

@@ -15,6 +15,7 @@ and the reference's own MoE operator is kept as a drop-in:
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 import torch
@@ -60,14 +61,27 @@ class ExpertParallelMoE:
     for local teams (all ranks in this process; lists indexed by rank)."""
 
     def __init__(self, team: Team, n_experts: int, hidden: int, k: int, max_tokens: int,
-                 max_recv: int | None = None):
+                 max_recv: int | None = None, capacity_factor: float | None = None):
+        """Receive capacity per rank: `max_recv` rows if given, else
+        ceil(capacity_factor * max_tokens * k) rows (balanced routing delivers
+        max_tokens * k rows to each rank on average), else the worst case
+        max_tokens * k * world (every token of every source to one rank), which can
+        never overflow.  A dispatch that would write past the capacity skips those
+        rows and `team.check()` raises (TF_ERR_INVALID, "receive buffer overflow")."""
         if n_experts % team.world:
             raise ValueError("n_experts must divide across ranks")
         if hidden % 8:
             raise ValueError("hidden must be a multiple of 8")
+        if max_recv is not None and capacity_factor is not None:
+            raise ValueError("give max_recv or capacity_factor, not both")
+        if capacity_factor is not None and not capacity_factor > 0:
+            raise ValueError("capacity_factor must be > 0")
         self.team, self.E, self.H, self.k = team, n_experts, hidden, k
         self.max_tokens = max_tokens
-        self.max_recv = max_recv if max_recv is not None else max_tokens * k * team.world
+        if max_recv is None:
+            worst = max_tokens * k * team.world
+            max_recv = worst if capacity_factor is None else min(worst, math.ceil(capacity_factor * max_tokens * k))
+        self.max_recv = int(max_recv)
         self.state = {}
         for r in team.local_ranks():
             dev = team.devices[r]

@@ -103,6 +103,41 @@ def test_dispatch_combine_vs_oracle(world, e, k, t, h):
         assert OC.compare(outs[r].float().cpu().numpy(), want[r]) <= TOL_BF16
 
 
+def test_capacity_factor_exact_and_overflow():
+    """capacity_factor sizes the receive buffer below the worst case: a routing that
+    fits stays bit-exact; one that does not (every token of both sources to rank 0's
+    experts) is reported by team.check() as a receive overflow, not a timeout."""
+    M = _m()
+    world, e, k, t, h = 2, 16, 2, 64, 64
+    rng = np.random.default_rng(7)
+    team = _team(world)
+    xs = [torch.from_numpy(rng.standard_normal((t, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+          for _ in range(world)]
+    skew = [torch.tensor([[0, 1]] * t, dtype=torch.int32).cuda() for _ in range(world)]  # 2*t*k rows to rank 0
+    ok = M.ExpertParallelMoE(team, e, h, k, max_tokens=t, capacity_factor=2.0)
+    assert ok.max_recv == 2 * t * k
+    recv = ok.dispatch(xs, skew)
+    torch.cuda.synchronize()
+    team.check()
+    counts, want_recv, slot_row = OM.dispatch_layout([i.cpu().numpy() for i in skew], e, world)
+    x_np = [x.float().cpu().numpy() for x in xs]
+    for r in range(world):
+        n = ok.recv_rows(r)
+        assert n == len(want_recv[r])
+        want = np.stack([x_np[s][tok] for s, tok, _ in want_recv[r]]) if n else np.zeros((0, h))
+        assert np.array_equal(recv[r][:n].float().cpu().numpy(), want)
+        assert np.array_equal(ok.dest_rows(r).cpu().numpy(), slot_row[r])
+    small = M.ExpertParallelMoE(team, e, h, k, max_tokens=t, capacity_factor=1.0)
+    assert small.max_recv == t * k
+    small.dispatch(xs, skew)
+    torch.cuda.synchronize()
+    with pytest.raises(Exception, match="overflow"):
+        team.check()
+    team.check()  # the error word was cleared
+    with pytest.raises(ValueError):
+        M.ExpertParallelMoE(team, e, h, k, max_tokens=t, max_recv=8, capacity_factor=1.0)
+
+
 @pytest.mark.parametrize("world,e,k,t,h", [(1, 256, 8, 4096, 256), (1, 60, 4, 300, 64), (2, 8, 2, 37, 64),
                                            (8, 256, 8, 200, 128), (1, 1024, 16, 33, 64),
                                            (1, 64, 8, 40000, 16)])
