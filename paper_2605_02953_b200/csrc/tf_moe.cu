@@ -799,7 +799,11 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
       };
       if ((reinterpret_cast<uintptr_t>(p.idx) & 15) == 0) {
         const int4* idx4 = reinterpret_cast<const int4*>(p.idx);
-        for (int64_t q = tid; q < nent / 4; q += blockDim.x) {
+        // every CTA reads the same 16-byte vectors: start each CTA at its own slice so
+        // the 148 readers of a line are spread in time (no L2 hot spot)
+        const int64_t n4 = nent / 4, rot = n4 * c / G;
+        for (int64_t qq = tid; qq < n4; qq += blockDim.x) {
+          const int64_t q = qq + rot < n4 ? qq + rot : qq + rot - n4;
           const int4 v = __ldcg(idx4 + q);
           count(v.x, 4 * q);
           count(v.y, 4 * q + 1);
@@ -894,7 +898,8 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
         int4 t = make_int4(0, 0, 0, 0), o = make_int4(0, 0, 0, 0);
         const int4* col = reinterpret_cast<const int4*>(p.chunk_hist) + q;
 #pragma unroll 16
-        for (int cc = g; cc < G; cc += groups) {
+        for (int c0 = g; c0 < G; c0 += groups) {
+          const int cc = c0 + c < G ? c0 + c : c0 + c - G;  // rotated start: spread the readers of a row
           const int4 v = __ldcg(col + static_cast<int64_t>(cc) * quads);
           t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
           if (cc < c) { o.x += v.x; o.y += v.y; o.z += v.z; o.w += v.w; }

@@ -390,6 +390,9 @@ int tf_team_device(tf_team* t, int pe, int* device) {
 
 int tf_team_check(tf_team* t) {
   if (!t) return fail(TF_ERR_INVALID, "NULL team");
+  // read and clear every owned PE's error word, then report the first one set
+  int first = -1;
+  unsigned long long first_w = 0;
   for (int p = 0; p < t->world; ++p) {
     if (t->ipc && p != t->my_rank) continue;
     tf::DeviceGuard g(t->pes[p].device);
@@ -398,6 +401,13 @@ int tf_team_check(tf_team* t) {
     if (w) {
       unsigned long long z = 0;
       cudaMemcpy(t->err_word(p), &z, sizeof(z), cudaMemcpyHostToDevice);
+      if (first < 0) { first = p; first_w = w; }
+    }
+  }
+  if (first >= 0) {
+    const int p = first;
+    const unsigned long long w = first_w;
+    {
       const unsigned kind = static_cast<unsigned>(w >> 24);
       if (kind == 9)
         return fail(TF_ERR_PROTOCOL, "double release of scoreboard slot " + std::to_string(w & 0xFFFFFF) +
