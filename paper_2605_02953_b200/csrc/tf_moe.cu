@@ -802,13 +802,23 @@ __global__ void __launch_bounds__(32 * kFdWarps, 1) dispatch_fused_kernel(const 
         // every CTA reads the same 16-byte vectors: start each CTA at its own slice so
         // the 148 readers of a line are spread in time (no L2 hot spot)
         const int64_t n4 = nent / 4, rot = n4 * c / G;
-        for (int64_t qq = tid; qq < n4; qq += blockDim.x) {
-          const int64_t q = qq + rot < n4 ? qq + rot : qq + rot - n4;
-          const int4 v = __ldcg(idx4 + q);
-          count(v.x, 4 * q);
-          count(v.y, 4 * q + 1);
-          count(v.z, 4 * q + 2);
-          count(v.w, 4 * q + 3);
+        constexpr int kBatch = 8;  // independent 16-byte loads in flight per thread before counting
+        for (int64_t base = tid; base < n4; base += kBatch * blockDim.x) {
+          int4 v[kBatch];
+          int64_t q[kBatch];
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            const int64_t qq = base + static_cast<int64_t>(u) * blockDim.x;
+            q[u] = qq + rot < n4 ? qq + rot : qq + rot - n4;
+            v[u] = qq < n4 ? __ldcg(idx4 + q[u]) : make_int4(-1, -1, -1, -1);
+          }
+#pragma unroll
+          for (int u = 0; u < kBatch; ++u) {
+            count(v[u].x, 4 * q[u]);
+            count(v[u].y, 4 * q[u] + 1);
+            count(v[u].z, 4 * q[u] + 2);
+            count(v[u].w, 4 * q[u] + 3);
+          }
         }
         for (int64_t i = (nent / 4) * 4 + tid; i < nent; i += blockDim.x) count(__ldcg(p.idx + i), i);
       } else {
