@@ -77,6 +77,9 @@ struct AttnParams {
 #define TF_ATTN_SPLIT_ROWS 1  // 2 measured slower: 3.89 vs 3.47 ms per rank (same box)
 #endif
 constexpr int kRowSplit = TF_ATTN_SPLIT_ROWS;
+#if defined(TF_ATTN_EARLY_S) && TF_ATTN_EARLY_S && TF_ATTN_SPLIT_ROWS == 2
+#error "TF_ATTN_EARLY_S needs the four-warp softmax (TF_ATTN_SPLIT_ROWS=1)"
+#endif
 struct AttnSmem {
   static constexpr int kQ = 2 * kHalf;        // one Q tile, 32 KB
   static constexpr int kSlot = 2 * kHalf;     // one K or V tile (128 keys x 128 dims), 32 KB
@@ -188,6 +191,15 @@ __device__ __forceinline__ float ex2(float x) {
 #define SM_WAIT mbar_wait
 #else
 #define SM_WAIT mbar_wait_spin
+#endif
+// TF_ATTN_EARLY_S=1: P_t(j) lives in the upper 64 columns of S_t, so QK^T for keys
+// 0-63 of tile j+1 (N=64, into the lower 64 columns) is issued as soon as the softmax
+// has read S_t(j) into registers ("S free"), overlapping the exponentials; only keys
+// 64-127 of S_t(j+1) still wait behind PV_t(j) on the in-order tensor pipe
+// Measured slower (session 3, one box): 3.88-3.90 vs 3.54-3.62 ms per rank -- the two
+// N=64 halves read Q from shared memory twice, and QK^T is shared-memory bound here.
+#ifndef TF_ATTN_EARLY_S
+#define TF_ATTN_EARLY_S 0
 #endif
 #ifndef TF_ATTN_STAGGER
 #define TF_ATTN_STAGGER 0  // per-CTA rotation inside a chunk: measured neutral (no L2 hot spot)
@@ -354,6 +366,8 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
   uint64_t* o_ready = bars + 15;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
   uint64_t* p_half = bars + 18;    // [2] first 64 keys of P_t written
+  uint64_t* s_free = bars + 20;    // [2] S_t(j) read into the softmax registers (TF_ATTN_EARLY_S)
+  constexpr uint32_t kPCol = TF_ATTN_EARLY_S ? 64 : 0;  // P_t's first column inside S_t
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q0 = blockIdx.x * 2 * kQT;
@@ -374,6 +388,7 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
       mbar_init(&p_full[i], 4);
       mbar_init(&p_half[i], 4 * kRowSplit);  // split: half-1 warps also report "O rescaled"
       mbar_init(&o_ready[i], 1);
+      mbar_init(&s_free[i], 4);
     }
     fence_barrier_init();
   }
@@ -452,6 +467,18 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
         }
         umma_commit_elect(&s_full[t]);
       };
+      // keys [64 hf, 64 hf + 64) of S_t into columns [64 hf, +64) (no commit)
+      constexpr uint32_t idesc_s64 = umma_idesc_bf16(kQT, kKT / 2);
+      auto issue_s_half = [&](int t, int sl, int hf) {
+        const uint32_t qa = q_lo0 + t * (S::kQ >> 4);
+        const uint32_t kb = (ring_lo + sl * (S::kSlot >> 4) + hf * ((64 * 128) >> 4)) | kLoK;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (kHalf >> 4) + (kk & 3) * 2;
+          umma_ss_elect(tmem + t * 128 + hf * 64, mk(qa + off), mk(kb + off), idesc_s64, kk != 0);
+        }
+      };
+      (void)issue_s_half;
       MMA_WAIT(&r_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < nq; ++t) issue_s(t, 0);
@@ -465,7 +492,14 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
         ATTN_STAMP(j, 8);
         const uint32_t vb = (ring_lo + vs * (S::kSlot >> 4)) | kLoV;
         for (int t = 0; t < nq; ++t) {
-          const uint32_t pa = tmem + t * 128, od = tmem + 256 + t * 128;
+          const uint32_t pa = tmem + t * 128 + kPCol, od = tmem + 256 + t * 128;
+#if TF_ATTN_EARLY_S
+          if (j + 1 < n) {  // S_t(j+1) keys 0-63 while the softmax works on S_t(j)
+            MMA_WAIT(&s_free[t], j & 1);
+            tc_fence_after();
+            issue_s_half(t, ks, 0);
+          }
+#endif
           // keys 0-63 of P_t(j) as soon as the softmax has them, keys 64-127 after
           if (t == 0) ATTN_STAMP(j, 16);
           MMA_WAIT(&p_half[t], j & 1);
@@ -481,8 +515,17 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
           for (int kk = kKT / 32; kk < kKT / 16; ++kk)
             umma_ts_elect(od, pa + kk * 8, mk(vb + kk * (2048 >> 4)), idesc_pv, 1);
           ATTN_STAMP(j, 6 + t);
+#if TF_ATTN_EARLY_S
+          if (j + 1 < n) {
+            issue_s_half(t, ks, 1);  // over P_t(j): the pipe has read it for PV_t(j)
+            umma_commit_elect(&s_full[t]);
+          } else {
+            umma_commit_elect(&o_ready[t]);
+          }
+#else
           if (j + 1 < n) issue_s(t, ks);
           else umma_commit_elect(&o_ready[t]);
+#endif
         }
         umma_commit_elect(&r_empty[vs]);
         if (j + 1 < n) umma_commit_elect(&r_empty[ks]);
@@ -618,6 +661,11 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, sv[c]);
         tmem_ld_wait();
+#if TF_ATTN_EARLY_S
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[t]);  // the MMA may overwrite S_t's lower columns
+#endif
         float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -675,7 +723,7 @@ __global__ void __launch_bounds__(kAttnThreads2, 1)
               sv[hk][cc * 16 + i] = pack_bf16x2(p0, p1);
             }
           }
-          tmem_st_32x32b_x32(t_s + hk * 32, sv[hk]);
+          tmem_st_32x32b_x32(t_s + kPCol + hk * 32, sv[hk]);
 #if TF_ATTN_SPLIT_P
           tmem_st_wait();
           tc_fence_before();
