@@ -58,8 +58,8 @@ __device__ __forceinline__ float key2f(uint32_t k) {
 // stable sort by (-logit, expert id).
 // Lane j < k returns slot j's (expert, weight) of the token whose logits are `row`.
 template <int VPL>  // logits per lane (E <= 32 * VPL)
-__device__ __forceinline__ void topk_warp(const float* __restrict__ row, int E, int k, int lane,
-                                          int& out_idx, float& out_w) {
+__device__ __forceinline__ void topk_warp_scan(const float* __restrict__ row, int E, int k, int lane,
+                                               int& out_idx, float& out_w) {
   uint32_t key[VPL];
 #pragma unroll
   for (int c = 0; c < VPL; ++c) {  // coalesced: lane + 32c
@@ -94,6 +94,62 @@ __device__ __forceinline__ void topk_warp(const float* __restrict__ row, int E, 
   }
   out_idx = my_idx;
   out_w = my_val / z;
+}
+
+// Same picks with each lane's keys pre-sorted (odd-even transposition, stable: equal
+// keys keep the lower expert id first), so a round is one max reduction, a ballot of
+// the lanes whose head holds it (a second reduction only on a cross-lane tie) and a
+// register shift in the winning lane -- instead of two reductions and a rescan.
+template <int VPL>
+__device__ __forceinline__ void topk_warp_sorted(const float* __restrict__ row, int E, int k, int lane,
+                                                 int& out_idx, float& out_w) {
+  uint32_t key[VPL], id[VPL];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {  // coalesced: lane + 32c
+    const int e = lane + 32 * c;
+    key[c] = e < E ? f2key(row[e]) : 0u;
+    id[c] = static_cast<uint32_t>(e);
+  }
+#pragma unroll
+  for (int rnd = 0; rnd < VPL; ++rnd)
+#pragma unroll
+    for (int a = rnd & 1; a + 1 < VPL; a += 2) {
+      const bool sw = key[a + 1] > key[a];  // strict: stable
+      const uint32_t k0 = sw ? key[a + 1] : key[a], k1 = sw ? key[a] : key[a + 1];
+      const uint32_t i0 = sw ? id[a + 1] : id[a], i1 = sw ? id[a] : id[a + 1];
+      key[a] = k0; key[a + 1] = k1; id[a] = i0; id[a + 1] = i1;
+    }
+  float sel0 = 0.f, z = 0.f, my_val = 0.f;
+  int my_idx = 0;
+  for (int r = 0; r < k; ++r) {
+    const uint32_t m = __reduce_max_sync(0xffffffffu, key[0]);
+    const unsigned hold = __ballot_sync(0xffffffffu, key[0] == m);
+    uint32_t wi;
+    if (__popc(hold) == 1) wi = __shfl_sync(0xffffffffu, id[0], __ffs(hold) - 1);
+    else wi = __reduce_min_sync(0xffffffffu, key[0] == m ? id[0] : 0xFFFFFFFFu);
+    if ((wi & 31) == static_cast<uint32_t>(lane)) {  // pop the head
+#pragma unroll
+      for (int c = 0; c + 1 < VPL; ++c) { key[c] = key[c + 1]; id[c] = id[c + 1]; }
+      key[VPL - 1] = 0u;
+    }
+    const float best = key2f(m);
+    if (r == 0) sel0 = best;
+    const float ez = __expf(best - sel0);
+    z += ez;
+    if (lane == r) { my_val = ez; my_idx = static_cast<int>(wi); }
+  }
+  out_idx = my_idx;
+  out_w = my_val / z;
+}
+
+#ifndef TF_MOE_TOPK_SORTED
+#define TF_MOE_TOPK_SORTED 1
+#endif
+template <int VPL>
+__device__ __forceinline__ void topk_warp(const float* __restrict__ row, int E, int k, int lane,
+                                          int& out_idx, float& out_w) {
+  if constexpr (TF_MOE_TOPK_SORTED && VPL <= 8) topk_warp_sorted<VPL>(row, E, k, lane, out_idx, out_w);
+  else topk_warp_scan<VPL>(row, E, k, lane, out_idx, out_w);
 }
 
 template <int VPL>
