@@ -946,8 +946,15 @@ def main_ours(args):
         team = Team.from_process_group(heap_bytes=heap, signal_slots=4096)
     else:
         team = Team(1, [dev], heap_bytes=heap, signal_slots=4096)
-    ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=args.group_m)
+    # ranks sharing one GPU (functional test mode): each rank's persistent GEMM takes its
+    # share of the SMs, so every rank's kernels are co-resident and their flags can move
+    gemm_sms = 0
+    if shared_gpus:
+        per_gpu = -(-world // torch.cuda.device_count())
+        gemm_sms = max(2, (torch.cuda.get_device_properties(dev).multi_processor_count // per_gpu - 8) & ~1)
+    ag = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, group_m=args.group_m, num_gemm_sms=gemm_sms)
     rs = K.GemmReduceScatter(team, m, f_tp, HIDDEN, block_n=256, group_m=args.group_m, num_comm_sms=8,
+                             num_gemm_sms=gemm_sms,
                              fuse_scatter=True, reduce_order="ascending")
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -1022,7 +1029,7 @@ def main_ours(args):
     # pulls above): same flush/event protocol, reported beside the main line
     ag_sm = None
     try:
-        ag_pull = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, num_comm_sms=16)
+        ag_pull = K.AllGatherGemm(team, m, HIDDEN, f_tp, block_n=256, num_comm_sms=16, num_gemm_sms=gemm_sms)
         h2 = torch.empty_like(h)
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -1187,7 +1194,12 @@ def main_ours(args):
                "one_thread": cpu_sample_1thread(tp)}
 
     moe = None
-    if not args.no_moe:
+    if not args.no_moe and shared_gpus:
+        # the fused dispatch keeps one CTA per SM co-resident per rank (grid-wide waits):
+        # two ranks' launches cannot share one GPU at this size (tests/test_gpu_ipc.py covers
+        # the protocol with ranks sharing a GPU at sizes whose grids fit together)
+        moe = {"skipped": "ranks share a GPU: the fused dispatch grid needs every SM per rank"}
+    elif not args.no_moe:
         moe = bench_moe(team, dev, world, rank, args.steps, args.warmup, flush, stream,
                         distributed, peaks)
 
