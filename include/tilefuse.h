@@ -90,7 +90,10 @@ int tf_team_open_peers(tf_team* t, const void* blobs, size_t blob_len);
 int tf_team_destroy(tf_team* t);
 int tf_team_world(tf_team* t, int* world);
 int tf_team_device(tf_team* t, int pe, int* device);
-/* Reads and clears the device error word; TF_ERR_TIMEOUT if a spin timed out. */
+/* Reads and clears the device error word of every PE this process owns and reports
+ * the first one set: TF_ERR_TIMEOUT if a spin timed out, TF_ERR_PROTOCOL for a double
+ * scoreboard release, TF_ERR_INVALID for a MoE receive-buffer overflow (a destination
+ * row >= max_recv; those rows were not written) or an expert id outside [-1, E). */
 int tf_team_check(tf_team* t);
 
 /* alloc (shmem.py:109-121): identical offset on every PE, bump allocator. */
